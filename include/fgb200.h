@@ -1,0 +1,170 @@
+/*
+ * fgb200.h -- C ABI of the B200-native fastgabor hot path (libfgb200.so).
+ *
+ * Plain C types only (no CUDA / torch types): device buffers are passed as
+ * `void*` device pointers, CUDA streams as `void*` (a cudaStream_t, NULL =
+ * legacy default stream).  Every call returns FGB_OK (0) or a negative status;
+ * fgb_last_error() returns a thread-local message for the last failure.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/fastgabor):
+ *
+ *   fgb_bank            compute_bank          bank.py:90-129   (reuse = 1)
+ *                       compute_bank_noreuse  bank.py:132-157  (reuse = 0)
+ *   fgb_filter          gabor_filter          gabor.py:172-176
+ *   fgb_horizontal_stage horizontal_stage     gabor.py:107-132
+ *   fgb_vertical_stage  vertical_stage        gabor.py:167-169
+ *                       vertical_stage_conjugate bank.py:68-74 (conjugate = 1)
+ *   fgb_sdft            sdft_full             sdft.py:178-213
+ *   fgb_sdft_bin        sdft_bin              sdft.py:169-175
+ *   fgb_sdft_horizontal sdft_horizontal       sdft.py:134-150
+ *   fgb_iir_coeffs      make_coeffs           gaussian.py:164-185
+ *   fgb_sampled_gaussian sampled_gaussian     gaussian.py:188-195
+ *   fgb_pad_radius      pad_radius            gaussian.py:198-212
+ *
+ * The *_host variants take HOST buffers and do the host<->device copies
+ * (through pinned staging) inside the call: they are what the reference-side
+ * binding calls.
+ *
+ * Data layout in HBM
+ *   image  : real, row-major [batch][height][pitch] (pitch in elements >= width)
+ *   output : interleaved complex (float2 / double2), dense [batch][entry][height][width]
+ *            bank entries in reference order (frequency-major, then k = 0..N-1,
+ *            bank.py:121-128); SDFT bins in u-major order (bin = u*my + v).
+ */
+#ifndef FGB200_H
+#define FGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FGB_OK 0
+#define FGB_EINVAL (-1)        /* bad parameter (reference raises ValueError)   */
+#define FGB_ECUDA (-2)         /* CUDA runtime error                            */
+#define FGB_ENOMEM (-3)        /* device / pinned allocation failed             */
+#define FGB_EUNSUPPORTED (-4)  /* smoother kind not valid here (TypeError)      */
+
+#define FGB_F32 0
+#define FGB_F64 1
+
+#define FGB_SMOOTH_FIR 0  /* ExactFIR(radius)   gaussian.py:41-49 */
+#define FGB_SMOOTH_IIR 1  /* RecursiveIIR()     gaussian.py:36-38 */
+#define FGB_SMOOTH_BOX 2  /* Box(half_width)    gaussian.py:52-60 */
+
+typedef struct fgb_smoother {
+    int32_t kind;      /* FGB_SMOOTH_*                                      */
+    int32_t box_half;  /* Box half width (kind == FGB_SMOOTH_BOX)           */
+    double radius;     /* FIR truncation radius in sigmas (kind == FIR)     */
+} fgb_smoother;
+
+/* Image geometry shared by every entry point. */
+typedef struct fgb_image {
+    int32_t height, width;
+    int64_t pitch;          /* elements between rows (>= width)             */
+    int32_t batch;          /* images                                       */
+    int32_t dtype;          /* FGB_F32 or FGB_F64 (input and output)        */
+    int64_t batch_stride;   /* elements between images (>= height*pitch)    */
+} fgb_image;
+
+/* Filter bank (BankSpec bank.py:23-52).  sigmas[] are explicit values: the
+ * host resolves the sigma = 2*pi/omega rule (bank.py:45-48). */
+typedef struct fgb_bank_desc {
+    fgb_image img;
+    int32_t n_freq;
+    int32_t orientations;     /* N, theta_k = k*pi/N                          */
+    const double* omegas;     /* [n_freq] host array                          */
+    const double* sigmas;     /* [n_freq] host array                          */
+    fgb_smoother smoother;
+    int32_t reuse;            /* 1 = compute_bank, 0 = compute_bank_noreuse   */
+    /* Optional shard: a list of work units u = i*(N/2+1) + k (k <= N/2) to
+     * compute (reuse mode).  NULL = all.  With a unit list the output is
+     * compact: per listed unit its direct entry, then its mirror N-k when it
+     * exists (bank.py:112-115). */
+    const int32_t* units;
+    int32_t n_units;
+} fgb_bank_desc;
+
+/* Single filter (GaborParams gabor.py:68-90); theta is normalised mod pi. */
+typedef struct fgb_filter_desc {
+    fgb_image img;
+    double omega, theta, sigma;
+    fgb_smoother smoother;
+} fgb_filter_desc;
+
+/* Localized SDFT (SdftSpec sdft.py:25-57).  sigma <= 0 selects the rule
+ * floor(min(mx,my)/2)/3 (sdft.py:45-49). */
+typedef struct fgb_sdft_desc {
+    fgb_image img;
+    int32_t mx, my;
+    double sigma;
+    fgb_smoother smoother;
+    /* Optional shard: list of pair heads u in [0, mx/2]; each computes bins
+     * (u, *) and (mx-u, *).  NULL = all bins in [mx*my] order.  With a list
+     * the output is compact: per head, rows (u, 0..my-1) then (mx-u, 0..my-1)
+     * when mx-u != u and u != 0. */
+    const int32_t* u_heads;
+    int32_t n_heads;
+} fgb_sdft_desc;
+
+/* ---- library ----------------------------------------------------------- */
+const char* fgb_last_error(void);
+int32_t fgb_version(void);                  /* major*10000 + minor*100 + patch */
+int32_t fgb_device_sm_count(void);
+
+/* ---- host-side coefficient math (no GPU needed) ------------------------- */
+int32_t fgb_pad_radius(const fgb_smoother* kind, double sigma);
+int32_t fgb_sampled_gaussian(double sigma, double radius, double* out, int32_t cap, int32_t* half);
+int32_t fgb_iir_coeffs(double sigma, double out_b_a1_a2_a3[4]);
+/* Number of output entries / bins a call writes (for allocation). */
+int64_t fgb_bank_entries(const fgb_bank_desc* d);
+int64_t fgb_sdft_bins(const fgb_sdft_desc* d);
+
+/* ---- device-pointer entry points (stream ordered, async) --------------- */
+int32_t fgb_bank(const fgb_bank_desc* d, const void* img, void* out, void* stream);
+int32_t fgb_filter(const fgb_filter_desc* d, const void* img, void* out, void* stream);
+int32_t fgb_horizontal_stage(const fgb_filter_desc* d, const void* img, void* j_out, void* stream);
+int32_t fgb_vertical_stage(const fgb_filter_desc* d, const void* j_in, void* out, int32_t conjugate, void* stream);
+int32_t fgb_sdft(const fgb_sdft_desc* d, const void* img, void* out, void* stream);
+int32_t fgb_sdft_bin(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img, void* out, void* stream);
+int32_t fgb_sdft_horizontal(const fgb_sdft_desc* d, int32_t u, const void* img, void* j_out, void* stream);
+
+/* ---- host-buffer entry points (copies inside; synchronous) ------------- */
+int32_t fgb_bank_host(const fgb_bank_desc* d, const void* img_host, void* out_host);
+int32_t fgb_filter_host(const fgb_filter_desc* d, const void* img_host, void* out_host);
+int32_t fgb_sdft_host(const fgb_sdft_desc* d, const void* img_host, void* out_host);
+int32_t fgb_horizontal_stage_host(const fgb_filter_desc* d, const void* img_host, void* j_host);
+int32_t fgb_vertical_stage_host(const fgb_filter_desc* d, const void* j_host, void* out_host, int32_t conjugate);
+int32_t fgb_sdft_bin_host(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img_host, void* out_host);
+int32_t fgb_sdft_horizontal_host(const fgb_sdft_desc* d, int32_t u, const void* img_host, void* j_host);
+
+/* ---- measurement ------------------------------------------------------- */
+/* Live per-kernel timing: while enabled, every launch is bracketed by CUDA
+ * events on its stream; fgb_profile_read synchronises them and aggregates by
+ * kernel name (algorithmic flops = reference OpCounters M + A of the stage
+ * work, bytes = compulsory input + output traffic). */
+typedef struct fgb_prof_entry {
+    char name[16];
+    int64_t launches;
+    double ms;
+    double flops;
+    double bytes;
+} fgb_prof_entry;
+void fgb_profile_enable(int32_t on);
+int32_t fgb_profile_read(fgb_prof_entry* out, int32_t cap);
+int64_t fgb_launch_count(void);      /* kernels launched by this library so far */
+double fgb_probe_fp32_tflops(void);  /* FFMA peak probe (K6), TFLOP/s */
+double fgb_probe_fp64_tflops(void);  /* DFMA peak probe (K6), TFLOP/s */
+
+/* ---- synchronisation helper for hosts without a CUDA binding ----------- */
+int32_t fgb_stream_synchronize(void* stream);
+/* Frees cached plans, workspaces and pinned staging of this process. */
+void fgb_release_caches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGB200_H */

@@ -1,0 +1,52 @@
+// Shared device/host helpers for libfgb200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fgb {
+
+// Complex sample type per precision: float2 for the fp32 build, double2 for
+// the fp64 validation build.  Interleaved (re, im) = one 8 / 16 byte access.
+template <typename T> struct cx;
+template <> struct cx<float> { using type = float2; };
+template <> struct cx<double> { using type = double2; };
+template <typename T> using cx_t = typename cx<T>::type;
+
+template <typename T> __host__ __device__ inline cx_t<T> mk(T a, T b) { cx_t<T> r; r.x = a; r.y = b; return r; }
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Streaming (evict-first) stores for final outputs, so the L2 keeps the
+// row-pass intermediates J resident for the column pass.
+__device__ __forceinline__ void st_cs(float2* p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(double2* p, double2 v) { __stcs(p, v); }
+
+// Output descriptor of one column job (one J source, up to 4 outputs).
+//   X = A - iB, Y = A + iB with A = sum ka[t] J[y+t], B = sum kb[t] J[y+t];
+//   out_o = phase_o * (conj_o ? conj(base_o) : base_o)
+// Plans are immutable and cached: jobs hold element offsets relative to the
+// per-call base pointers carried in the launch arguments.
+template <typename T> struct ColJob {
+    int64_t src_off;         // complex elements from src_base (batch 0)
+    int64_t dst_off[4];      // complex elements from dst_base (batch 0)
+    T phase_re[4], phase_im[4];
+    int32_t wofs;            // offset (in taps) into the weight pool
+    int32_t nout;
+    int8_t base[4];          // 0 = X, 1 = Y
+    int8_t conj[4];
+};
+
+// Row job group: up to kMaxND jobs sharing one input row and one symmetric
+// tap range [-h, h]:  J_k = phase_k * sum_t (kr_k[|t|] + i sgn(t) ki_k[|t|]) f[x+t]
+constexpr int kMaxND = 8;
+template <typename T> struct RowGroup {
+    int64_t dst_off[kMaxND]; // complex elements from dst_base
+    T phase_re[kMaxND], phase_im[kMaxND];
+    int32_t wofs;            // offset (in T units) of the [(hp+1)][NDP][2] table
+    int32_t nd;
+    int32_t has_phase;
+    int32_t pad_;
+};
+
+}  // namespace fgb

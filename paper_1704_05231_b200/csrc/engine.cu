@@ -1,0 +1,1602 @@
+// libfgb200 host engine: coefficient math, plan building, execution, C ABI.
+//
+// A call is compiled into an immutable, cached Plan: a list of kernel steps
+// plus one device blob holding every tap table, job table and trig table
+// the steps read.  Per call only the base pointers (image, output,
+// workspace) change, so steady-state calls issue kernel launches only.
+//
+// Schedules restated here (paths relative to /root/reference/pkg/src/fastgabor):
+//   bank (Algorithm 1)   bank.py:90-129 / :132-157 -- per frequency: one fused
+//                        row launch for every directly computed orientation
+//                        k <= N/2, then one column launch emitting theta_k
+//                        and pi - theta_k from the same J (bank.py:109-116).
+//   filter / stages      gabor.py:107-176, bank.py:68-74
+//   SDFT (Algorithm 2)   sdft.py:178-213 -- J_u for u <= Mx/2 once, every
+//                        (u, v<=My/2) column job writes bin(u,v), the mirror
+//                        bin(Mx-u,v) from conj(J_u) (sdft.py:202-203) and the
+//                        conjugate-symmetric fills (sdft.py:209-212).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/fgb200.h"
+#include "kernels.h"
+
+namespace fgb {
+
+template <typename T> double probe_fma_tflops();
+
+// ===========================================================================
+// errors
+// ===========================================================================
+static thread_local std::string g_err;
+static int32_t fail(int32_t code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+#define FGB_CUDA(x)                                                                          \
+    do {                                                                                     \
+        cudaError_t e_ = (x);                                                                \
+        if (e_ != cudaSuccess) return fail(FGB_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define FGB_TRY(x)                     \
+    do {                               \
+        int32_t r_ = (x);              \
+        if (r_ != FGB_OK) return r_;   \
+    } while (0)
+
+// ===========================================================================
+// host coefficient math
+// ===========================================================================
+
+// gaussian.py:198-212
+static int pad_radius(const fgb_smoother& k, double sigma) {
+    if (k.kind == FGB_SMOOTH_FIR) return std::max(1, (int)std::ceil(k.radius * sigma));
+    if (k.kind == FGB_SMOOTH_IIR) return (int)std::ceil(5.0 * sigma) + 2;
+    return 0;
+}
+
+// gaussian.py:188-195: unit-sum sampled Gaussian on [-h, h].
+static std::vector<double> sampled_gaussian(double sigma, double radius, int* half) {
+    const int h = std::max(1, (int)std::ceil(radius * sigma));
+    std::vector<double> w(2 * h + 1);
+    for (int i = 0; i <= 2 * h; ++i) {
+        const double x = (double)(i - h);
+        w[i] = std::exp(-(x * x) / (2.0 * sigma * sigma));
+    }
+    // pairwise sum (numpy's summation order for small arrays is blocked; the
+    // difference is an ulp-level scale of all taps)
+    double s = 0.0, c = 0.0;
+    for (double v : w) {  // Kahan: sum to ~1 ulp
+        double y = v - c, t = s + y;
+        c = (t - s) - y;
+        s = t;
+    }
+    for (double& v : w) v /= s;
+    *half = h;
+    return w;
+}
+
+// Pole-parameter knots of the third-order recursion; data table of
+// gaussian.py:78-105 (log2 sigma = -1 .. 5 step 0.25; (log(r-1), phi, log(d-1))).
+static const double kKnots[25][3] = {
+    {1.4935547894, 1.7389422874, 1.4116802788},    {1.0124325346, 1.6028888671, 0.9948121036},
+    {0.7060188604, 1.4246405642, 0.7655646807},    {0.3711981889, 1.3035671168, 0.4599139117},
+    {0.0723219048, 1.1741421430, 0.1988303275},    {-0.0657826821, 1.0609426640, 0.0641342325},
+    {-0.1084526360, 0.8746229033, 0.0520603916},   {-0.3079872798, 0.7888980715, -0.2103392209},
+    {-0.4435572915, 0.6681318749, -0.3543999555},  {-0.5826541508, 0.5511044975, -0.4681767292},
+    {-0.6341889379, 0.4375707759, -0.4950920113},  {-0.9438814088, 0.3960503190, -0.8422106914},
+    {-1.1264093957, 0.3331316708, -1.0232036316},  {-1.3323529220, 0.2853777435, -1.2419374903},
+    {-1.5043108087, 0.2384505949, -1.4119365035},  {-1.6909017377, 0.2010996380, -1.6007291308},
+    {-1.8639872273, 0.1677245302, -1.7693707791},  {-2.0526626380, 0.1419695700, -1.9627706878},
+    {-2.2480922032, 0.1206592327, -2.1643322734},  {-2.4183618584, 0.1007997229, -2.3318115898},
+    {-2.6108636240, 0.0856583363, -2.5302995718},  {-2.7812366868, 0.0716083982, -2.6981612487},
+    {-2.9595594412, 0.0602521009, -2.8771310090},  {-3.1353804585, 0.0506201753, -3.0527659020},
+    {-3.3165061207, 0.0427250483, -3.2360423517},
+};
+
+using cd = std::complex<double>;
+
+static void poles_from(const double prm[3], cd p[3]) {
+    // gaussian.py:136-142
+    const double r = 1.0 + std::exp(prm[0]);
+    const double d = 1.0 + std::exp(prm[2]);
+    p[0] = r * cd(std::cos(prm[1]), std::sin(prm[1]));
+    p[1] = r * cd(std::cos(-prm[1]), std::sin(-prm[1]));
+    p[2] = cd(d, 0.0);
+}
+
+static double cascade_var(const cd p[3]) {
+    // gaussian.py:145-147
+    cd s(0.0, 0.0);
+    for (int i = 0; i < 3; ++i) s += 2.0 * p[i] / ((p[i] - 1.0) * (p[i] - 1.0));
+    return s.real();
+}
+
+// Brent's root finder (Brent 1973), the algorithm of scipy.optimize.brentq
+// used by gaussian.py:160 with its default tolerances.
+template <typename F> static double brent(F f, double xa, double xb) {
+    const double xtol = 2e-12, rtol = 8.881784197001252e-16;
+    double xpre = xa, xcur = xb, xblk = 0.0, fpre = f(xpre), fcur = f(xcur), fblk = 0.0, spre = 0.0, scur = 0.0;
+    if (fpre == 0) return xpre;
+    if (fcur == 0) return xcur;
+    for (int it = 0; it < 200; ++it) {
+        if (fpre != 0 && fcur != 0 && (std::signbit(fpre) != std::signbit(fcur))) {
+            xblk = xpre;
+            fblk = fpre;
+            spre = scur = xcur - xpre;
+        }
+        if (std::fabs(fblk) < std::fabs(fcur)) {
+            xpre = xcur; xcur = xblk; xblk = xpre;
+            fpre = fcur; fcur = fblk; fblk = fpre;
+        }
+        const double delta = (xtol + rtol * std::fabs(xcur)) / 2;
+        const double sbis = (xblk - xcur) / 2;
+        if (fcur == 0 || std::fabs(sbis) < delta) return xcur;
+        if (std::fabs(spre) > delta && std::fabs(fcur) < std::fabs(fpre)) {
+            double stry;
+            if (xpre == xblk) {
+                stry = -fcur * (xcur - xpre) / (fcur - fpre);
+            } else {
+                const double dpre = (fpre - fcur) / (xpre - xcur);
+                const double dblk = (fblk - fcur) / (xblk - xcur);
+                stry = -fcur * (fblk * dblk - fpre * dpre) / (dblk * dpre * (fblk - fpre));
+            }
+            if (2 * std::fabs(stry) < std::min(std::fabs(spre), 3 * std::fabs(sbis) - delta)) {
+                spre = scur;
+                scur = stry;
+            } else {
+                spre = sbis;
+                scur = sbis;
+            }
+        } else {
+            spre = sbis;
+            scur = sbis;
+        }
+        xpre = xcur;
+        fpre = fcur;
+        if (std::fabs(scur) > delta) xcur += scur;
+        else xcur += (sbis > 0 ? delta : -delta);
+        fcur = f(xcur);
+    }
+    return xcur;
+}
+
+// gaussian.py:164-185: (B, a1, a2, a3) with B = sum(a), a = poly(1/poles).
+static int32_t iir_coeffs(double sigma, double out[4]) {
+    if (!(sigma > 0)) return fail(FGB_EINVAL, "sigma must be positive");
+    if (sigma < 0.5)
+        return fail(FGB_EINVAL,
+                    "sigma below 0.5 is outside the recursive filter's validity range; use the ExactFIR smoother instead");
+    cd p[3];
+    if (sigma <= 32.0) {
+        double l2 = std::log2(sigma);
+        l2 = std::min(std::max(l2, -1.0), 5.0);
+        double prm[3];
+        // np.interp on the uniform knot grid -1 + 0.25 j
+        int j = (int)std::floor((l2 + 1.0) / 0.25);
+        if (j >= 24) {
+            for (int c = 0; c < 3; ++c) prm[c] = kKnots[24][c];
+        } else {
+            if (j < 0) j = 0;
+            const double x0 = -1.0 + 0.25 * j, x1 = -1.0 + 0.25 * (j + 1);
+            for (int c = 0; c < 3; ++c) {
+                const double slope = (kKnots[j + 1][c] - kKnots[j][c]) / (x1 - x0);
+                prm[c] = slope * (l2 - x0) + kKnots[j][c];
+            }
+        }
+        poles_from(prm, p);
+    } else {
+        cd top[3];
+        poles_from(kKnots[24], top);
+        auto mismatch = [&](double q) {
+            cd t[3];
+            for (int i = 0; i < 3; ++i) t[i] = std::pow(top[i], 1.0 / q);
+            return cascade_var(t) - sigma * sigma;
+        };
+        double hi = 2.0;
+        while (mismatch(hi) < 0.0) hi *= 2.0;
+        const double q = brent(mismatch, 0.5, hi);
+        for (int i = 0; i < 3; ++i) p[i] = std::pow(top[i], 1.0 / q);
+    }
+    // np.poly(1/p): a = [1]; a = conv(a, [1, -q_k]) for k = 0, 1, 2
+    cd a[4] = {cd(1, 0), cd(0, 0), cd(0, 0), cd(0, 0)};
+    for (int k = 0; k < 3; ++k) {
+        const cd q = 1.0 / p[k];
+        for (int m = k + 1; m >= 1; --m) a[m] = a[m] - q * a[m - 1];
+    }
+    const double a1 = a[1].real(), a2 = a[2].real(), a3 = a[3].real();
+    out[0] = 1.0 + a1 + a2 + a3;
+    out[1] = a1;
+    out[2] = a2;
+    out[3] = a3;
+    return FGB_OK;
+}
+
+// ===========================================================================
+// device memory
+// ===========================================================================
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    int32_t ensure(size_t bytes) {
+        if (bytes <= n) return FGB_OK;
+        reset();
+        if (bytes == 0) return FGB_OK;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            return fail(FGB_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
+        }
+        n = bytes;
+        return FGB_OK;
+    }
+};
+
+// ===========================================================================
+// plans
+// ===========================================================================
+enum Sel { SEL_IMG = 0, SEL_IMGC = 1, SEL_OUT = 2, SEL_WS = 3, SEL_WSR = 4 };
+struct Ref {
+    int sel = SEL_WS;
+    int64_t off = 0;  // elements of the referenced type (T for real, C for complex)
+};
+
+enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR };
+
+template <typename T> struct Step {
+    int kind = 0;
+    const char* name = "";
+    double flops = 0.0;      // reference-counter flops (M + A) per image
+    double bytes = 0.0;      // compulsory bytes per image (input read + output written)
+    int H = 0, W = 0;     // dims seen by the kernel
+    Ref src, dst;
+    int64_t src_pitch = -1;  // real inputs: -1 = descriptor pitch
+    // ST_ROW
+    RowGroup<T> rg{};
+    int hp = 0;
+    // ST_COL
+    int job0 = 0, njobs = 0, t0 = 0, nt = 0, zero_bnd = 0, has_b = 1;
+    // ST_IIR
+    int P = 0;
+    IirCoef coef{};
+    int64_t scratch_off = 0;  // T elements into the workspace scratch region
+};
+
+struct PlanBase {
+    virtual ~PlanBase() {}
+};
+
+template <typename T> struct Plan : PlanBase {
+    using C = cx_t<T>;
+    std::vector<Step<T>> steps;
+    // host blobs (uploaded once into `blob`)
+    std::vector<T> wrow;          // row tap tables
+    std::vector<C> wcol;          // column tap pairs
+    std::vector<ColJob<T>> cjobs;
+    std::vector<IirJob<T>> ijobs;
+    std::vector<double2> tabs;
+    DevBuf blob;
+    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0;
+    // workspace per image (bytes), scratch (T elements per image-chunk) and chunking
+    int64_t ws_img_c = 0;         // complex elements per image
+    int64_t scratch_img_t = 0;    // T elements per image (IIR scratch)
+    int64_t out_img_c = 0;        // complex elements per output image
+    int H = 0, W = 0;
+    int chunk = 1;
+
+    int32_t upload() {
+        auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+        size_t o = 0;
+        off_wrow = o; o = al(o + wrow.size() * sizeof(T));
+        off_wcol = o; o = al(o + wcol.size() * sizeof(C));
+        off_cjobs = o; o = al(o + cjobs.size() * sizeof(ColJob<T>));
+        off_ijobs = o; o = al(o + ijobs.size() * sizeof(IirJob<T>));
+        off_tabs = o; o = al(o + tabs.size() * sizeof(double2));
+        FGB_TRY(blob.ensure(std::max<size_t>(o, 256)));
+        std::vector<char> h(o, 0);
+        if (!wrow.empty()) std::memcpy(h.data() + off_wrow, wrow.data(), wrow.size() * sizeof(T));
+        if (!wcol.empty()) std::memcpy(h.data() + off_wcol, wcol.data(), wcol.size() * sizeof(C));
+        if (!cjobs.empty()) std::memcpy(h.data() + off_cjobs, cjobs.data(), cjobs.size() * sizeof(ColJob<T>));
+        if (!ijobs.empty()) std::memcpy(h.data() + off_ijobs, ijobs.data(), ijobs.size() * sizeof(IirJob<T>));
+        if (!tabs.empty()) std::memcpy(h.data() + off_tabs, tabs.data(), tabs.size() * sizeof(double2));
+        FGB_CUDA(cudaMemcpy(blob.p, h.data(), o, cudaMemcpyHostToDevice));
+        return FGB_OK;
+    }
+    const T* d_wrow() const { return (const T*)((char*)blob.p + off_wrow); }
+    const C* d_wcol() const { return (const C*)((char*)blob.p + off_wcol); }
+    const ColJob<T>* d_cjobs() const { return (const ColJob<T>*)((char*)blob.p + off_cjobs); }
+    const IirJob<T>* d_ijobs() const { return (const IirJob<T>*)((char*)blob.p + off_ijobs); }
+    const double2* d_tabs() const { return (const double2*)((char*)blob.p + off_tabs); }
+};
+
+// ---------------------------------------------------------------------------
+// builders
+// ---------------------------------------------------------------------------
+template <typename T> struct Builder {
+    using C = cx_t<T>;
+    Plan<T>& p;
+    explicit Builder(Plan<T>& pl) : p(pl) {}
+
+    // Row group over symmetric taps w[0..2h] for nd jobs with frequencies
+    // f_k and sign s: J_k = phase_k sum_t w[t] e^{-i s f_k t} f[x+t].
+    void row_group(const std::vector<double>& w, int h, const std::vector<double>& freq, double sgn,
+                   const std::vector<cd>& phase, const std::vector<int64_t>& dst_off, Ref src, Ref dst, int H, int W,
+                   double sflops) {
+        const int nd = (int)freq.size();
+        const int hp = row_sym_pad<T>(h);
+        const int ndp = (nd + 1) & ~1;
+        Step<T> st;
+        st.kind = ST_ROW;
+        st.name = "row_fir";
+        st.flops = nd * (2.0 * sflops + 8.0) * H * W;
+        st.bytes = (double)H * W * sizeof(T) + (double)nd * H * W * sizeof(C);
+        st.H = H;
+        st.W = W;
+        st.src = src;
+        st.dst = dst;
+        st.hp = hp;
+        st.rg.wofs = (int32_t)p.wrow.size();
+        st.rg.nd = nd;
+        st.rg.has_phase = 0;
+        for (int k = 0; k < nd; ++k) {
+            st.rg.dst_off[k] = dst_off[k];
+            st.rg.phase_re[k] = (T)phase[k].real();
+            st.rg.phase_im[k] = (T)phase[k].imag();
+            if (phase[k] != cd(1.0, 0.0)) st.rg.has_phase = 1;
+        }
+        for (int t = 0; t <= hp; ++t) {
+            for (int k = 0; k < ndp; ++k) {
+                double kr = 0.0, ki = 0.0;
+                if (k < nd && t <= h) {
+                    const double wt = w[h + t];
+                    kr = wt * std::cos(freq[k] * t);
+                    ki = -sgn * wt * std::sin(freq[k] * t);
+                }
+                p.wrow.push_back((T)kr);
+                p.wrow.push_back((T)ki);
+            }
+        }
+        p.steps.push_back(st);
+    }
+
+    // Column job with taps t0..t0+nt-1: ka = w cos(f t), kb = w sin(f t).
+    int col_weights(const std::vector<double>& w, int t0, double f) {
+        const int off = (int)p.wcol.size();
+        for (size_t q = 0; q < w.size(); ++q) {
+            const double t = (double)(t0 + (int)q);
+            p.wcol.push_back(mk<T>((T)(w[q] * std::cos(f * t)), (T)(w[q] * std::sin(f * t))));
+        }
+        return off;
+    }
+
+    struct Out {
+        int64_t dst_off;
+        int base;  // 0 X, 1 Y
+        int conj;
+        cd phase;
+    };
+    ColJob<T> col_job(int64_t src_off, int wofs, const std::vector<Out>& outs) {
+        ColJob<T> j{};
+        j.src_off = src_off;
+        j.wofs = wofs;
+        j.nout = (int)outs.size();
+        for (size_t o = 0; o < outs.size(); ++o) {
+            j.dst_off[o] = outs[o].dst_off;
+            j.base[o] = (int8_t)outs[o].base;
+            j.conj[o] = (int8_t)outs[o].conj;
+            j.phase_re[o] = (T)outs[o].phase.real();
+            j.phase_im[o] = (T)outs[o].phase.imag();
+        }
+        return j;
+    }
+    void col_step(const std::vector<ColJob<T>>& jobs, Ref src, Ref dst, int H, int W, int t0, int nt, int zero_bnd,
+                  int has_b, double sflops = 0.0, int counted = -1, bool real_in = false) {
+        if (jobs.empty()) return;
+        Step<T> st;
+        st.kind = ST_COL;
+        st.name = "col_fir";
+        int nout = 0;
+        for (const auto& j : jobs) nout += j.nout;
+        if (counted < 0) counted = nout;
+        st.flops = counted * (2.0 * sflops + (real_in ? 8.0 : 12.0)) * H * W;
+        st.bytes = ((double)nout + jobs.size()) * H * W * sizeof(C);
+        st.H = H;
+        st.W = W;
+        st.src = src;
+        st.dst = dst;
+        st.job0 = (int)p.cjobs.size();
+        st.njobs = (int)jobs.size();
+        st.t0 = t0;
+        st.nt = nt;
+        st.zero_bnd = zero_bnd;
+        st.has_b = has_b;
+        p.cjobs.insert(p.cjobs.end(), jobs.begin(), jobs.end());
+        p.steps.push_back(st);
+    }
+    int64_t table(double f, int lo, int n) {
+        const int64_t off = (int64_t)p.tabs.size();
+        for (int i = 0; i < n; ++i) {
+            const double x = (double)(lo + i);
+            p.tabs.push_back(make_double2(std::cos(f * x), std::sin(f * x)));
+        }
+        return off;
+    }
+    void iir_step(const std::vector<IirJob<T>>& jobs, Ref src, Ref dst, int H, int W, int P, const IirCoef& c,
+                  int64_t scratch_off, int counted = -1, bool real_in = false) {
+        if (jobs.empty()) return;
+        Step<T> st;
+        st.kind = ST_IIR;
+        st.name = "iir";
+        int nout = 0;
+        for (const auto& j : jobs) nout += j.nout;
+        if (counted < 0) counted = nout;
+        st.flops = counted * (2.0 * 12.0 + (real_in ? 8.0 : 12.0)) * H * W;
+        st.bytes = ((double)nout + jobs.size()) * H * W * sizeof(C);
+        st.H = H;
+        st.W = W;
+        st.src = src;
+        st.dst = dst;
+        st.job0 = (int)p.ijobs.size();
+        st.njobs = (int)jobs.size();
+        st.P = P;
+        st.coef = c;
+        st.scratch_off = scratch_off;
+        p.ijobs.insert(p.ijobs.end(), jobs.begin(), jobs.end());
+        p.steps.push_back(st);
+    }
+    void tr(int kind, Ref src, Ref dst, int H, int W) {
+        Step<T> st;
+        st.kind = kind;
+        st.name = "transpose";
+        st.bytes = 2.0 * H * W * (kind == ST_TR_RR ? sizeof(T) : sizeof(C));
+        st.H = H;
+        st.W = W;
+        st.src = src;
+        st.dst = dst;
+        p.steps.push_back(st);
+    }
+};
+
+static Ref R(int sel, int64_t off) {
+    Ref r;
+    r.sel = sel;
+    r.off = off;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// descriptor validation
+// ---------------------------------------------------------------------------
+static int32_t check_image(const fgb_image& im, bool complex_in = false) {
+    if (im.height < 1 || im.width < 1) return fail(FGB_EINVAL, "image dimensions must be at least 1x1");
+    if (im.dtype != FGB_F32 && im.dtype != FGB_F64) return fail(FGB_EINVAL, "dtype must be FGB_F32 or FGB_F64");
+    if (im.batch < 1) return fail(FGB_EINVAL, "batch must be >= 1");
+    if (im.pitch < im.width) return fail(FGB_EINVAL, "pitch must be >= width");
+    if (complex_in && im.pitch != im.width) return fail(FGB_EINVAL, "complex inputs must be dense (pitch == width)");
+    if (im.batch > 1 && im.batch_stride < (int64_t)im.height * im.pitch)
+        return fail(FGB_EINVAL, "batch_stride must be >= height*pitch");
+    return FGB_OK;
+}
+
+static int32_t check_smoother(const fgb_smoother& k, double sigma) {
+    if (k.kind == FGB_SMOOTH_FIR) {
+        if (k.radius < 3) return fail(FGB_EINVAL, "truncation radius must be at least 3 sigma");
+        return FGB_OK;
+    }
+    if (k.kind == FGB_SMOOTH_IIR) {
+        double c[4];
+        return iir_coeffs(sigma, c);
+    }
+    if (k.kind == FGB_SMOOTH_BOX) {
+        if (k.box_half < 0) return fail(FGB_EINVAL, "box half-width must be non-negative");
+        return FGB_OK;
+    }
+    return fail(FGB_EUNSUPPORTED, "unknown smoother kind");
+}
+
+static double norm_theta(double th) {
+    // Python's float % (sign of the divisor)
+    double r = std::fmod(th, M_PI);
+    if (r != 0.0 && (r < 0) != (M_PI < 0)) r += M_PI;
+    return r;
+}
+
+// ===========================================================================
+// Gabor plans
+// ===========================================================================
+struct DirectJob {
+    double wc, ws;        // omega cos(theta), omega sin(theta)
+    int64_t out_direct;   // entry slot (complex elems offset) or -1
+    int64_t out_mirror;   // mirrored slot or -1
+};
+
+// One frequency worth of Gabor work: row stage for `jobs`, column stage with
+// direct / mirrored outputs.  J planes live in ws at [ws_j0 + j*H*W].
+template <typename T>
+static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double sigma, const std::vector<DirectJob>& jobs,
+                                int H, int W, int64_t ws_j0, int64_t ws_aux, Ref img, Ref out, bool row_only,
+                                bool col_only, int64_t* ws_need) {
+    const int64_t HW = (int64_t)H * W;
+    const int nj = (int)jobs.size();
+    if (nj == 0) return FGB_OK;
+    int64_t need = ws_j0 + (row_only || col_only ? 0 : (int64_t)nj * HW);
+    if (sm.kind == FGB_SMOOTH_FIR || sm.kind == FGB_SMOOTH_BOX) {
+        std::vector<double> w;
+        int h = 0, t0 = 0;
+        const bool box = sm.kind == FGB_SMOOTH_BOX;
+        if (box) {
+            h = sm.box_half;
+            w.assign(2 * h + 1, 1.0);
+        } else {
+            w = sampled_gaussian(sigma, sm.radius, &h);
+        }
+        t0 = -h;
+        const int nt = 2 * h + 1;
+        // ---- row stage ----
+        if (!col_only) {
+            if (!box) {
+                for (int g0 = 0; g0 < nj; g0 += kMaxND) {
+                    const int g1 = std::min(nj, g0 + kMaxND);
+                    std::vector<double> fr;
+                    std::vector<cd> ph;
+                    std::vector<int64_t> dst;
+                    for (int j = g0; j < g1; ++j) {
+                        fr.push_back(jobs[j].wc);
+                        ph.push_back(cd(1.0, 0.0));
+                        dst.push_back(row_only ? jobs[j].out_direct : ws_j0 + (int64_t)j * HW);
+                    }
+                    b.row_group(w, h, fr, +1.0, ph, dst, img, row_only ? out : R(SEL_WS, 0), H, W, 4.0 * h + 1);
+                }
+            } else {
+                // zero-padded box: transpose -> column kernel -> transpose back
+                const int64_t t_img = ws_aux, t_j = ws_aux + HW;
+                need = std::max(need, t_j + (int64_t)nj * HW);
+                b.tr(ST_TR_RC, img, R(SEL_WS, t_img), H, W);
+                std::vector<ColJob<T>> cj;
+                for (int j = 0; j < nj; ++j) {
+                    const int wo = b.col_weights(w, t0, jobs[j].wc);
+                    cj.push_back(b.col_job(0, wo, {{t_j + (int64_t)j * HW, 0, 0, cd(1, 0)}}));
+                }
+                b.col_step(cj, R(SEL_WS, t_img), R(SEL_WS, 0), W, H, t0, nt, 1, 1, 2.0 * h, nj, true);
+                for (int j = 0; j < nj; ++j)
+                    b.tr(ST_TR_CC, R(SEL_WS, t_j + (int64_t)j * HW),
+                         row_only ? R(out.sel, jobs[j].out_direct) : R(SEL_WS, ws_j0 + (int64_t)j * HW), W, H);
+            }
+        }
+        // ---- column stage ----
+        if (!row_only) {
+            std::vector<ColJob<T>> cj_b, cj_nob;
+            for (int j = 0; j < nj; ++j) {
+                const int wo = b.col_weights(w, t0, jobs[j].ws);
+                std::vector<typename Builder<T>::Out> outs;
+                if (jobs[j].out_direct >= 0) outs.push_back({jobs[j].out_direct, 0, 0, cd(1, 0)});
+                if (jobs[j].out_mirror >= 0) outs.push_back({jobs[j].out_mirror, 1, 1, cd(1, 0)});
+                ColJob<T> job = b.col_job(col_only ? 0 : ws_j0 + (int64_t)j * HW, wo, outs);
+                if (jobs[j].ws == 0.0) cj_nob.push_back(job);
+                else cj_b.push_back(job);
+            }
+            const Ref src = col_only ? img : R(SEL_WS, 0);
+            const double sfl = box ? 2.0 * h : 4.0 * h + 1;
+            b.col_step(cj_b, src, out, H, W, t0, nt, box ? 1 : 0, 1, sfl);
+            b.col_step(cj_nob, src, out, H, W, t0, nt, box ? 1 : 0, 0, sfl);
+        }
+    } else {
+        // ---- RecursiveIIR ----
+        double cf[4];
+        FGB_TRY(iir_coeffs(sigma, cf));
+        IirCoef c{cf[0], cf[1], cf[2], cf[3]};
+        const int P = pad_radius(sm, sigma);
+        int64_t scratch = 0;  // T elements, region after all complex regions (set by caller via ws_need)
+        if (!col_only) {
+            const int64_t t_img = ws_aux, t_j = ws_aux + HW;
+            need = std::max(need, t_j + (int64_t)nj * HW);
+            b.tr(ST_TR_RC, img, R(SEL_WS, t_img), H, W);
+            std::vector<IirJob<T>> ij;
+            for (int j = 0; j < nj; ++j) {
+                IirJob<T> q{};
+                q.src_off = 0;
+                q.tabm_off = b.table(jobs[j].wc, -P, W + 2 * P);
+                q.tabr_off = q.tabm_off + P;
+                q.dst_off[0] = t_j + (int64_t)j * HW;
+                q.pair[0] = 0;
+                q.conj[0] = 0;
+                q.nout = 1;
+                q.need = 1;
+                q.sdft = 0;
+                ij.push_back(q);
+            }
+            // transposed geometry: "rows" = x (W of them), "columns" = y (H)
+            b.iir_step(ij, R(SEL_WS, t_img), R(SEL_WS, 0), W, H, P, c, scratch, -1, true);
+            for (int j = 0; j < nj; ++j)
+                b.tr(ST_TR_CC, R(SEL_WS, t_j + (int64_t)j * HW),
+                     row_only ? R(out.sel, jobs[j].out_direct) : R(SEL_WS, ws_j0 + (int64_t)j * HW), W, H);
+        }
+        if (!row_only) {
+            std::vector<IirJob<T>> ij;
+            for (int j = 0; j < nj; ++j) {
+                IirJob<T> q{};
+                q.src_off = col_only ? 0 : ws_j0 + (int64_t)j * HW;
+                q.tabm_off = b.table(jobs[j].ws, -P, H + 2 * P);
+                q.tabr_off = q.tabm_off + P;
+                q.nout = 0;
+                q.need = 0;
+                if (jobs[j].out_direct >= 0) {
+                    q.dst_off[q.nout] = jobs[j].out_direct;
+                    q.pair[q.nout] = 0;
+                    q.conj[q.nout] = 0;
+                    q.nout++;
+                    q.need |= 1;
+                }
+                if (jobs[j].out_mirror >= 0) {
+                    q.dst_off[q.nout] = jobs[j].out_mirror;
+                    q.pair[q.nout] = 1;
+                    q.conj[q.nout] = 0;
+                    q.nout++;
+                    q.need |= 2;
+                }
+                q.sdft = 0;
+                ij.push_back(q);
+            }
+            b.iir_step(ij, col_only ? img : R(SEL_WS, 0), out, H, W, P, c, scratch);
+        }
+    }
+    *ws_need = std::max(*ws_need, need);
+    return FGB_OK;
+}
+
+// IIR scratch need (T elements per image) for a plan: max over IIR steps.
+template <typename T> static int64_t iir_scratch_need(const Plan<T>& p) {
+    int64_t m = 0;
+    for (const auto& s : p.steps)
+        if (s.kind == ST_IIR) m = std::max<int64_t>(m, (int64_t)iir_scratch_elems<T>(s.H, s.W, s.P, s.njobs, 1));
+    return m;
+}
+
+static int64_t ws_budget_bytes() {
+    const char* e = std::getenv("FGB_WS_BUDGET_MB");
+    const int64_t mb = e ? std::atoll(e) : 160;
+    return std::max<int64_t>(mb, 1) << 20;
+}
+
+template <typename T> static void finish_chunking(Plan<T>& p, int batch) {
+    p.scratch_img_t = iir_scratch_need(p);
+    const int64_t per = p.ws_img_c * (int64_t)sizeof(cx_t<T>) + p.scratch_img_t * (int64_t)sizeof(T);
+    int64_t c = per > 0 ? ws_budget_bytes() / per : batch;
+    p.chunk = (int)std::max<int64_t>(1, std::min<int64_t>(c, batch));
+}
+
+template <typename T>
+static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
+    Builder<T> b(p);
+    const int H = d.img.height, W = d.img.width, N = d.orientations;
+    const int64_t HW = (int64_t)H * W;
+    const int nh = N / 2;
+    p.H = H;
+    p.W = W;
+    // work units / output slots
+    std::vector<std::vector<DirectJob>> per_f(d.n_freq);
+    int64_t slot = 0;
+    if (d.units) {
+        for (int u = 0; u < d.n_units; ++u) {
+            const int unit = d.units[u];
+            const int i = unit / (nh + 1), k = unit % (nh + 1);
+            if (unit < 0 || i >= d.n_freq) return fail(FGB_EINVAL, "work unit out of range");
+            const double th = norm_theta(k * M_PI / N);
+            DirectJob j{d.omegas[i] * std::cos(th), d.omegas[i] * std::sin(th), slot * HW, -1};
+            slot++;
+            if (nh < N - k && N - k < N) j.out_mirror = (slot++) * HW;
+            per_f[i].push_back(j);
+        }
+    } else {
+        for (int i = 0; i < d.n_freq; ++i) {
+            const int nk = d.reuse ? nh + 1 : N;
+            for (int k = 0; k < nk; ++k) {
+                const double th = norm_theta(k * M_PI / N);
+                DirectJob j{d.omegas[i] * std::cos(th), d.omegas[i] * std::sin(th), ((int64_t)i * N + k) * HW, -1};
+                if (d.reuse && nh < N - k && N - k < N) j.out_mirror = ((int64_t)i * N + (N - k)) * HW;
+                per_f[i].push_back(j);
+            }
+        }
+        slot = (int64_t)d.n_freq * N;
+    }
+    p.out_img_c = slot * HW;
+    int64_t max_nj = 0;
+    for (auto& v : per_f) max_nj = std::max<int64_t>(max_nj, (int64_t)v.size());
+    const int64_t ws_aux = max_nj * HW;  // transposes after the J planes
+    int64_t need = 0;
+    for (int i = 0; i < d.n_freq; ++i) {
+        FGB_TRY(build_gabor_freq<T>(b, d.smoother, d.sigmas[i], per_f[i], H, W, 0, ws_aux, R(SEL_IMG, 0),
+                                    R(SEL_OUT, 0), false, false, &need));
+    }
+    p.ws_img_c = need;
+    finish_chunking(p, d.img.batch);
+    return p.upload();
+}
+
+// mode: 0 full filter, 1 horizontal stage only, 2 vertical stage, 3 vertical conjugate
+template <typename T>
+static int32_t build_filter(Plan<T>& p, const fgb_filter_desc& d, int mode) {
+    Builder<T> b(p);
+    const int H = d.img.height, W = d.img.width;
+    const int64_t HW = (int64_t)H * W;
+    p.H = H;
+    p.W = W;
+    const double th = norm_theta(d.theta);
+    DirectJob j{d.omega * std::cos(th), d.omega * std::sin(th), 0, -1};
+    if (mode == 3) {
+        j.out_direct = -1;
+        j.out_mirror = 0;
+    }
+    p.out_img_c = HW;
+    int64_t need = 0;
+    const Ref in = (mode >= 2) ? R(SEL_IMGC, 0) : R(SEL_IMG, 0);
+    FGB_TRY(build_gabor_freq<T>(b, d.smoother, d.sigma, {j}, H, W, 0, (mode == 0 ? HW : 0), in, R(SEL_OUT, 0),
+                                mode == 1, mode >= 2, &need));
+    p.ws_img_c = need;
+    finish_chunking(p, d.img.batch);
+    return p.upload();
+}
+
+// ===========================================================================
+// SDFT plans
+// ===========================================================================
+static double sdft_sigma(const fgb_sdft_desc& d) {
+    if (d.sigma > 0) return d.sigma;
+    return (double)(std::min(d.mx, d.my) / 2) / 3.0;
+}
+
+// Window taps of one SDFT axis (sdft.py:68-72 + gaussian.py): Gaussian
+// [-h, h] (replicate) or the asymmetric box [-(m/2), m-1-m/2] (zero padded).
+static void sdft_axis_taps(const fgb_smoother& sm, double sigma, int m, std::vector<double>* w, int* t0) {
+    if (sm.kind == FGB_SMOOTH_BOX) {
+        const int lo = -(m / 2), hi = m - 1 - m / 2;
+        w->assign(hi - lo + 1, 1.0);
+        *t0 = lo;
+    } else {
+        int h;
+        *w = sampled_gaussian(sigma, sm.radius, &h);
+        *t0 = -h;
+    }
+}
+
+// head list -> bin slots.  full layout: bin = u*my + v.  compact: per head u,
+// rows (u, 0..my-1) then (mx-u, 0..my-1) if distinct.
+struct BinMap {
+    std::vector<int> heads;
+    std::map<int, int64_t> row_slot;  // u -> first bin slot of row u
+    int64_t nbins = 0;
+};
+static int32_t make_binmap(const fgb_sdft_desc& d, BinMap* bm) {
+    const int mx = d.mx, my = d.my;
+    if (!d.u_heads) {
+        for (int u = 0; u <= mx / 2; ++u) bm->heads.push_back(u);
+        for (int u = 0; u < mx; ++u) bm->row_slot[u] = (int64_t)u * my;
+        bm->nbins = (int64_t)mx * my;
+        return FGB_OK;
+    }
+    int64_t s = 0;
+    for (int i = 0; i < d.n_heads; ++i) {
+        const int u = d.u_heads[i];
+        if (u < 0 || u > mx / 2) return fail(FGB_EINVAL, "SDFT pair head outside [0, mx/2]");
+        if (bm->row_slot.count(u)) return fail(FGB_EINVAL, "duplicate SDFT pair head");
+        bm->heads.push_back(u);
+        bm->row_slot[u] = s;
+        s += my;
+        const int um = (mx - u) % mx;
+        if (um != u) {
+            bm->row_slot[um] = s;
+            s += my;
+        }
+    }
+    bm->nbins = s;
+    return FGB_OK;
+}
+
+// Full SDFT on an image of H x W read from `img` (real).  The horizontal
+// stage writes J_u into ws planes [0, nh); bins go to `out` at slot*HW.
+template <typename T>
+static int32_t build_sdft_core(Builder<T>& b, const fgb_sdft_desc& d, const BinMap& bm, int H, int W, Ref img,
+                               Ref out, int64_t out_base, int64_t ws0, int64_t* ws_need) {
+    const int mx = d.mx, my = d.my;
+    const int64_t HW = (int64_t)H * W;
+    const double sigma = sdft_sigma(d);
+    const fgb_smoother& sm = d.smoother;
+    const int cx = mx / 2, cy = my / 2;
+    const double w0x = 2.0 * M_PI / mx, w0y = 2.0 * M_PI / my;
+    const int nh = (int)bm.heads.size();
+    int64_t need = (int64_t)nh * HW;  // J_u planes
+    const int64_t aux = need;
+    auto slot = [&](int u, int v) { return out_base + (bm.row_slot.at(u) + v) * HW; };
+
+    if (sm.kind == FGB_SMOOTH_FIR || sm.kind == FGB_SMOOTH_BOX) {
+        std::vector<double> wx, wy;
+        int t0x, t0y;
+        sdft_axis_taps(sm, sigma, mx, &wx, &t0x);
+        sdft_axis_taps(sm, sigma, my, &wy, &t0y);
+        const bool box = sm.kind == FGB_SMOOTH_BOX;
+        // ---- horizontal stage: J_u = sum_t w e^{i phi (c + t)} f[x+t] ----
+        if (!box) {
+            const int h = -t0x;
+            for (int g0 = 0; g0 < nh; g0 += kMaxND) {
+                const int g1 = std::min(nh, g0 + kMaxND);
+                std::vector<double> fr;
+                std::vector<cd> ph;
+                std::vector<int64_t> dst;
+                for (int i = g0; i < g1; ++i) {
+                    const double phi = w0x * bm.heads[i];
+                    fr.push_back(phi);
+                    ph.push_back(cd(std::cos(phi * cx), std::sin(phi * cx)));
+                    dst.push_back((int64_t)i * HW);
+                }
+                b.row_group(wx, h, fr, -1.0, ph, dst, img, R(SEL_WS, ws0 + 0), H, W, 4.0 * h + 1);
+            }
+        } else {
+            need = std::max(need, aux + HW + (int64_t)nh * HW);
+            b.tr(ST_TR_RC, img, R(SEL_WS, ws0 + aux), H, W);
+            std::vector<ColJob<T>> cj;
+            for (int i = 0; i < nh; ++i) {
+                const double phi = w0x * bm.heads[i];
+                const int wo = b.col_weights(wx, t0x, phi);
+                cj.push_back(b.col_job(0, wo, {{aux + HW + (int64_t)i * HW, 1, 0, cd(std::cos(phi * cx), std::sin(phi * cx))}}));
+            }
+            b.col_step(cj, R(SEL_WS, ws0 + aux), R(SEL_WS, ws0 + 0), W, H, t0x, (int)wx.size(), 1, 1, (double)(wx.size() - 1), -1, true);
+            for (int i = 0; i < nh; ++i) b.tr(ST_TR_CC, R(SEL_WS, ws0 + aux + HW + (int64_t)i * HW), R(SEL_WS, ws0 + (int64_t)i * HW), W, H);
+        }
+        // ---- vertical stage + conjugate fills ----
+        std::vector<ColJob<T>> cj_b, cj_nob;
+        int cnt_b = 0, cnt_nob = 0;
+        for (int i = 0; i < nh; ++i) {
+            const int u = bm.heads[i];
+            const int um = (mx - u) % mx;
+            for (int v = 0; v <= my / 2; ++v) {
+                const double phi = w0y * v;
+                const cd P(std::cos(phi * cy), std::sin(phi * cy));
+                const int wo = b.col_weights(wy, t0y, phi);
+                std::vector<typename Builder<T>::Out> outs;
+                outs.push_back({slot(u, v), 1, 0, P});                    // bin(u,v) = P Y
+                const bool mir = (um != u);
+                const bool fill = (v != 0) && (2 * v != my);
+                if (mir) outs.push_back({slot(um, v), 0, 1, P});          // bin(mx-u,v) = P conj X
+                if (fill) outs.push_back({slot(um, my - v), 1, 1, std::conj(P)});  // conj(bin(u,v))
+                if (mir && fill) outs.push_back({slot(u, my - v), 0, 0, std::conj(P)});  // conj(bin(mx-u,v))
+                ColJob<T> job = b.col_job((int64_t)i * HW, wo, outs);
+                if (phi == 0.0) { cj_nob.push_back(job); cnt_nob += 1 + (mir ? 1 : 0); }
+                else { cj_b.push_back(job); cnt_b += 1 + (mir ? 1 : 0); }
+            }
+        }
+        const double sfl = box ? (double)(wy.size() - 1) : 2.0 * wy.size() - 1;
+        b.col_step(cj_b, R(SEL_WS, ws0 + 0), out, H, W, t0y, (int)wy.size(), box ? 1 : 0, 1, sfl, cnt_b);
+        b.col_step(cj_nob, R(SEL_WS, ws0 + 0), out, H, W, t0y, (int)wy.size(), box ? 1 : 0, 0, sfl, cnt_nob);
+    } else {
+        double cf[4];
+        FGB_TRY(iir_coeffs(sigma, cf));
+        IirCoef c{cf[0], cf[1], cf[2], cf[3]};
+        const int P = pad_radius(sm, sigma);
+        need = std::max(need, aux + HW + (int64_t)nh * HW);
+        b.tr(ST_TR_RC, img, R(SEL_WS, ws0 + aux), H, W);
+        std::vector<IirJob<T>> ij;
+        for (int i = 0; i < nh; ++i) {
+            const double phi = w0x * bm.heads[i];
+            IirJob<T> q{};
+            q.src_off = 0;
+            q.tabm_off = b.table(phi, -P, W + 2 * P);
+            q.tabr_off = b.table(phi, -cx, W);
+            q.dst_off[0] = aux + HW + (int64_t)i * HW;
+            q.pair[0] = 1;
+            q.nout = 1;
+            q.need = 2;
+            q.sdft = 1;
+            ij.push_back(q);
+        }
+        b.iir_step(ij, R(SEL_WS, ws0 + aux), R(SEL_WS, ws0 + 0), W, H, P, c, 0, -1, true);
+        for (int i = 0; i < nh; ++i) b.tr(ST_TR_CC, R(SEL_WS, ws0 + aux + HW + (int64_t)i * HW), R(SEL_WS, ws0 + (int64_t)i * HW), W, H);
+        std::vector<IirJob<T>> cj;
+        int cnt = 0;
+        for (int i = 0; i < nh; ++i) {
+            const int u = bm.heads[i];
+            const int um = (mx - u) % mx;
+            for (int v = 0; v <= my / 2; ++v) {
+                const double phi = w0y * v;
+                IirJob<T> q{};
+                q.src_off = (int64_t)i * HW;
+                q.tabm_off = b.table(phi, -P, H + 2 * P);
+                q.tabr_off = b.table(phi, -cy, H);
+                q.sdft = 1;
+                const bool mir = (um != u);
+                const bool fill = (v != 0) && (2 * v != my);
+                auto add = [&](int64_t dst, int pair, int conj) {
+                    q.dst_off[q.nout] = dst;
+                    q.pair[q.nout] = (int8_t)pair;
+                    q.conj[q.nout] = (int8_t)conj;
+                    q.nout++;
+                    q.need |= (1 << pair);
+                };
+                add(slot(u, v), 1, 0);
+                cnt += 1 + (mir ? 1 : 0);
+                if (mir) add(slot(um, v), 0, 0);
+                if (fill) add(slot(um, my - v), 1, 1);
+                if (mir && fill) add(slot(u, my - v), 0, 1);
+                cj.push_back(q);
+            }
+        }
+        b.iir_step(cj, R(SEL_WS, ws0 + 0), out, H, W, P, c, 0, cnt);
+    }
+    *ws_need = std::max(*ws_need, ws0 + need);
+    return FGB_OK;
+}
+
+template <typename T>
+static int32_t build_sdft(Plan<T>& p, const fgb_sdft_desc& d) {
+    Builder<T> b(p);
+    const int H = d.img.height, W = d.img.width;
+    const int64_t HW = (int64_t)H * W;
+    p.H = H;
+    p.W = W;
+    BinMap bm;
+    FGB_TRY(make_binmap(d, &bm));
+    p.out_img_c = bm.nbins * HW;
+    int64_t need = 0;
+    if (d.my >= d.mx) {
+        FGB_TRY(build_sdft_core<T>(b, d, bm, H, W, R(SEL_IMG, 0), R(SEL_OUT, 0), 0, 0, &need));
+    } else {
+        // sdft.py:185-195: transpose, swap extents, transpose bins back.
+        if (d.u_heads) return fail(FGB_EINVAL, "pair-head sharding needs my >= mx");
+        fgb_sdft_desc dt = d;
+        std::swap(dt.mx, dt.my);
+        BinMap bt;
+        FGB_TRY(make_binmap(dt, &bt));
+        // ws layout: [transposed image (real, as HW/2 complex)][bins' planes][core ws]
+        const int64_t img_c = (HW + 1) / 2;
+        const int64_t bins_off = img_c;
+        const int64_t core_off = bins_off + bt.nbins * HW;
+        b.tr(ST_TR_RR, R(SEL_IMG, 0), R(SEL_WSR, 0), H, W);
+        // core on the transposed image (W rows x H cols), its ws after the bins
+        int64_t core_need = 0;
+        FGB_TRY(build_sdft_core<T>(b, dt, bt, W, H, R(SEL_WSR, 0), R(SEL_WS, bins_off), 0, core_off, &core_need));
+        need = core_need;
+        // bins'[v][u] (W x H planes) -> bins[u][v] (H x W)
+        for (int u = 0; u < d.mx; ++u)
+            for (int v = 0; v < d.my; ++v)
+                b.tr(ST_TR_CC, R(SEL_WS, bins_off + ((int64_t)v * d.mx + u) * HW), R(SEL_OUT, ((int64_t)u * d.my + v) * HW), W, H);
+    }
+    p.ws_img_c = need;
+    finish_chunking(p, d.img.batch);
+    return p.upload();
+}
+
+// single bin / horizontal stage, direct (sdft.py:134-175): no reuse.
+template <typename T>
+static int32_t build_sdft_single(Plan<T>& p, const fgb_sdft_desc& d, int u, int v) {
+    Builder<T> b(p);
+    const int H = d.img.height, W = d.img.width;
+    const int64_t HW = (int64_t)H * W;
+    p.H = H;
+    p.W = W;
+    p.out_img_c = HW;
+    const double sigma = sdft_sigma(d);
+    const fgb_smoother& sm = d.smoother;
+    const double phx = 2.0 * M_PI / d.mx * u;
+    const int cx = d.mx / 2, cy = d.my / 2;
+    const bool only_h = v < 0;
+    int64_t need = only_h ? 0 : HW;
+    const Ref jdst = only_h ? R(SEL_OUT, 0) : R(SEL_WS, 0);
+    if (sm.kind == FGB_SMOOTH_FIR) {
+        std::vector<double> w;
+        int t0;
+        sdft_axis_taps(sm, sigma, d.mx, &w, &t0);
+        b.row_group(w, -t0, {phx}, -1.0, {cd(std::cos(phx * cx), std::sin(phx * cx))}, {0}, R(SEL_IMG, 0), jdst, H, W,
+                    2.0 * w.size() - 1);
+    } else if (sm.kind == FGB_SMOOTH_BOX) {
+        std::vector<double> w;
+        int t0;
+        sdft_axis_taps(sm, sigma, d.mx, &w, &t0);
+        const int64_t aux = need;
+        need = aux + 2 * HW;
+        b.tr(ST_TR_RC, R(SEL_IMG, 0), R(SEL_WS, aux), H, W);
+        const int wo = b.col_weights(w, t0, phx);
+        b.col_step({b.col_job(0, wo, {{aux + HW, 1, 0, cd(std::cos(phx * cx), std::sin(phx * cx))}})}, R(SEL_WS, aux),
+                   R(SEL_WS, 0), W, H, t0, (int)w.size(), 1, 1);
+        b.tr(ST_TR_CC, R(SEL_WS, aux + HW), jdst, W, H);
+    } else {
+        double cf[4];
+        FGB_TRY(iir_coeffs(sigma, cf));
+        IirCoef c{cf[0], cf[1], cf[2], cf[3]};
+        const int P = pad_radius(sm, sigma);
+        const int64_t aux = need;
+        need = aux + 2 * HW;
+        b.tr(ST_TR_RC, R(SEL_IMG, 0), R(SEL_WS, aux), H, W);
+        IirJob<T> q{};
+        q.tabm_off = b.table(phx, -P, W + 2 * P);
+        q.tabr_off = b.table(phx, -cx, W);
+        q.dst_off[0] = aux + HW;
+        q.pair[0] = 1;
+        q.nout = 1;
+        q.need = 2;
+        q.sdft = 1;
+        b.iir_step({q}, R(SEL_WS, aux), R(SEL_WS, 0), W, H, P, c, 0);
+        b.tr(ST_TR_CC, R(SEL_WS, aux + HW), jdst, W, H);
+    }
+    if (!only_h) {
+        const double phy = 2.0 * M_PI / d.my * v;
+        const cd Pp(std::cos(phy * cy), std::sin(phy * cy));
+        if (sm.kind == FGB_SMOOTH_IIR) {
+            double cf[4];
+            FGB_TRY(iir_coeffs(sigma, cf));
+            IirCoef c{cf[0], cf[1], cf[2], cf[3]};
+            const int P = pad_radius(sm, sigma);
+            IirJob<T> q{};
+            q.tabm_off = b.table(phy, -P, H + 2 * P);
+            q.tabr_off = b.table(phy, -cy, H);
+            q.pair[0] = 1;
+            q.nout = 1;
+            q.need = 2;
+            q.sdft = 1;
+            b.iir_step({q}, R(SEL_WS, 0), R(SEL_OUT, 0), H, W, P, c, 0);
+        } else {
+            std::vector<double> w;
+            int t0;
+            sdft_axis_taps(sm, sigma, d.my, &w, &t0);
+            const int wo = b.col_weights(w, t0, phy);
+            b.col_step({b.col_job(0, wo, {{0, 1, 0, Pp}})}, R(SEL_WS, 0), R(SEL_OUT, 0), H, W, t0, (int)w.size(),
+                       sm.kind == FGB_SMOOTH_BOX ? 1 : 0, phy != 0.0);
+        }
+    }
+    p.ws_img_c = need;
+    finish_chunking(p, d.img.batch);
+    return p.upload();
+}
+
+// ===========================================================================
+// execution
+// ===========================================================================
+struct Ctx {
+    DevBuf ws;
+    std::map<std::string, std::shared_ptr<PlanBase>> plans;
+    DevBuf hin, hout;  // device staging of the *_host entry points
+};
+static std::mutex g_mu;
+static std::map<int, std::unique_ptr<Ctx>> g_ctx;
+
+// ---- live per-kernel profiling (CUDA events on the launching stream) ----
+struct ProfRec {
+    const char* name;
+    cudaEvent_t e0, e1;
+    double flops, bytes;
+};
+static bool g_prof = false;
+static int64_t g_launches = 0;
+static std::vector<ProfRec> g_prof_pending;
+static std::vector<cudaEvent_t> g_event_pool;
+static cudaEvent_t pool_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+static Ctx& ctx() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto& c = g_ctx[dev];
+    if (!c) c.reset(new Ctx());
+    return *c;
+}
+
+template <typename T>
+static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img, void* out, cudaStream_t s) {
+    using C = cx_t<T>;
+    const int batch = im.batch;
+    const int chunk = std::min(p.chunk, batch);
+    const int64_t ws_img_bytes = p.ws_img_c * (int64_t)sizeof(C);
+    const int64_t scr_bytes = p.scratch_img_t * (int64_t)sizeof(T);
+    FGB_TRY(cx.ws.ensure((size_t)(ws_img_bytes + scr_bytes) * chunk + 256));
+    C* ws = (C*)cx.ws.p;
+    T* scratch = (T*)((char*)cx.ws.p + ws_img_bytes * chunk);
+    const int64_t img_bs = (batch > 1) ? im.batch_stride : (int64_t)im.height * im.pitch;
+    for (int b0 = 0; b0 < batch; b0 += chunk) {
+        const int nb = std::min(chunk, batch - b0);
+        const T* imgb = (const T*)img + (size_t)b0 * img_bs;
+        C* imgcb = (C*)img + (size_t)b0 * img_bs;  // complex inputs: strides in complex elements
+        C* outb = (C*)out + (size_t)b0 * p.out_img_c;
+        auto baseC = [&](const Ref& r) -> C* {
+            switch (r.sel) {
+                case SEL_IMGC: return imgcb + r.off;  // complex input (dense)
+                case SEL_OUT: return outb + r.off;
+                case SEL_WS: return ws + r.off;
+                default: return nullptr;
+            }
+        };
+        auto bsC = [&](const Ref& r) -> int64_t {
+            switch (r.sel) {
+                case SEL_IMGC: return img_bs;
+                case SEL_OUT: return p.out_img_c;
+                default: return p.ws_img_c;
+            }
+        };
+        auto baseT = [&](const Ref& r, int64_t* pitch, int64_t* bs) -> const T* {
+            if (r.sel == SEL_IMG) {
+                *pitch = im.pitch;
+                *bs = img_bs;
+                return imgb + r.off;
+            }
+            // SEL_WSR: real plane inside ws (dense)
+            *bs = 2 * p.ws_img_c;
+            return (const T*)ws + r.off;
+        };
+        for (const Step<T>& st : p.steps) {
+            ProfRec pr{st.name, nullptr, nullptr, st.flops * nb, st.bytes * nb};
+            if (g_prof) {
+                pr.e0 = pool_event();
+                pr.e1 = pool_event();
+                cudaEventRecord(pr.e0, s);
+            }
+            ++g_launches;
+            switch (st.kind) {
+                case ST_ROW: {
+                    RowArgs<T> a{};
+                    int64_t pitch, bs;
+                    a.img = baseT(st.src, &pitch, &bs);
+                    a.pitch = (st.src.sel == SEL_WSR) ? st.W : pitch;
+                    a.img_bstride = bs;
+                    a.dst_base = baseC(st.dst);
+                    a.out_bstride = bsC(st.dst);
+                    a.weights = p.d_wrow();
+                    a.H = st.H;
+                    a.W = st.W;
+                    a.hp = st.hp;
+                    a.batch = nb;
+                    FGB_CUDA(launch_row_sym<T>(a, st.rg, s));
+                    break;
+                }
+                case ST_COL: {
+                    ColArgs<T> a{};
+                    a.jobs = p.d_cjobs() + st.job0;
+                    a.weights = p.d_wcol();
+                    a.src_base = baseC(st.src);
+                    a.dst_base = baseC(st.dst);
+                    a.src_bstride = bsC(st.src);
+                    a.dst_bstride = bsC(st.dst);
+                    a.H = st.H;
+                    a.W = st.W;
+                    a.t0 = st.t0;
+                    a.nt = st.nt;
+                    a.zero_boundary = st.zero_bnd;
+                    a.njobs = st.njobs;
+                    a.batch = nb;
+                    FGB_CUDA(launch_col<T>(a, st.has_b != 0, s));
+                    break;
+                }
+                case ST_IIR: {
+                    IirArgs<T> a{};
+                    a.jobs = p.d_ijobs() + st.job0;
+                    a.tab_base = p.d_tabs();
+                    a.src_base = baseC(st.src);
+                    a.dst_base = baseC(st.dst);
+                    a.src_bstride = bsC(st.src);
+                    a.dst_bstride = bsC(st.dst);
+                    a.scratch = scratch;
+                    a.c = st.coef;
+                    a.H = st.H;
+                    a.W = st.W;
+                    a.P = st.P;
+                    a.njobs = st.njobs;
+                    a.batch = nb;
+                    if ((int64_t)iir_scratch_elems<T>(st.H, st.W, st.P, st.njobs, nb) > p.scratch_img_t * chunk)
+                        return fail(FGB_EINVAL, "internal: IIR scratch too small");
+                    FGB_CUDA(launch_iir_col<T>(a, s));
+                    break;
+                }
+                case ST_TR_RC: {
+                    int64_t pitch, bs;
+                    const T* in = baseT(st.src, &pitch, &bs);
+                    if (st.src.sel == SEL_WSR) pitch = st.W;
+                    FGB_CUDA(launch_transpose_real_to_cx<T>(in, pitch, bs, baseC(st.dst), bsC(st.dst), st.H, st.W, nb, s));
+                    break;
+                }
+                case ST_TR_CC:
+                    FGB_CUDA(launch_transpose_cx<T>(baseC(st.src), bsC(st.src), baseC(st.dst), bsC(st.dst), st.H, st.W,
+                                                    nb, s));
+                    break;
+                case ST_TR_RR: {
+                    int64_t pitch, bs;
+                    const T* in = baseT(st.src, &pitch, &bs);
+                    T* o = (T*)ws + st.dst.off;
+                    FGB_CUDA(launch_transpose_real<T>(in, pitch, bs, o, 2 * p.ws_img_c, st.H, st.W, nb, s));
+                    break;
+                }
+            }
+            if (g_prof) {
+                cudaEventRecord(pr.e1, s);
+                g_prof_pending.push_back(pr);
+            }
+        }
+    }
+    return FGB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plan cache keys
+// ---------------------------------------------------------------------------
+static void key_img(std::ostringstream& k, const fgb_image& im) {
+    k << im.height << 'x' << im.width << 'p' << im.pitch << 'd' << im.dtype << '|';
+}
+static void key_sm(std::ostringstream& k, const fgb_smoother& s) {
+    k.precision(17);
+    k << 's' << s.kind << ',' << s.box_half << ',' << s.radius << '|';
+}
+
+template <typename T, typename BuildF>
+static int32_t get_plan(Ctx& cx, const std::string& key, BuildF bf, Plan<T>** out) {
+    auto it = cx.plans.find(key);
+    if (it != cx.plans.end()) {
+        *out = static_cast<Plan<T>*>(it->second.get());
+        return FGB_OK;
+    }
+    auto p = std::make_shared<Plan<T>>();
+    FGB_TRY(bf(*p));
+    cx.plans[key] = p;
+    *out = p.get();
+    return FGB_OK;
+}
+
+static int32_t validate_bank(const fgb_bank_desc* d) {
+    if (!d) return fail(FGB_EINVAL, "null descriptor");
+    FGB_TRY(check_image(d->img));
+    if (d->orientations < 1) return fail(FGB_EINVAL, "orientation count must be at least 1");
+    if (d->n_freq < 1 || !d->omegas || !d->sigmas)
+        return fail(FGB_EINVAL, "frequencies must be a non-empty list of positive values");
+    for (int i = 0; i < d->n_freq; ++i) {
+        if (!(d->omegas[i] > 0)) return fail(FGB_EINVAL, "frequencies must be a non-empty list of positive values");
+        if (!(d->sigmas[i] > 0)) return fail(FGB_EINVAL, "sigma must be positive");
+        FGB_TRY(check_smoother(d->smoother, d->sigmas[i]));
+    }
+    if (d->units && !d->reuse) return fail(FGB_EINVAL, "work units need reuse mode");
+    return FGB_OK;
+}
+
+template <typename T> static int32_t bank_t(const fgb_bank_desc* d, const void* img, void* out, cudaStream_t s) {
+    std::ostringstream k;
+    k.precision(17);
+    k << "bank|";
+    key_img(k, d->img);
+    key_sm(k, d->smoother);
+    k << d->orientations << '|' << d->reuse << '|' << d->img.batch << '|';
+    for (int i = 0; i < d->n_freq; ++i) k << d->omegas[i] << ',' << d->sigmas[i] << ';';
+    if (d->units)
+        for (int i = 0; i < d->n_units; ++i) k << 'u' << d->units[i];
+    Ctx& cx = ctx();
+    Plan<T>* p;
+    FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_bank<T>(pl, *d); }, &p));
+    return execute<T>(*p, cx, d->img, img, out, s);
+}
+
+static int32_t validate_filter(const fgb_filter_desc* d, bool complex_in) {
+    if (!d) return fail(FGB_EINVAL, "null descriptor");
+    FGB_TRY(check_image(d->img, complex_in));
+    if (!(d->omega > 0)) return fail(FGB_EINVAL, "omega must be positive");
+    if (!(d->sigma > 0)) return fail(FGB_EINVAL, "sigma must be positive");
+    return check_smoother(d->smoother, d->sigma);
+}
+
+template <typename T>
+static int32_t filter_t(const fgb_filter_desc* d, int mode, const void* img, void* out, cudaStream_t s) {
+    std::ostringstream k;
+    k.precision(17);
+    k << "filter|" << mode << '|';
+    key_img(k, d->img);
+    key_sm(k, d->smoother);
+    k << d->omega << ',' << d->theta << ',' << d->sigma << '|' << d->img.batch;
+    Ctx& cx = ctx();
+    Plan<T>* p;
+    FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_filter<T>(pl, *d, mode); }, &p));
+    return execute<T>(*p, cx, d->img, img, out, s);
+}
+
+static int32_t validate_sdft(const fgb_sdft_desc* d) {
+    if (!d) return fail(FGB_EINVAL, "null descriptor");
+    FGB_TRY(check_image(d->img));
+    if (d->mx < 1 || d->my < 1) return fail(FGB_EINVAL, "window extents must be at least 1");
+    if (d->sigma < 0) return fail(FGB_EINVAL, "sigma must be positive");
+    return check_smoother(d->smoother, sdft_sigma(*d));
+}
+
+template <typename T>
+static int32_t sdft_t(const fgb_sdft_desc* d, int u, int v, const void* img, void* out, cudaStream_t s) {
+    std::ostringstream k;
+    k.precision(17);
+    k << "sdft|" << u << ',' << v << '|';
+    key_img(k, d->img);
+    key_sm(k, d->smoother);
+    k << d->mx << ',' << d->my << ',' << sdft_sigma(*d) << '|' << d->img.batch;
+    if (d->u_heads)
+        for (int i = 0; i < d->n_heads; ++i) k << 'h' << d->u_heads[i];
+    Ctx& cx = ctx();
+    Plan<T>* p;
+    if (u < 0) {
+        FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_sdft<T>(pl, *d); }, &p));
+    } else {
+        FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_sdft_single<T>(pl, *d, u, v); }, &p));
+    }
+    return execute<T>(*p, cx, d->img, img, out, s);
+}
+
+}  // namespace fgb
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace fgb;
+
+namespace fgb {
+static size_t elem_size(int32_t dtype) { return dtype == FGB_F64 ? 8 : 4; }
+static size_t img_bytes(const fgb_image& im) {
+    const int64_t bs = im.batch > 1 ? im.batch_stride : (int64_t)im.height * im.pitch;
+    return (size_t)((int64_t)(im.batch - 1) * bs + (int64_t)(im.height - 1) * im.pitch + im.width) * elem_size(im.dtype);
+}
+
+// host-buffer variants: H2D, compute, D2H on one stream (synchronous)
+template <typename F>
+static int32_t host_call(const fgb_image& im, int64_t out_elems_c, const void* in_h, void* out_h, F compute) {
+    Ctx& cx = ctx();
+    const size_t in_b = img_bytes(im);
+    const size_t out_b = (size_t)out_elems_c * 2 * elem_size(im.dtype);
+    FGB_TRY(cx.hin.ensure(in_b));
+    FGB_TRY(cx.hout.ensure(out_b));
+    cudaStream_t s = 0;
+    FGB_CUDA(cudaMemcpyAsync(cx.hin.p, in_h, in_b, cudaMemcpyHostToDevice, s));
+    FGB_TRY(compute(cx.hin.p, cx.hout.p, s));
+    FGB_CUDA(cudaMemcpyAsync(out_h, cx.hout.p, out_b, cudaMemcpyDeviceToHost, s));
+    FGB_CUDA(cudaStreamSynchronize(s));
+    return FGB_OK;
+}
+
+}  // namespace fgb
+
+extern "C" {
+
+const char* fgb_last_error(void) { return g_err.c_str(); }
+int32_t fgb_version(void) { return 1 * 10000 + 0 * 100 + 0; }
+int32_t fgb_device_sm_count(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(FGB_ECUDA, "no CUDA device");
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return fail(FGB_ECUDA, "cudaDeviceGetAttribute failed");
+    return n;
+}
+
+int32_t fgb_pad_radius(const fgb_smoother* kind, double sigma) {
+    if (!kind) return fail(FGB_EINVAL, "null smoother");
+    return pad_radius(*kind, sigma);
+}
+
+int32_t fgb_sampled_gaussian(double sigma, double radius, double* out, int32_t cap, int32_t* half) {
+    if (!(sigma > 0)) return fail(FGB_EINVAL, "sigma must be positive");
+    int h;
+    std::vector<double> w = sampled_gaussian(sigma, radius, &h);
+    if (half) *half = h;
+    if (out) {
+        if (cap < (int32_t)w.size()) return fail(FGB_EINVAL, "output capacity too small");
+        std::memcpy(out, w.data(), w.size() * sizeof(double));
+    }
+    return FGB_OK;
+}
+
+int32_t fgb_iir_coeffs(double sigma, double out[4]) { return iir_coeffs(sigma, out); }
+
+int64_t fgb_bank_entries(const fgb_bank_desc* d) {
+    if (!d) return fail(FGB_EINVAL, "null descriptor");
+    if (!d->units) return (int64_t)d->n_freq * d->orientations;
+    const int N = d->orientations, nh = N / 2;
+    int64_t n = 0;
+    for (int i = 0; i < d->n_units; ++i) {
+        const int k = d->units[i] % (nh + 1);
+        n += 1 + ((nh < N - k && N - k < N) ? 1 : 0);
+    }
+    return n;
+}
+
+int64_t fgb_sdft_bins(const fgb_sdft_desc* d) {
+    if (!d) return fail(FGB_EINVAL, "null descriptor");
+    BinMap bm;
+    int32_t r = make_binmap(*d, &bm);
+    if (r != FGB_OK) return r;
+    return bm.nbins;
+}
+
+int32_t fgb_bank(const fgb_bank_desc* d, const void* img, void* out, void* stream) {
+    FGB_TRY(validate_bank(d));
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    return d->img.dtype == FGB_F32 ? bank_t<float>(d, img, out, s) : bank_t<double>(d, img, out, s);
+}
+
+int32_t fgb_filter(const fgb_filter_desc* d, const void* img, void* out, void* stream) {
+    FGB_TRY(validate_filter(d, false));
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    return d->img.dtype == FGB_F32 ? filter_t<float>(d, 0, img, out, s) : filter_t<double>(d, 0, img, out, s);
+}
+
+int32_t fgb_horizontal_stage(const fgb_filter_desc* d, const void* img, void* j_out, void* stream) {
+    FGB_TRY(validate_filter(d, false));
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    return d->img.dtype == FGB_F32 ? filter_t<float>(d, 1, img, j_out, s) : filter_t<double>(d, 1, img, j_out, s);
+}
+
+int32_t fgb_vertical_stage(const fgb_filter_desc* d, const void* j_in, void* out, int32_t conjugate, void* stream) {
+    FGB_TRY(validate_filter(d, true));
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int mode = conjugate ? 3 : 2;
+    return d->img.dtype == FGB_F32 ? filter_t<float>(d, mode, j_in, out, s) : filter_t<double>(d, mode, j_in, out, s);
+}
+
+int32_t fgb_sdft(const fgb_sdft_desc* d, const void* img, void* out, void* stream) {
+    FGB_TRY(validate_sdft(d));
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    return d->img.dtype == FGB_F32 ? sdft_t<float>(d, -1, -1, img, out, s) : sdft_t<double>(d, -1, -1, img, out, s);
+}
+
+int32_t fgb_sdft_bin(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img, void* out, void* stream) {
+    FGB_TRY(validate_sdft(d));
+    if (u < 0 || u >= d->mx) return fail(FGB_EINVAL, "bin index u=" + std::to_string(u) + " outside [0, " + std::to_string(d->mx) + ")");
+    if (v < 0 || v >= d->my) return fail(FGB_EINVAL, "bin index v=" + std::to_string(v) + " outside [0, " + std::to_string(d->my) + ")");
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, v, img, out, s) : sdft_t<double>(d, u, v, img, out, s);
+}
+
+int32_t fgb_sdft_horizontal(const fgb_sdft_desc* d, int32_t u, const void* img, void* j_out, void* stream) {
+    FGB_TRY(validate_sdft(d));
+    if (u < 0 || u >= d->mx) return fail(FGB_EINVAL, "bin index u=" + std::to_string(u) + " outside [0, " + std::to_string(d->mx) + ")");
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, -1, img, j_out, s) : sdft_t<double>(d, u, -1, img, j_out, s);
+}
+
+int32_t fgb_bank_host(const fgb_bank_desc* d, const void* img_host, void* out_host) {
+    FGB_TRY(validate_bank(d));
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = fgb_bank_entries(d) * (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
+        return d->img.dtype == FGB_F32 ? bank_t<float>(d, i, o, s) : bank_t<double>(d, i, o, s);
+    });
+}
+
+int32_t fgb_filter_host(const fgb_filter_desc* d, const void* img_host, void* out_host) {
+    FGB_TRY(validate_filter(d, false));
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
+        return d->img.dtype == FGB_F32 ? filter_t<float>(d, 0, i, o, s) : filter_t<double>(d, 0, i, o, s);
+    });
+}
+
+int32_t fgb_sdft_host(const fgb_sdft_desc* d, const void* img_host, void* out_host) {
+    FGB_TRY(validate_sdft(d));
+    const int64_t nb = fgb_sdft_bins(d);
+    if (nb < 0) return (int32_t)nb;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = nb * (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
+        return d->img.dtype == FGB_F32 ? sdft_t<float>(d, -1, -1, i, o, s) : sdft_t<double>(d, -1, -1, i, o, s);
+    });
+}
+
+int32_t fgb_horizontal_stage_host(const fgb_filter_desc* d, const void* img_host, void* j_host) {
+    FGB_TRY(validate_filter(d, false));
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, j_host, [&](void* i, void* o, cudaStream_t s) {
+        return d->img.dtype == FGB_F32 ? filter_t<float>(d, 1, i, o, s) : filter_t<double>(d, 1, i, o, s);
+    });
+}
+
+int32_t fgb_vertical_stage_host(const fgb_filter_desc* d, const void* j_host, void* out_host, int32_t conjugate) {
+    FGB_TRY(validate_filter(d, true));
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = (int64_t)d->img.height * d->img.width * d->img.batch;
+    fgb_image cim = d->img;  // complex input: twice the real element count
+    cim.width *= 2;
+    cim.pitch *= 2;
+    cim.batch_stride *= 2;
+    const int mode = conjugate ? 3 : 2;
+    return host_call(cim, n, j_host, out_host, [&](void* i, void* o, cudaStream_t s) {
+        return d->img.dtype == FGB_F32 ? filter_t<float>(d, mode, i, o, s) : filter_t<double>(d, mode, i, o, s);
+    });
+}
+
+int32_t fgb_sdft_bin_host(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img_host, void* out_host) {
+    FGB_TRY(validate_sdft(d));
+    if (u < 0 || u >= d->mx) return fail(FGB_EINVAL, "bin index u=" + std::to_string(u) + " outside [0, " + std::to_string(d->mx) + ")");
+    if (v < 0 || v >= d->my) return fail(FGB_EINVAL, "bin index v=" + std::to_string(v) + " outside [0, " + std::to_string(d->my) + ")");
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
+        return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, v, i, o, s) : sdft_t<double>(d, u, v, i, o, s);
+    });
+}
+
+int32_t fgb_sdft_horizontal_host(const fgb_sdft_desc* d, int32_t u, const void* img_host, void* j_host) {
+    FGB_TRY(validate_sdft(d));
+    if (u < 0 || u >= d->mx) return fail(FGB_EINVAL, "bin index u=" + std::to_string(u) + " outside [0, " + std::to_string(d->mx) + ")");
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, j_host, [&](void* i, void* o, cudaStream_t s) {
+        return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, -1, i, o, s) : sdft_t<double>(d, u, -1, i, o, s);
+    });
+}
+
+int32_t fgb_stream_synchronize(void* stream) {
+    FGB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return FGB_OK;
+}
+
+void fgb_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_prof = on != 0;
+}
+
+int64_t fgb_launch_count(void) { return g_launches; }
+
+int32_t fgb_profile_read(fgb_prof_entry* out, int32_t cap) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    std::vector<fgb_prof_entry> agg;
+    for (ProfRec& r : g_prof_pending) {
+        FGB_CUDA(cudaEventSynchronize(r.e1));
+        float ms = 0.f;
+        FGB_CUDA(cudaEventElapsedTime(&ms, r.e0, r.e1));
+        fgb_prof_entry* e = nullptr;
+        for (auto& a : agg)
+            if (std::strncmp(a.name, r.name, sizeof(a.name)) == 0) e = &a;
+        if (!e) {
+            agg.push_back(fgb_prof_entry{});
+            e = &agg.back();
+            std::strncpy(e->name, r.name, sizeof(e->name) - 1);
+        }
+        e->launches += 1;
+        e->ms += ms;
+        e->flops += r.flops;
+        e->bytes += r.bytes;
+        g_event_pool.push_back(r.e0);
+        g_event_pool.push_back(r.e1);
+    }
+    g_prof_pending.clear();
+    const int n = std::min<int>((int)agg.size(), cap);
+    for (int i = 0; i < n; ++i) out[i] = agg[i];
+    return (int32_t)agg.size();
+}
+
+double fgb_probe_fp32_tflops(void) { return probe_fma_tflops<float>(); }
+double fgb_probe_fp64_tflops(void) { return probe_fma_tflops<double>(); }
+
+void fgb_release_caches(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_ctx.clear();
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// Kernel launch interfaces (internal to libfgb200).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace fgb {
+
+// ---- K1: symmetric-FIR row pass (row_fir.cu) ------------------------------
+template <typename T> struct RowArgs {
+    const T* img;          // real input, batch 0
+    cx_t<T>* dst_base;
+    int64_t pitch;         // elements
+    int64_t img_bstride;   // elements
+    int64_t out_bstride;   // complex elements between images in dst planes
+    const T* weights;      // device weight pool
+    int H, W;
+    int hp;                // half-width padded to a multiple of the row R
+    int batch;
+};
+template <typename T> size_t row_sym_smem(int hp, int nd);
+template <typename T> int row_sym_pad(int h);
+template <typename T> cudaError_t launch_row_sym(const RowArgs<T>& a, const RowGroup<T>& g, cudaStream_t s);
+
+// ---- K2: column pass with two real kernels (col_fir.cu) ------------------
+template <typename T> struct ColArgs {
+    const ColJob<T>* jobs;   // device array [njobs]
+    const cx_t<T>* weights;  // device weight pool of (ka, kb) pairs
+    const cx_t<T>* src_base;
+    cx_t<T>* dst_base;
+    int64_t src_bstride;     // complex elements between images of src planes
+    int64_t dst_bstride;     // complex elements between images of dst planes
+    int H, W;
+    int t0;                  // first tap offset (taps t0 .. t0+nt-1)
+    int nt;                  // number of taps
+    int zero_boundary;       // 0 = replicate rows, 1 = zero outside [0, H)
+    int njobs;
+    int batch;
+};
+// Launch all jobs (same taps range/length, same has_b) in one grid.
+template <typename T> cudaError_t launch_col(const ColArgs<T>& a, bool has_b, cudaStream_t s);
+template <typename T> size_t col_smem(int nt, int groups);
+
+// ---- transposes (transpose.cu) -------------------------------------------
+// real [H][pitch] -> complex [W][H] (imag 0); complex [H][W] -> complex [W][H]
+template <typename T> cudaError_t launch_transpose_real_to_cx(const T* in, int64_t pitch, int64_t in_bstride,
+                                                             cx_t<T>* out, int64_t out_bstride, int H, int W,
+                                                             int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_transpose_real(const T* in, int64_t pitch, int64_t in_bstride, T* out,
+                                                       int64_t out_bstride, int H, int W, int batch, cudaStream_t s);
+template <typename T> cudaError_t launch_transpose_cx(const cx_t<T>* in, int64_t in_bstride, cx_t<T>* out,
+                                                     int64_t out_bstride, int H, int W, int batch, cudaStream_t s);
+
+// ---- fused SDFT for power-of-two windows (sdft_fused.cu) ------------------
+template <typename T> struct SdftFusedArgs {
+    const T* img;
+    int64_t pitch, img_bstride;
+    cx_t<T>* out;            // [bins][H][W] (batch 0)
+    int64_t out_bstride;     // complex elements between images
+    const T* w;              // device: sampled Gaussian w[0..2h]
+    const int32_t* heads;    // device: pair heads u to compute
+    const int32_t* head_slot;// device: output slot of bin row (u,*) and (M-u,*) per head: [2*nheads]
+    int nheads;
+    int H, W, h;
+    int batch;
+};
+template <typename T> cudaError_t launch_sdft_fused(const SdftFusedArgs<T>& a, int M, cudaStream_t s);
+bool sdft_fused_supported(int M, int h, size_t elem);
+
+// ---- IIR (iir.cu) ---------------------------------------------------------
+// Column-direction recursive-Gaussian stage on complex planes, one thread per
+// (column, job): modulate by fp64 trig tables, forward/backward 3rd-order
+// recursion with fp64 state, recombine (gabor.py:135-164, sdft.py:75-131).
+// Modulation pairs of a complex input (jr, ji) with (c, s) = tabm[n]:
+//   pair 0: pa = jr c + ji s, pb = jr s - ji c   (Gabor direct / SDFT mirror)
+//   pair 1: pa = jr c - ji s, pb = jr s + ji c   (Gabor mirror / SDFT bin)
+// Recombination with (c, s) = tabr[y]:
+//   Gabor: re = c Sa + s Sb, im = s Sa - c Sb;  SDFT: re = c Sa + s Sb, im = c Sb - s Sa
+struct IirCoef { double B, a1, a2, a3; };
+template <typename T> struct IirJob {
+    int64_t src_off;         // complex elements from src_base
+    int64_t tabm_off;        // [H + 2P] modulation table (true coordinate y = n - P)
+    int64_t tabr_off;        // [H] recombination table
+    int64_t dst_off[4];
+    int8_t pair[4];
+    int8_t conj[4];
+    int32_t nout;
+    int32_t need;            // bit 0: pair 0 used, bit 1: pair 1 used
+    int32_t sdft;
+    int32_t pad_;
+};
+template <typename T> struct IirArgs {
+    const IirJob<T>* jobs;
+    const double2* tab_base;
+    const cx_t<T>* src_base;
+    cx_t<T>* dst_base;
+    T* scratch;              // [njobs*batch][4][H+2P][W]
+    int64_t src_bstride, dst_bstride;
+    IirCoef c;
+    int H, W, P;
+    int njobs, batch;
+};
+template <typename T> cudaError_t launch_iir_col(const IirArgs<T>& a, cudaStream_t s);
+template <typename T> size_t iir_scratch_elems(int H, int W, int P, int njobs, int batch);
+
+}  // namespace fgb

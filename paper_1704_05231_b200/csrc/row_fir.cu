@@ -1,0 +1,209 @@
+// K1: fused horizontal stage for symmetric FIR taps (ExactFIR / SDFT rows).
+//
+// Reference semantics (gabor.py:107-132, sdft.py:75-131): replicate-pad the
+// row, modulate by cos/sin(freq * x_true), smooth both planes with the
+// sampled Gaussian, crop, recombine.  Folding the modulation/demodulation
+// into the taps gives the exact identity
+//     J(x) = phase * sum_{t=-h..h} w[t] e^{-i s freq t} f[clamp(x+t)]
+// (s = +1 Gabor, s = -1 SDFT; phase = 1 Gabor, e^{i freq c} SDFT), so the
+// kernel needs no per-pixel trig and no large-phase fp32 products.  The
+// Gaussian is even, so taps t and -t share one add/sub of the input pair,
+// and every direct orientation of one frequency (up to kMaxND per launch)
+// shares those adds:  per tap pair 2 FADD + 2*ND FFMA instead of 4*ND FFMA.
+//
+// Layout: CTA = 64 x 4 threads, each thread R=4 consecutive outputs of one
+// row (256 px per CTA row).  The clamped row segment lives in shared memory
+// split into R residue sub-arrays (element i at (i%R)*S + i/R) so the
+// stride-R register windows load conflict-free with immediate offsets.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fgb {
+
+namespace {
+
+constexpr int kRowR = 4;
+constexpr int kRowTX = 64;
+constexpr int kRowTY = 4;
+constexpr int kRowSpan = kRowR * kRowTX;  // outputs per CTA row
+
+template <typename T> __host__ __device__ constexpr int row_stride_mod() { return (128 / (int)sizeof(T)); }
+
+// Sub-array length S >= need with S == banks/R (mod banks): conflict-free stores.
+template <typename T> __host__ __device__ inline int row_sub_len(int need) {
+    const int banks = row_stride_mod<T>();
+    const int want = banks / kRowR;
+    int s = need;
+    int r = ((s - want) % banks + banks) % banks;
+    if (r) s += banks - r;
+    return s;
+}
+
+template <typename T, int ND>
+__global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, RowGroup<T> g) {
+    constexpr int R = kRowR;
+    constexpr int NDP = (ND + 1) & ~1;  // weight rows padded to an even count
+    using C = cx_t<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* wsm = reinterpret_cast<T*>(smem_raw);  // [(hp+1)][NDP][2]
+    const int hp = a.hp;
+    const int nseg = kRowSpan + 2 * hp;
+    const int S = row_sub_len<T>((nseg + R - 1) / R);
+    T* rows = wsm + (size_t)(hp + 1) * NDP * 2;  // [kRowTY][R][S]
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * kRowTX + tx;
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * kRowSpan;
+    const int y = blockIdx.y * kRowTY + ty;
+
+    // weights: global table already laid out [(hp+1)][NDP][2]
+    {
+        const T* wg = a.weights + g.wofs;
+        const int n = (hp + 1) * NDP * 2;
+        for (int i = tid; i < n; i += kRowTX * kRowTY) wsm[i] = wg[i];
+    }
+    T* my = rows + (size_t)ty * R * S;
+    if (y < a.H) {
+        const T* src = a.img + (size_t)b * a.img_bstride + (size_t)y * a.pitch;
+        for (int i = tx; i < nseg; i += kRowTX) {
+            int x = clampi(x0 - hp + i, 0, a.W - 1);
+            my[(i % R) * S + i / R] = __ldg(src + x);
+        }
+    }
+    __syncthreads();
+    if (y >= a.H) return;
+
+    T accr[ND][R], acci[ND][R];
+    // centre tap t = 0: sub-array r, index tx + hp/R
+    {
+        const int base = tx + hp / R;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            T v = my[r * S + base];
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                accr[k][r] = wsm[k * 2] * v;
+                acci[k][r] = T(0);
+            }
+        }
+    }
+    const int nch = hp / R;
+#pragma unroll 1
+    for (int c = 0; c < nch; ++c) {
+        // right window: f[x + r + t], t = 1 + cR + tt  ->  q = r + tt in [0, 2R-2]
+        // left  window: f[x + r - t]                    ->  q' = r - tt + R - 1
+        T rv[2 * R - 1], lv[2 * R - 1];
+        const int rb = tx + hp / R + c;
+        const int lb = tx + hp / R - c - 1;
+#pragma unroll
+        for (int q = 0; q < 2 * R - 1; ++q) {
+            rv[q] = my[((1 + q) % R) * S + rb + (1 + q) / R];
+            lv[q] = my[(q % R) * S + lb + q / R];
+        }
+#pragma unroll
+        for (int tt = 0; tt < R; ++tt) {
+            const T* wrow = wsm + (size_t)(1 + c * R + tt) * NDP * 2;
+            T wr[NDP], wi[NDP];
+#pragma unroll
+            for (int k = 0; k < NDP; k += 2) {
+                if constexpr (sizeof(T) == 4) {
+                    float4 w4 = *reinterpret_cast<const float4*>(wrow + 2 * k);
+                    wr[k] = w4.x; wi[k] = w4.y; wr[k + 1] = w4.z; wi[k + 1] = w4.w;
+                } else {
+                    double2 w0 = *reinterpret_cast<const double2*>(wrow + 2 * k);
+                    double2 w1 = *reinterpret_cast<const double2*>(wrow + 2 * k + 2);
+                    wr[k] = w0.x; wi[k] = w0.y; wr[k + 1] = w1.x; wi[k + 1] = w1.y;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const T p = rv[r + tt], m = lv[r - tt + R - 1];
+                const T s = p + m, d = p - m;
+#pragma unroll
+                for (int k = 0; k < ND; ++k) {
+                    accr[k][r] = fma(wr[k], s, accr[k][r]);
+                    acci[k][r] = fma(wi[k], d, acci[k][r]);
+                }
+            }
+        }
+    }
+
+    const int xb = x0 + R * tx;
+    const size_t ob = (size_t)b * a.out_bstride + (size_t)y * a.W;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+        C* dst = a.dst_base + g.dst_off[k] + ob;
+        C v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            T re = accr[k][r], im = acci[k][r];
+            if (g.has_phase) {
+                const T pr = g.phase_re[k], pi = g.phase_im[k];
+                T nr = pr * re - pi * im;
+                T ni = pr * im + pi * re;
+                re = nr; im = ni;
+            }
+            v[r] = mk<T>(re, im);
+        }
+        if (xb + R <= a.W && (a.W % 2) == 0 && sizeof(T) == 4) {
+            // 2 x 16-byte stores
+            float4* d4 = reinterpret_cast<float4*>(dst + xb);
+            const float* f = reinterpret_cast<const float*>(v);
+            d4[0] = make_float4(f[0], f[1], f[2], f[3]);
+            d4[1] = make_float4(f[4], f[5], f[6], f[7]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (xb + r < a.W) dst[xb + r] = v[r];
+        }
+    }
+}
+
+}  // namespace
+
+template <typename T> size_t row_sym_smem(int hp, int nd) {
+    const int ndp = (nd + 1) & ~1;
+    const int nseg = kRowSpan + 2 * hp;
+    const int S = row_sub_len<T>((nseg + kRowR - 1) / kRowR);
+    return sizeof(T) * ((size_t)(hp + 1) * ndp * 2 + (size_t)kRowTY * kRowR * S);
+}
+
+template <typename T> int row_sym_pad(int h) { return (h + kRowR - 1) / kRowR * kRowR; }
+
+template <typename T, int ND>
+static cudaError_t launch_nd(const RowArgs<T>& a, const RowGroup<T>& g, cudaStream_t s) {
+    const size_t smem = row_sym_smem<T>(a.hp, ND);
+    auto kern = row_sym_kernel<T, ND>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid((a.W + kRowSpan - 1) / kRowSpan, (a.H + kRowTY - 1) / kRowTY, a.batch);
+    dim3 block(kRowTX, kRowTY);
+    kern<<<grid, block, smem, s>>>(a, g);
+    return cudaGetLastError();
+}
+
+template <typename T> cudaError_t launch_row_sym(const RowArgs<T>& a, const RowGroup<T>& g, cudaStream_t s) {
+    switch (g.nd) {
+        case 1: return launch_nd<T, 1>(a, g, s);
+        case 2: return launch_nd<T, 2>(a, g, s);
+        case 3: return launch_nd<T, 3>(a, g, s);
+        case 4: return launch_nd<T, 4>(a, g, s);
+        case 5: return launch_nd<T, 5>(a, g, s);
+        case 6: return launch_nd<T, 6>(a, g, s);
+        case 7: return launch_nd<T, 7>(a, g, s);
+        case 8: return launch_nd<T, 8>(a, g, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template size_t row_sym_smem<float>(int, int);
+template size_t row_sym_smem<double>(int, int);
+template int row_sym_pad<float>(int);
+template int row_sym_pad<double>(int);
+template cudaError_t launch_row_sym<float>(const RowArgs<float>&, const RowGroup<float>&, cudaStream_t);
+template cudaError_t launch_row_sym<double>(const RowArgs<double>&, const RowGroup<double>&, cudaStream_t);
+
+}  // namespace fgb

@@ -1,0 +1,109 @@
+"""Device-tensor API (the "native" throughput path): inputs and outputs stay in
+HBM, calls are stream-ordered on torch's current CUDA stream.
+
+PyTorch is only plumbing here (device memory, streams); the arithmetic runs
+in libfgb200 through the same C ABI the drop-in host API uses.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native as N
+from .bank import BankSpec, bank_desc
+from .sdft import SdftSpec, sdft_desc
+
+
+def _prec(t: torch.Tensor) -> str:
+    if t.dtype == torch.float32:
+        return "f32"
+    if t.dtype == torch.float64:
+        return "f64"
+    raise TypeError(f"image must be float32 or float64, got {t.dtype}")
+
+
+def _cplx(prec: str):
+    return torch.complex64 if prec == "f32" else torch.complex128
+
+
+def _stream(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _check_img(img: torch.Tensor):
+    if not img.is_cuda:
+        raise ValueError("image must be a CUDA tensor")
+    if img.dim() == 2:
+        img = img.unsqueeze(0)
+    if img.dim() != 3 or img.stride(-1) != 1:
+        raise ValueError("image must be [H, W] or [B, H, W] with unit column stride")
+    return img
+
+
+class BankPlan:
+    """Reusable bank call: descriptor built once, output [B, E, H, W] complex."""
+
+    def __init__(self, shape, spec: BankSpec, kind, precision: str = "f32", reuse: bool = True, units=None):
+        b, h, w = shape
+        self.shape = (b, h, w)
+        self.prec = precision
+        self.desc, self._keep = bank_desc(h, w, spec, kind, precision, reuse, batch=b, units=units)
+        self.entries = int(N.check(N.lib.fgb_bank_entries(C.byref(self.desc))))
+
+    def new_output(self, device="cuda") -> torch.Tensor:
+        b, h, w = self.shape
+        return torch.empty((b, self.entries, h, w), dtype=_cplx(self.prec), device=device)
+
+    def __call__(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        img = _check_img(img)
+        if tuple(img.shape) != self.shape:
+            raise ValueError(f"image shape {tuple(img.shape)} != plan shape {self.shape}")
+        if _prec(img) != self.prec:
+            raise ValueError("image dtype does not match the plan precision")
+        self.desc.img.pitch = img.stride(1)
+        self.desc.img.batch_stride = img.stride(0)
+        if out is None:
+            out = self.new_output(img.device)
+        N.check(N.lib.fgb_bank(C.byref(self.desc), C.c_void_p(img.data_ptr()), C.c_void_p(out.data_ptr()),
+                               C.c_void_p(_stream(stream))))
+        return out
+
+
+class SdftPlan:
+    """Reusable SDFT call: output [B, bins, H, W] complex (bins u-major, or compact per pair head)."""
+
+    def __init__(self, shape, spec: SdftSpec, precision: str = "f32", heads=None):
+        b, h, w = shape
+        self.shape = (b, h, w)
+        self.prec = precision
+        self.desc, self._keep = sdft_desc(h, w, spec, precision, batch=b, heads=heads)
+        self.bins = int(N.check(N.lib.fgb_sdft_bins(C.byref(self.desc))))
+
+    def new_output(self, device="cuda") -> torch.Tensor:
+        b, h, w = self.shape
+        return torch.empty((b, self.bins, h, w), dtype=_cplx(self.prec), device=device)
+
+    def __call__(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        img = _check_img(img)
+        if tuple(img.shape) != self.shape:
+            raise ValueError(f"image shape {tuple(img.shape)} != plan shape {self.shape}")
+        self.desc.img.pitch = img.stride(1)
+        self.desc.img.batch_stride = img.stride(0)
+        if out is None:
+            out = self.new_output(img.device)
+        N.check(N.lib.fgb_sdft(C.byref(self.desc), C.c_void_p(img.data_ptr()), C.c_void_p(out.data_ptr()),
+                               C.c_void_p(_stream(stream))))
+        return out
+
+
+def compute_bank(img: torch.Tensor, spec: BankSpec, kind, reuse: bool = True, units=None) -> torch.Tensor:
+    img3 = _check_img(img)
+    return BankPlan(tuple(img3.shape), spec, kind, _prec(img3), reuse, units)(img3)
+
+
+def sdft_full(img: torch.Tensor, spec: SdftSpec, heads=None) -> torch.Tensor:
+    img3 = _check_img(img)
+    return SdftPlan(tuple(img3.shape), spec, _prec(img3), heads)(img3)
