@@ -158,6 +158,9 @@ int32_t fgb_profile_read(fgb_prof_entry* out, int32_t cap);
 int64_t fgb_launch_count(void);      /* kernels launched by this library so far */
 double fgb_probe_fp32_tflops(void);  /* FFMA peak probe (K6), TFLOP/s */
 double fgb_probe_fp64_tflops(void);  /* DFMA peak probe (K6), TFLOP/s */
+/* FMA probe by operand form: mode 0 immediate operands, 1 register operands
+ * with a shared multiplier (operand reuse), 2 three distinct registers. */
+double fgb_probe_fma(int32_t dtype, int32_t mode);
 
 /* ---- synchronisation helper for hosts without a CUDA binding ----------- */
 int32_t fgb_stream_synchronize(void* stream);

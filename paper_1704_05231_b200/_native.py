@@ -121,6 +121,7 @@ _SIGS = {
     "fgb_launch_count": (C.c_int64, []),
     "fgb_probe_fp32_tflops": (C.c_double, []),
     "fgb_probe_fp64_tflops": (C.c_double, []),
+    "fgb_probe_fma": (C.c_double, [C.c_int32, C.c_int32]),
     "fgb_stream_synchronize": (C.c_int32, [_vp]),
     "fgb_release_caches": (None, []),
 }

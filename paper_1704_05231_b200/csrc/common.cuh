@@ -22,6 +22,28 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 __device__ __forceinline__ void st_cs(float2* p, float2 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_cs(double2* p, double2 v) { __stcs(p, v); }
 
+// Asynchronous global->shared copies (LDGSTS): every thread issues all of its
+// tile copies back to back, then waits once -- the tile load costs one
+// memory latency instead of one per row.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+template <int BYTES> __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    if constexpr (BYTES == 4) cp_async4(smem, gmem);
+    else if constexpr (BYTES == 8) cp_async8(smem, gmem);
+    else cp_async16(smem, gmem);
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // Output descriptor of one column job (one J source, up to 4 outputs).
 //   X = A - iB, Y = A + iB with A = sum ka[t] J[y+t], B = sum kb[t] J[y+t];
 //   out_o = phase_o * (conj_o ? conj(base_o) : base_o)
@@ -35,6 +57,8 @@ template <typename T> struct ColJob {
     int32_t nout;
     int8_t base[4];          // 0 = X, 1 = Y
     int8_t conj[4];
+    int32_t has_b;           // kb != 0 (0 for the theta = 0 / v = 0 jobs: A only)
+    int32_t pad_;
 };
 
 // Row job group: up to kMaxND jobs sharing one input row and one symmetric

@@ -35,6 +35,7 @@
 namespace fgb {
 
 template <typename T> double probe_fma_tflops();
+template <typename T> double probe_fma_reg_tflops(int mode);
 
 // ===========================================================================
 // errors
@@ -259,7 +260,7 @@ struct Ref {
     int64_t off = 0;  // elements of the referenced type (T for real, C for complex)
 };
 
-enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR };
+enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF };
 
 template <typename T> struct Step {
     int kind = 0;
@@ -278,6 +279,9 @@ template <typename T> struct Step {
     int P = 0;
     IirCoef coef{};
     int64_t scratch_off = 0;  // T elements into the workspace scratch region
+    // ST_SDFTF
+    int M = 0, h = 0, nheads = 0;
+    int64_t heads_off = 0, slots_off = 0, w_off = 0;
 };
 
 struct PlanBase {
@@ -293,8 +297,9 @@ template <typename T> struct Plan : PlanBase {
     std::vector<ColJob<T>> cjobs;
     std::vector<IirJob<T>> ijobs;
     std::vector<double2> tabs;
+    std::vector<int32_t> ints;
     DevBuf blob;
-    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0;
+    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0, off_ints = 0;
     // workspace per image (bytes), scratch (T elements per image-chunk) and chunking
     int64_t ws_img_c = 0;         // complex elements per image
     int64_t scratch_img_t = 0;    // T elements per image (IIR scratch)
@@ -310,6 +315,7 @@ template <typename T> struct Plan : PlanBase {
         off_cjobs = o; o = al(o + cjobs.size() * sizeof(ColJob<T>));
         off_ijobs = o; o = al(o + ijobs.size() * sizeof(IirJob<T>));
         off_tabs = o; o = al(o + tabs.size() * sizeof(double2));
+        off_ints = o; o = al(o + ints.size() * sizeof(int32_t));
         FGB_TRY(blob.ensure(std::max<size_t>(o, 256)));
         std::vector<char> h(o, 0);
         if (!wrow.empty()) std::memcpy(h.data() + off_wrow, wrow.data(), wrow.size() * sizeof(T));
@@ -317,6 +323,7 @@ template <typename T> struct Plan : PlanBase {
         if (!cjobs.empty()) std::memcpy(h.data() + off_cjobs, cjobs.data(), cjobs.size() * sizeof(ColJob<T>));
         if (!ijobs.empty()) std::memcpy(h.data() + off_ijobs, ijobs.data(), ijobs.size() * sizeof(IirJob<T>));
         if (!tabs.empty()) std::memcpy(h.data() + off_tabs, tabs.data(), tabs.size() * sizeof(double2));
+        if (!ints.empty()) std::memcpy(h.data() + off_ints, ints.data(), ints.size() * sizeof(int32_t));
         FGB_CUDA(cudaMemcpy(blob.p, h.data(), o, cudaMemcpyHostToDevice));
         return FGB_OK;
     }
@@ -325,6 +332,7 @@ template <typename T> struct Plan : PlanBase {
     const ColJob<T>* d_cjobs() const { return (const ColJob<T>*)((char*)blob.p + off_cjobs); }
     const IirJob<T>* d_ijobs() const { return (const IirJob<T>*)((char*)blob.p + off_ijobs); }
     const double2* d_tabs() const { return (const double2*)((char*)blob.p + off_tabs); }
+    const int32_t* d_ints() const { return (const int32_t*)((char*)blob.p + off_ints); }
 };
 
 // ---------------------------------------------------------------------------
@@ -393,10 +401,11 @@ template <typename T> struct Builder {
         int conj;
         cd phase;
     };
-    ColJob<T> col_job(int64_t src_off, int wofs, const std::vector<Out>& outs) {
+    ColJob<T> col_job(int64_t src_off, int wofs, const std::vector<Out>& outs, int has_b = 1) {
         ColJob<T> j{};
         j.src_off = src_off;
         j.wofs = wofs;
+        j.has_b = has_b;
         j.nout = (int)outs.size();
         for (size_t o = 0; o < outs.size(); ++o) {
             j.dst_off[o] = outs[o].dst_off;
@@ -589,8 +598,9 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 std::vector<typename Builder<T>::Out> outs;
                 if (jobs[j].out_direct >= 0) outs.push_back({jobs[j].out_direct, 0, 0, cd(1, 0)});
                 if (jobs[j].out_mirror >= 0) outs.push_back({jobs[j].out_mirror, 1, 1, cd(1, 0)});
-                ColJob<T> job = b.col_job(col_only ? 0 : ws_j0 + (int64_t)j * HW, wo, outs);
-                if (jobs[j].ws == 0.0) cj_nob.push_back(job);
+                ColJob<T> job = b.col_job(col_only ? 0 : ws_j0 + (int64_t)j * HW, wo, outs, jobs[j].ws != 0.0);
+                // theta = 0 (ws = 0) jobs need A only; they share the launch (per-CTA branch)
+                if (jobs[j].ws == 0.0) cj_b.insert(cj_b.begin(), job);
                 else cj_b.push_back(job);
             }
             const Ref src = col_only ? img : R(SEL_WS, 0);
@@ -826,6 +836,41 @@ static int32_t build_sdft_core(Builder<T>& b, const fgb_sdft_desc& d, const BinM
     const int64_t aux = need;
     auto slot = [&](int u, int v) { return out_base + (bm.row_slot.at(u) + v) * HW; };
 
+    if (sm.kind == FGB_SMOOTH_FIR && mx == my && ws0 == 0 && !std::getenv("FGB_SDFT_UNFUSED")) {
+        int h = 0;
+        std::vector<double> w = sampled_gaussian(sigma, sm.radius, &h);
+        if (sdft_fused_supported(mx, h, sizeof(T)) && out.sel == SEL_OUT) {
+            Step<T> st;
+            st.kind = ST_SDFTF;
+            st.name = "sdft_fused";
+            st.H = H;
+            st.W = W;
+            st.src = img;
+            st.dst = out;
+            st.M = mx;
+            st.h = h;
+            st.nheads = nh;
+            st.w_off = (int64_t)b.p.wrow.size();
+            for (double v : w) b.p.wrow.push_back((T)v);
+            while (b.p.wrow.size() % 4) b.p.wrow.push_back((T)0);
+            st.heads_off = (int64_t)b.p.ints.size();
+            for (int u : bm.heads) b.p.ints.push_back(u);
+            st.slots_off = (int64_t)b.p.ints.size();
+            int counted = 0;
+            for (int u : bm.heads) {
+                const int um = (mx - u) % mx;
+                b.p.ints.push_back((int32_t)(out_base / HW + bm.row_slot.at(u)));
+                b.p.ints.push_back(um != u ? (int32_t)(out_base / HW + bm.row_slot.at(um)) : -1);
+                counted += (um != u) ? 2 : 1;
+            }
+            const double T_ = 2.0 * h + 1;
+            st.flops = ((double)nh * (4 * T_ + 6) + (double)counted * (my / 2 + 1) * (4 * T_ + 10)) * HW;
+            st.bytes = (double)HW * sizeof(T) + (double)bm.nbins * HW * sizeof(cx_t<T>);
+            b.p.steps.push_back(st);
+            *ws_need = std::max(*ws_need, (int64_t)0);
+            return FGB_OK;
+        }
+    }
     if (sm.kind == FGB_SMOOTH_FIR || sm.kind == FGB_SMOOTH_BOX) {
         std::vector<double> wx, wy;
         int t0x, t0y;
@@ -877,9 +922,9 @@ static int32_t build_sdft_core(Builder<T>& b, const fgb_sdft_desc& d, const BinM
                 if (mir) outs.push_back({slot(um, v), 0, 1, P});          // bin(mx-u,v) = P conj X
                 if (fill) outs.push_back({slot(um, my - v), 1, 1, std::conj(P)});  // conj(bin(u,v))
                 if (mir && fill) outs.push_back({slot(u, my - v), 0, 0, std::conj(P)});  // conj(bin(mx-u,v))
-                ColJob<T> job = b.col_job((int64_t)i * HW, wo, outs);
-                if (phi == 0.0) { cj_nob.push_back(job); cnt_nob += 1 + (mir ? 1 : 0); }
-                else { cj_b.push_back(job); cnt_b += 1 + (mir ? 1 : 0); }
+                ColJob<T> job = b.col_job((int64_t)i * HW, wo, outs, phi != 0.0);
+                cj_b.push_back(job);
+                cnt_b += 1 + (mir ? 1 : 0);
             }
         }
         const double sfl = box ? (double)(wy.size() - 1) : 2.0 * wy.size() - 1;
@@ -1055,7 +1100,7 @@ static int32_t build_sdft_single(Plan<T>& p, const fgb_sdft_desc& d, int u, int 
             int t0;
             sdft_axis_taps(sm, sigma, d.my, &w, &t0);
             const int wo = b.col_weights(w, t0, phy);
-            b.col_step({b.col_job(0, wo, {{0, 1, 0, Pp}})}, R(SEL_WS, 0), R(SEL_OUT, 0), H, W, t0, (int)w.size(),
+            b.col_step({b.col_job(0, wo, {{0, 1, 0, Pp}}, phy != 0.0)}, R(SEL_WS, 0), R(SEL_OUT, 0), H, W, t0, (int)w.size(),
                        sm.kind == FGB_SMOOTH_BOX ? 1 : 0, phy != 0.0);
         }
     }
@@ -1219,6 +1264,25 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     FGB_CUDA(launch_transpose_cx<T>(baseC(st.src), bsC(st.src), baseC(st.dst), bsC(st.dst), st.H, st.W,
                                                     nb, s));
                     break;
+                case ST_SDFTF: {
+                    SdftFusedArgs<T> a{};
+                    int64_t pitch, bs;
+                    a.img = baseT(st.src, &pitch, &bs);
+                    a.pitch = pitch;
+                    a.img_bstride = bs;
+                    a.out = baseC(st.dst);
+                    a.out_bstride = bsC(st.dst);
+                    a.w = p.d_wrow() + st.w_off;
+                    a.heads = p.d_ints() + st.heads_off;
+                    a.head_slot = p.d_ints() + st.slots_off;
+                    a.nheads = st.nheads;
+                    a.H = st.H;
+                    a.W = st.W;
+                    a.h = st.h;
+                    a.batch = nb;
+                    FGB_CUDA(launch_sdft_fused<T>(a, st.M, s));
+                    break;
+                }
                 case ST_TR_RR: {
                     int64_t pitch, bs;
                     const T* in = baseT(st.src, &pitch, &bs);
@@ -1593,6 +1657,10 @@ int32_t fgb_profile_read(fgb_prof_entry* out, int32_t cap) {
 
 double fgb_probe_fp32_tflops(void) { return probe_fma_tflops<float>(); }
 double fgb_probe_fp64_tflops(void) { return probe_fma_tflops<double>(); }
+double fgb_probe_fma(int32_t dtype, int32_t mode) {
+    if (mode == 0) return dtype == FGB_F64 ? probe_fma_tflops<double>() : probe_fma_tflops<float>();
+    return dtype == FGB_F64 ? probe_fma_reg_tflops<double>(mode) : probe_fma_reg_tflops<float>(mode);
+}
 
 void fgb_release_caches(void) {
     std::lock_guard<std::mutex> lk(g_mu);

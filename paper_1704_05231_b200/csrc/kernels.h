@@ -39,6 +39,7 @@ template <typename T> struct ColArgs {
     int zero_boundary;       // 0 = replicate rows, 1 = zero outside [0, H)
     int njobs;
     int batch;
+    int seg;                 // rows per CTA segment (set by launch_col)
 };
 // Launch all jobs (same taps range/length, same has_b) in one grid.
 template <typename T> cudaError_t launch_col(const ColArgs<T>& a, bool has_b, cudaStream_t s);

@@ -30,7 +30,83 @@ __global__ void __launch_bounds__(256) fma_probe(T* out, int iters, T a, T b) {
     if (s == (T)12345.678) out[threadIdx.x] = s;  // keep the chains alive
 }
 
+// Register-operand FFMA variants: mode 1 = shared multiplier (operand reuse,
+// the pattern of the FIR kernels), mode 2 = distinct multipliers (3 register
+// reads per FFMA).
+__constant__ float c_probe_w32[16];
+__constant__ double c_probe_w64[16];
+template <typename T> __device__ __forceinline__ T cw(int i);
+template <> __device__ __forceinline__ float cw<float>(int i) { return c_probe_w32[i]; }
+template <> __device__ __forceinline__ double cw<double>(int i) { return c_probe_w64[i]; }
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) fma_probe_reg(T* out, int iters, const T* wp) {
+    T acc[8], v[8], w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        acc[i] = (T)(threadIdx.x + i) * (T)1e-3;
+        v[i] = wp[i] + (T)threadIdx.x;
+        w[i] = wp[8 + i] + (T)(threadIdx.x & 1) * (T)1e-7;  // per-thread: forces vector registers
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (MODE == 3)  // multiplier from the constant bank (compile-time offset)
+                    acc[i] = fma(cw<T>(u & 7), v[(i + u) & 7], acc[i]);
+                else
+                    acc[i] = fma(MODE == 1 ? w[u & 7] : w[i], v[(i + u) & 7], acc[i]);
+            }
+        }
+    }
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == (T)12345.678) out[threadIdx.x] = s;
+}
+
 }  // namespace
+
+template <typename T> double probe_fma_reg_tflops(int mode) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    T* out = nullptr;
+    T* wp = nullptr;
+    if (cudaMalloc(&out, 256 * sizeof(T)) != cudaSuccess) return -1.0;
+    if (cudaMalloc(&wp, 16 * sizeof(T)) != cudaSuccess) return -1.0;
+    T hw[16];
+    for (int i = 0; i < 16; ++i) hw[i] = (T)(0.5 + 0.01 * i);
+    cudaMemcpy(wp, hw, sizeof(hw), cudaMemcpyHostToDevice);
+    const int blocks = sms * 8;
+    const int iters = sizeof(T) == 4 ? 4096 : 1024;
+    auto kern = mode == 1 ? fma_probe_reg<T, 1> : (mode == 2 ? fma_probe_reg<T, 2> : fma_probe_reg<T, 3>);
+    if (sizeof(T) == 4) cudaMemcpyToSymbol(c_probe_w32, hw, 16 * sizeof(float));
+    else cudaMemcpyToSymbol(c_probe_w64, hw, 16 * sizeof(double));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    kern<<<blocks, 256>>>(out, 64, wp);
+    double best = 0.0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        kern<<<blocks, 256>>>(out, iters, wp);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double fmas = (double)blocks * 256 * iters * 16 * 8;
+        best = std::max(best, 2.0 * fmas / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    cudaFree(wp);
+    return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
+template double probe_fma_reg_tflops<float>(int);
+template double probe_fma_reg_tflops<double>(int);
 
 // Returns achieved FMA throughput in TFLOP/s (2 flops per FMA), best of 5.
 template <typename T> double probe_fma_tflops() {

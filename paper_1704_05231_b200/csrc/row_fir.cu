@@ -59,18 +59,21 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, 
 
     // weights: global table already laid out [(hp+1)][NDP][2]
     {
+        // [(hp+1)][NDP][2] table: a multiple of 16 bytes, 16-byte aligned
         const T* wg = a.weights + g.wofs;
-        const int n = (hp + 1) * NDP * 2;
-        for (int i = tid; i < n; i += kRowTX * kRowTY) wsm[i] = wg[i];
+        constexpr int per16 = 16 / sizeof(T);
+        const int n = (hp + 1) * NDP * 2 / per16;
+        for (int i = tid; i < n; i += kRowTX * kRowTY) cp_async16(wsm + i * per16, wg + i * per16);
     }
     T* my = rows + (size_t)ty * R * S;
     if (y < a.H) {
         const T* src = a.img + (size_t)b * a.img_bstride + (size_t)y * a.pitch;
         for (int i = tx; i < nseg; i += kRowTX) {
             int x = clampi(x0 - hp + i, 0, a.W - 1);
-            my[(i % R) * S + i / R] = __ldg(src + x);
+            cp_async<sizeof(T)>(my + (i % R) * S + i / R, src + x);
         }
     }
+    cp_async_wait_all();
     __syncthreads();
     if (y >= a.H) return;
 
