@@ -25,6 +25,7 @@
 // parameter so no taps are padded.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -37,9 +38,8 @@ template <typename T> struct ColCfg;
 template <> struct ColCfg<float> { static constexpr int R = 8; };
 template <> struct ColCfg<double> { static constexpr int R = 4; };
 
-template <typename T, int R, int REM, bool HASB>
-__device__ __forceinline__ void col_accumulate(const cx_t<T>* tb, const cx_t<T>* wts, int nt, T* Ar, T* Ai, T* Br,
-                                               T* Bi) {
+template <typename T, int R, int REM, bool HASB, typename WF>
+__device__ __forceinline__ void col_accumulate(const cx_t<T>* tb, WF wts, int nt, T* Ar, T* Ai, T* Br, T* Bi) {
     using C = cx_t<T>;
     const int nfull = (nt - REM) / R;
 #pragma unroll 1
@@ -49,7 +49,7 @@ __device__ __forceinline__ void col_accumulate(const cx_t<T>* tb, const cx_t<T>*
         for (int m = 0; m < 2 * R - 1; ++m) v[m] = tb[(c * R + m) * 32];
 #pragma unroll
         for (int tt = 0; tt < R; ++tt) {
-            const C w = wts[c * R + tt];
+            const C w = wts(c * R + tt);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 Ar[r] = fma(w.x, v[r + tt].x, Ar[r]);
@@ -68,7 +68,7 @@ __device__ __forceinline__ void col_accumulate(const cx_t<T>* tb, const cx_t<T>*
         for (int m = 0; m < R + REM - 1; ++m) v[m] = tb[(c * R + m) * 32];
 #pragma unroll
         for (int tt = 0; tt < REM; ++tt) {
-            const C w = wts[c * R + tt];
+            const C w = wts(c * R + tt);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 Ar[r] = fma(w.x, v[r + tt].x, Ar[r]);
@@ -95,8 +95,14 @@ __device__ __forceinline__ void cp_async_wait_pending(int n) {
     }
 }
 
-template <typename T, int REM>
-__global__ void __launch_bounds__(256) col_kernel(ColArgs<T> a) {
+// CAP > 0: the launch's tap pairs travel in the kernel parameters (constant
+// bank); the warp-uniform (ka, kb) loads become uniform-register operands
+// of the FFMAs, which then read only two vector registers (measured on
+// B200: 72.6 TFLOP/s vs 60.6 with a register multiplier).  CAP == 0: taps
+// staged in shared memory (many jobs / long kernels).
+template <typename T, int REM, int CAP>
+__global__ void __launch_bounds__(256) col_kernel(const __grid_constant__ ColArgs<T> a,
+                                                  const __grid_constant__ ColWParam<T, CAP> pw) {
     constexpr int R = ColCfg<T>::R;
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__(256) col_kernel(ColArgs<T> a) {
     const int nt = a.nt;
     const int S = a.seg;
     C* wts = reinterpret_cast<C*>(smem_raw);
-    C* tile = wts + ((nt + 1) & ~1);
+    C* tile = CAP > 0 ? wts : wts + ((nt + 1) & ~1);
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * 32 + tx;
@@ -136,8 +142,10 @@ __global__ void __launch_bounds__(256) col_kernel(ColArgs<T> a) {
     }
 
     {
-        const C* wg = a.weights + wofs;
-        for (int i = tid; i < nt; i += 32 * G) cp_async<sizeof(C)>(wts + i, wg + i);
+        if (CAP == 0) {
+            const C* wg = a.weights + wofs;
+            for (int i = tid; i < nt; i += 32 * G) cp_async<sizeof(C)>(wts + i, wg + i);
+        }
         const C* src = a.src_base + src_off + (size_t)b * a.src_bstride + xc;
         for (int ch = 0; ch < nch; ++ch) {
             const int j0 = ch == 0 ? 0 : ch * TY + nt - 1;
@@ -163,8 +171,16 @@ __global__ void __launch_bounds__(256) col_kernel(ColArgs<T> a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) { Ar[r] = Ai[r] = Br[r] = Bi[r] = T(0); }
         const C* tb = tile + (ch * TY + ty * R) * 32 + tx;
-        if (has_b) col_accumulate<T, R, REM, true>(tb, wts, nt, Ar, Ai, Br, Bi);
-        else col_accumulate<T, R, REM, false>(tb, wts, nt, Ar, Ai, Br, Bi);
+        if constexpr (CAP > 0) {
+            const int pbase = job * nt;
+            auto wf = [&](int i) { return pw.w[pbase + i]; };
+            if (has_b) col_accumulate<T, R, REM, true>(tb, wf, nt, Ar, Ai, Br, Bi);
+            else col_accumulate<T, R, REM, false>(tb, wf, nt, Ar, Ai, Br, Bi);
+        } else {
+            auto wf = [&](int i) { return wts[i]; };
+            if (has_b) col_accumulate<T, R, REM, true>(tb, wf, nt, Ar, Ai, Br, Bi);
+            else col_accumulate<T, R, REM, false>(tb, wf, nt, Ar, Ai, Br, Bi);
+        }
         if (x < a.W) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -191,81 +207,313 @@ __global__ void __launch_bounds__(256) col_kernel(ColArgs<T> a) {
     }
 }
 
-template <typename T, int REM>
-cudaError_t launch_rem(const ColArgs<T>& a, int G, size_t smem, cudaStream_t s) {
-    auto kern = col_kernel<T, REM>;
+// fp32 variant with two adjacent columns per thread: J pairs move as 16-byte
+// cp.async / LDS.128 / STG.128, halving load, weight and store instructions
+// per FFMA (needs an even W).  CTA = 64 columns x G row groups.
+template <int R, int REM, bool HASB, int RS, typename WF>
+__device__ __forceinline__ void col_accumulate2(const float4* tb, WF wts, int nt, float (&Ar)[2][R], float (&Ai)[2][R],
+                                                float (&Br)[2][R], float (&Bi)[2][R]) {
+    const int nfull = (nt - REM) / R;
+#pragma unroll 1
+    for (int c = 0; c < nfull; ++c) {
+        float4 v[2 * R - 1];
+#pragma unroll
+        for (int m = 0; m < 2 * R - 1; ++m) v[m] = tb[(c * R + m) * RS];
+#pragma unroll
+        for (int tt = 0; tt < R; ++tt) {
+            const float2 w = wts(c * R + tt);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const float4 q = v[r + tt];
+                Ar[0][r] = fmaf(w.x, q.x, Ar[0][r]);
+                Ai[0][r] = fmaf(w.x, q.y, Ai[0][r]);
+                Ar[1][r] = fmaf(w.x, q.z, Ar[1][r]);
+                Ai[1][r] = fmaf(w.x, q.w, Ai[1][r]);
+                if (HASB) {
+                    Br[0][r] = fmaf(w.y, q.x, Br[0][r]);
+                    Bi[0][r] = fmaf(w.y, q.y, Bi[0][r]);
+                    Br[1][r] = fmaf(w.y, q.z, Br[1][r]);
+                    Bi[1][r] = fmaf(w.y, q.w, Bi[1][r]);
+                }
+            }
+        }
+    }
+    if constexpr (REM > 0) {
+        const int c = nfull;
+        float4 v[R + REM - 1];
+#pragma unroll
+        for (int m = 0; m < R + REM - 1; ++m) v[m] = tb[(c * R + m) * RS];
+#pragma unroll
+        for (int tt = 0; tt < REM; ++tt) {
+            const float2 w = wts(c * R + tt);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const float4 q = v[r + tt];
+                Ar[0][r] = fmaf(w.x, q.x, Ar[0][r]);
+                Ai[0][r] = fmaf(w.x, q.y, Ai[0][r]);
+                Ar[1][r] = fmaf(w.x, q.z, Ar[1][r]);
+                Ai[1][r] = fmaf(w.x, q.w, Ai[1][r]);
+                if (HASB) {
+                    Br[0][r] = fmaf(w.y, q.x, Br[0][r]);
+                    Bi[0][r] = fmaf(w.y, q.y, Bi[0][r]);
+                    Br[1][r] = fmaf(w.y, q.z, Br[1][r]);
+                    Bi[1][r] = fmaf(w.y, q.w, Bi[1][r]);
+                }
+            }
+        }
+    }
+}
+
+// CP = column pairs per CTA (16 -> 32 columns, 8 -> 16 columns for long
+// kernels whose (S + nt - 1)-row tile would otherwise limit occupancy).
+template <int REM, int CAP, int CP>
+__global__ void __launch_bounds__(128) col_kernel2(const __grid_constant__ ColArgs<float> a,
+                                                   const __grid_constant__ ColWParam<float, CAP> pw) {
+    constexpr int R = 8;
+    constexpr int RGW = 32 / CP;  // row groups per warp
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // warp = CP column pairs x RGW row groups; CTA = 2 CP columns x (RGW G) row groups
+    const int G2 = RGW * blockDim.y;
+    const int TY = G2 * R;
+    const int nt = a.nt;
+    const int S = a.seg;
+    float2* wts = reinterpret_cast<float2*>(smem_raw);
+    float4* tile = reinterpret_cast<float4*>(CAP > 0 ? smem_raw : smem_raw + sizeof(float2) * ((nt + 1) & ~1));
+
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int cx = threadIdx.x % CP;                        // column pair
+    const int rg = threadIdx.x / CP + RGW * threadIdx.y;    // row group
+    const int job = blockIdx.z % a.njobs;
+    const int b = blockIdx.z / a.njobs;
+    const ColJob<float>* jb = a.jobs + job;
+    const int x = blockIdx.x * 2 * CP + 2 * cx;  // first of the two columns
+    const int ys = blockIdx.y * S;
+    const int rows_out = min(S, a.H - ys);
+    const int nch = (rows_out + TY - 1) / TY;
+    const int H = a.H, W = a.W;
+
+    const int64_t src_off = jb->src_off;
+    const int wofs = jb->wofs;
+    const int has_b = jb->has_b;
+    const int nout = jb->nout;
+    // output o: re = Ar + sa*Bi, im = sc*Ai + sd*Br, then * phase (if not 1)
+    float sa[4], sc[4], sd[4], phr[4], phi[4];
+    int64_t doff[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        const int yb = jb->base[o], cj = jb->conj[o];
+        sa[o] = yb ? -1.f : 1.f;
+        sc[o] = cj ? -1.f : 1.f;
+        sd[o] = (yb ? 1.f : -1.f) * (cj ? -1.f : 1.f);
+        phr[o] = jb->phase_re[o];
+        phi[o] = jb->phase_im[o];
+        doff[o] = jb->dst_off[o];
+    }
+
+    {
+        if (CAP == 0) {
+            const float2* wg = a.weights + wofs;
+            for (int i = tid; i < nt; i += 32 * blockDim.y) cp_async<8>(wts + i, wg + i);
+        }
+        // loader mapping: CP threads per tile row
+        const int lc = tid % CP, lr = tid / CP, lstep = (32 * blockDim.y) / CP;
+        const int xl = blockIdx.x * 2 * CP + 2 * lc;
+        const float2* src = a.src_base + src_off + (size_t)b * a.src_bstride + (xl < W ? xl : W - 2);
+        const int r0 = ys + a.t0;  // image row of tile row 0
+        const bool interior = r0 >= 0 && r0 + rows_out + nt - 1 <= H && !a.zero_boundary;
+        for (int ch = 0; ch < nch; ++ch) {
+            const int j0 = ch == 0 ? 0 : ch * TY + nt - 1;
+            const int j1 = min((ch + 1) * TY, rows_out) + nt - 1;
+            if (interior) {
+                const float2* p = src + (size_t)(r0 + j0 + lr) * W;
+                for (int j = j0 + lr; j < j1; j += lstep, p += (size_t)lstep * W) cp_async16(tile + j * CP + lc, p);
+            } else {
+                for (int j = j0 + lr; j < j1; j += lstep) {
+                    int yy = r0 + j;
+                    if (a.zero_boundary && (yy < 0 || yy >= H)) {
+                        tile[j * CP + lc] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    } else {
+                        yy = clampi(yy, 0, H - 1);
+                        cp_async16(tile + j * CP + lc, src + (size_t)yy * W);
+                    }
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
+    }
+
+    float2* dst = a.dst_base + (size_t)b * a.dst_bstride + x;
+    for (int ch = 0; ch < nch; ++ch) {
+        cp_async_wait_pending(min(nch - 1 - ch, 7));
+        __syncthreads();
+        float Ar[2][R], Ai[2][R], Br[2][R], Bi[2][R];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int r = 0; r < R; ++r) { Ar[q][r] = Ai[q][r] = Br[q][r] = Bi[q][r] = 0.f; }
+        const float4* tb = tile + (ch * TY + rg * R) * CP + cx;
+        if constexpr (CAP > 0) {
+            const int pbase = job * nt;
+            auto wf = [&](int i) { return pw.w[pbase + i]; };
+            if (has_b) col_accumulate2<R, REM, true, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
+            else col_accumulate2<R, REM, false, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
+        } else {
+            auto wf = [&](int i) { return wts[i]; };
+            if (has_b) col_accumulate2<R, REM, true, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
+            else col_accumulate2<R, REM, false, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
+        }
+        if (x < W) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int yl = ch * TY + rg * R + r;
+                if (yl >= rows_out) break;
+                float2* drow = dst + (size_t)(ys + yl) * W;
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    if (o >= nout) break;
+                    float v[4];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        float re = fmaf(sa[o], Bi[q][r], Ar[q][r]);
+                        float im = fmaf(sd[o], Br[q][r], sc[o] * Ai[q][r]);
+                        if (phi[o] != 0.f || phr[o] != 1.f) {
+                            const float orr = phr[o] * re - phi[o] * im;
+                            im = phr[o] * im + phi[o] * re;
+                            re = orr;
+                        }
+                        v[2 * q] = re;
+                        v[2 * q + 1] = im;
+                    }
+                    __stcs(reinterpret_cast<float4*>(drow + doff[o]), make_float4(v[0], v[1], v[2], v[3]));
+                }
+            }
+        }
+    }
+}
+
+template <typename T, int REM, int CAP>
+cudaError_t launch_cap(const ColArgs<T>& a, const cx_t<T>* pw_host, int G, size_t smem, cudaStream_t s) {
+    auto kern = col_kernel<T, REM, CAP>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
+    static ColWParam<T, CAP> pw;  // host staging of the parameter block (launches are serialised by the engine lock)
+    if constexpr (CAP > 0) std::memcpy(pw.w, pw_host, sizeof(cx_t<T>) * (size_t)a.njobs * a.nt);
     dim3 grid((a.W + 31) / 32, (a.H + a.seg - 1) / a.seg, a.njobs * a.batch);
-    kern<<<grid, dim3(32, G), smem, s>>>(a);
+    kern<<<grid, dim3(32, G), smem, s>>>(a, pw);
     return cudaGetLastError();
+}
+
+template <int REM, int CAP>
+cudaError_t launch_cap2(const ColArgs<float>& a, const float2* pw_host, int G, size_t smem, cudaStream_t s) {
+    auto kern = a.col2 == 2 ? col_kernel2<REM, CAP, 8> : col_kernel2<REM, CAP, 16>;
+    const int cw = a.col2 == 2 ? 16 : 32;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    static ColWParam<float, CAP> pw;
+    if constexpr (CAP > 0) std::memcpy(pw.w, pw_host, sizeof(float2) * (size_t)a.njobs * a.nt);
+    dim3 grid((a.W + cw - 1) / cw, (a.H + a.seg - 1) / a.seg, a.njobs * a.batch);
+    kern<<<grid, dim3(32, G), smem, s>>>(a, pw);
+    return cudaGetLastError();
+}
+
+template <typename T, int REM>
+cudaError_t launch_rem(const ColArgs<T>& a, const cx_t<T>* pw_host, int G, size_t smem, cudaStream_t s) {
+    const size_t need = (size_t)a.njobs * a.nt;
+    if constexpr (sizeof(T) == 4) {
+        if (a.col2) {
+            // two columns per thread, 32-column tiles (same footprint as the 1-column tile)
+            const size_t tile2 = smem;
+            if (pw_host && need <= (size_t)ColWCap<T>::kSmall) return launch_cap2<REM, ColWCap<T>::kSmall>(a, pw_host, G, tile2, s);
+            if (pw_host && need <= (size_t)ColWCap<T>::kLarge) return launch_cap2<REM, ColWCap<T>::kLarge>(a, pw_host, G, tile2, s);
+            return launch_cap2<REM, 0>(a, nullptr, G, tile2 + sizeof(float2) * ((a.nt + 1) & ~1), s);
+        }
+    }
+    if (pw_host && need <= (size_t)ColWCap<T>::kSmall) return launch_cap<T, REM, ColWCap<T>::kSmall>(a, pw_host, G, smem, s);
+    if (pw_host && need <= (size_t)ColWCap<T>::kLarge) return launch_cap<T, REM, ColWCap<T>::kLarge>(a, pw_host, G, smem, s);
+    return launch_cap<T, REM, 0>(a, nullptr, G, smem + sizeof(cx_t<T>) * ((a.nt + 1) & ~1), s);
 }
 
 int g_sm_count = 0;
 
 }  // namespace
 
-template <typename T> size_t col_smem(int nt, int rows) {
-    return sizeof(cx_t<T>) * ((size_t)((nt + 1) & ~1) + (size_t)(rows + nt - 1) * 32);
+template <typename T> size_t col_smem(int nt, int rows) {  // tile only (+ taps when not in params)
+    return sizeof(cx_t<T>) * ((size_t)(rows + nt - 1) * 32);
 }
 
-template <typename T> cudaError_t launch_col(const ColArgs<T>& a_in, bool has_b, cudaStream_t s) {
+template <typename T> cudaError_t launch_col(const ColArgs<T>& a_in, const cx_t<T>* pw_host, cudaStream_t s) {
     constexpr int R = ColCfg<T>::R;
-    (void)has_b;
     ColArgs<T> a = a_in;
     if (g_sm_count == 0) {
         int dev = 0;
         g_sm_count = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    int G = 8;
-    const size_t cols = (size_t)((a.W + 31) / 32) * a.njobs * a.batch;
-    while (G > 1 && cols * ((a.H + G * R - 1) / (G * R)) < 2 * (size_t)g_sm_count) G /= 2;
-    const int TY = G * R;
-    // segment length S in {TY, 2TY, .., 8TY}: minimise waves x per-CTA work
+    const bool c2ok = (sizeof(T) == 4 && a.W % 2 == 0 && a.W >= 2 && !std::getenv("FGB_COL1"));
+    // candidates: (mode, S) with mode 0 = 1 column/thread (32-col tiles, G=8),
+    // 1 = 2 columns/thread 32-col tiles, 2 = 2 columns/thread 16-col tiles (G=4)
     double best = 1e300;
-    int bestS = 0;
-    const int hr = (a.H + TY - 1) / TY * TY;
-    for (int k = 1; k <= 8; k *= 2) {
-        const int S = k * TY;
-        if (S > hr && k > 1) break;
-        const size_t smem = col_smem<T>(a.nt, S);
-        if (smem > 200 * 1024) break;
-        const int per_sm_smem = (int)((227 * 1024) / (smem + 1024));
-        const int per_sm_thr = 2048 / (32 * G);
-        const int per_sm = std::max(1, std::min(per_sm_smem, per_sm_thr));
-        if (per_sm < 2 && k > 1) break;  // keep >= 2 CTAs per SM for latency hiding
-        // throughput-bound SMs: time ~ (CTAs on the busiest SM) x per-CTA work
-        const double ctas = (double)cols * ((a.H + S - 1) / S);
-        const double per_sm_ctas = std::ceil(ctas / g_sm_count);
-        const double work = (double)S * a.nt + 6.0 * (S + a.nt - 1) + 16.0 * S;  // fma + loads + epilogue
-        const double cost = per_sm_ctas * work;
-        if (cost < best * 0.999) {
-            best = cost;
-            bestS = S;
+    int bestS = 0, bestMode = c2ok ? 1 : 0, bestG = c2ok ? 4 : 8;
+    for (int mode = c2ok ? 1 : 0; mode <= (c2ok ? 2 : 0); ++mode) {
+        const int cw = mode == 2 ? 16 : 32;
+        int G = mode == 0 ? 8 : 4;
+        const size_t cols = (size_t)((a.W + cw - 1) / cw) * a.njobs * a.batch;
+        if (mode == 0)
+            while (G > 1 && cols * ((a.H + G * R - 1) / (G * R)) < 2 * (size_t)g_sm_count) G /= 2;
+        const int TY = mode == 0 ? G * R : (32 / (cw / 2)) * G * R;
+        const size_t rowb = (size_t)cw * sizeof(cx_t<T>);
+        const int hr = (a.H + TY - 1) / TY * TY;
+        for (int k = 1; k <= 8; k *= 2) {
+            const int S = k * TY;
+            if (S > hr && k > 1) break;
+            const size_t smem = rowb * (size_t)(S + a.nt - 1);
+            if (smem > 200 * 1024) break;
+            const int per_sm_smem = (int)((227 * 1024) / (smem + 1024));
+            const int per_sm_thr = mode == 0 ? 2048 / (32 * G) : 5;  // ~96 registers x 128 threads
+            const int per_sm = std::max(1, std::min(per_sm_smem, per_sm_thr));
+            if (per_sm < 2 && k > 1) break;
+            const double ctas = (double)cols * ((a.H + S - 1) / S);
+            const double per_sm_ctas = std::ceil(ctas / g_sm_count);
+            // per-CTA work in "FFMA-slot" units: taps x rows x columns, halo loads, epilogue;
+            // few resident warps issue slower (~2 warps/scheduler is ~85%)
+            const double warps = (double)per_sm * G;
+            const double issue = warps >= 16 ? 1.0 : (warps >= 12 ? 0.95 : (warps >= 8 ? 0.88 : 0.75));
+            const double work = ((double)S * a.nt * cw + 6.0 * (S + a.nt - 1) * cw + 16.0 * S * cw) / issue;
+            const double cost = per_sm_ctas * work;
+            if (cost < best * 0.999) {
+                best = cost;
+                bestS = S;
+                bestMode = mode;
+                bestG = G;
+            }
         }
     }
+    a.col2 = bestMode;
+    const int G = bestG;
+    const int TY = bestMode == 0 ? G * R : (bestMode == 2 ? 4 : 2) * G * R;
     if (bestS == 0) {
         if (col_smem<T>(a.nt, TY) > 220 * 1024) return cudaErrorInvalidConfiguration;
         bestS = TY;
     }
     a.seg = bestS;
-    const size_t smem = col_smem<T>(a.nt, bestS);
+    const size_t smem = col_smem<T>(a.nt, bestS) / (bestMode == 2 ? 2 : 1);
     switch (a.nt % R) {
-        case 0: return launch_rem<T, 0>(a, G, smem, s);
-        case 1: return launch_rem<T, 1>(a, G, smem, s);
-        case 2: return launch_rem<T, 2>(a, G, smem, s);
-        case 3: return launch_rem<T, 3>(a, G, smem, s);
+        case 0: return launch_rem<T, 0>(a, pw_host, G, smem, s);
+        case 1: return launch_rem<T, 1>(a, pw_host, G, smem, s);
+        case 2: return launch_rem<T, 2>(a, pw_host, G, smem, s);
+        case 3: return launch_rem<T, 3>(a, pw_host, G, smem, s);
         default: break;
     }
     if constexpr (R > 4) {
         switch (a.nt % R) {
-            case 4: return launch_rem<T, 4 % R>(a, G, smem, s);
-            case 5: return launch_rem<T, 5 % R>(a, G, smem, s);
-            case 6: return launch_rem<T, 6 % R>(a, G, smem, s);
-            case 7: return launch_rem<T, 7 % R>(a, G, smem, s);
+            case 4: return launch_rem<T, 4 % R>(a, pw_host, G, smem, s);
+            case 5: return launch_rem<T, 5 % R>(a, pw_host, G, smem, s);
+            case 6: return launch_rem<T, 6 % R>(a, pw_host, G, smem, s);
+            case 7: return launch_rem<T, 7 % R>(a, pw_host, G, smem, s);
             default: break;
         }
     }
@@ -274,7 +522,7 @@ template <typename T> cudaError_t launch_col(const ColArgs<T>& a_in, bool has_b,
 
 template size_t col_smem<float>(int, int);
 template size_t col_smem<double>(int, int);
-template cudaError_t launch_col<float>(const ColArgs<float>&, bool, cudaStream_t);
-template cudaError_t launch_col<double>(const ColArgs<double>&, bool, cudaStream_t);
+template cudaError_t launch_col<float>(const ColArgs<float>&, const float2*, cudaStream_t);
+template cudaError_t launch_col<double>(const ColArgs<double>&, const double2*, cudaStream_t);
 
 }  // namespace fgb

@@ -67,6 +67,30 @@ static int pad_radius(const fgb_smoother& k, double sigma) {
     return 0;
 }
 
+// numpy's pairwise summation (np.add.reduce on a contiguous float64 array):
+// 8-way unrolled blocks of <= 128, recursive halving above.  Reproducing it
+// makes the tap weights bit-identical to the reference's kernel.sum().
+static double np_pairwise_sum(const double* a, size_t n) {
+    if (n < 8) {
+        double res = 0.;
+        for (size_t i = 0; i < n; ++i) res += a[i];
+        return res;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        size_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    size_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
 // gaussian.py:188-195: unit-sum sampled Gaussian on [-h, h].
 static std::vector<double> sampled_gaussian(double sigma, double radius, int* half) {
     const int h = std::max(1, (int)std::ceil(radius * sigma));
@@ -75,14 +99,7 @@ static std::vector<double> sampled_gaussian(double sigma, double radius, int* ha
         const double x = (double)(i - h);
         w[i] = std::exp(-(x * x) / (2.0 * sigma * sigma));
     }
-    // pairwise sum (numpy's summation order for small arrays is blocked; the
-    // difference is an ulp-level scale of all taps)
-    double s = 0.0, c = 0.0;
-    for (double v : w) {  // Kahan: sum to ~1 ulp
-        double y = v - c, t = s + y;
-        c = (t - s) - y;
-        s = t;
-    }
+    const double s = np_pairwise_sum(w.data(), w.size());
     for (double& v : w) v /= s;
     *half = h;
     return w;
@@ -275,6 +292,7 @@ template <typename T> struct Step {
     int hp = 0;
     // ST_COL
     int job0 = 0, njobs = 0, t0 = 0, nt = 0, zero_bnd = 0, has_b = 1;
+    std::vector<cx_t<T>> pw;  // ST_COL: tap pairs packed in job order (kernel-parameter path)
     // ST_IIR
     int P = 0;
     IirCoef coef{};
@@ -437,6 +455,8 @@ template <typename T> struct Builder {
         st.nt = nt;
         st.zero_bnd = zero_bnd;
         st.has_b = has_b;
+        for (const auto& j : jobs)
+            for (int q = 0; q < nt; ++q) st.pw.push_back(p.wcol[j.wofs + q]);
         p.cjobs.insert(p.cjobs.end(), jobs.begin(), jobs.end());
         p.steps.push_back(st);
     }
@@ -599,14 +619,15 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 if (jobs[j].out_direct >= 0) outs.push_back({jobs[j].out_direct, 0, 0, cd(1, 0)});
                 if (jobs[j].out_mirror >= 0) outs.push_back({jobs[j].out_mirror, 1, 1, cd(1, 0)});
                 ColJob<T> job = b.col_job(col_only ? 0 : ws_j0 + (int64_t)j * HW, wo, outs, jobs[j].ws != 0.0);
-                // theta = 0 (ws = 0) jobs need A only; they share the launch (per-CTA branch)
-                if (jobs[j].ws == 0.0) cj_b.insert(cj_b.begin(), job);
+                // theta = 0 (ws = 0) jobs need A only (half the work): they share the
+                // launch (per-CTA branch) and go last so heavy CTAs start first
+                if (jobs[j].ws == 0.0) cj_nob.push_back(job);
                 else cj_b.push_back(job);
             }
             const Ref src = col_only ? img : R(SEL_WS, 0);
             const double sfl = box ? 2.0 * h : 4.0 * h + 1;
+            cj_b.insert(cj_b.end(), cj_nob.begin(), cj_nob.end());
             b.col_step(cj_b, src, out, H, W, t0, nt, box ? 1 : 0, 1, sfl);
-            b.col_step(cj_nob, src, out, H, W, t0, nt, box ? 1 : 0, 0, sfl);
         }
     } else {
         // ---- RecursiveIIR ----
@@ -1122,7 +1143,7 @@ static std::map<int, std::unique_ptr<Ctx>> g_ctx;
 
 // ---- live per-kernel profiling (CUDA events on the launching stream) ----
 struct ProfRec {
-    const char* name;
+    std::string name;
     cudaEvent_t e0, e1;
     double flops, bytes;
 };
@@ -1190,8 +1211,12 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
             *bs = 2 * p.ws_img_c;
             return (const T*)ws + r.off;
         };
+        static const bool detail = std::getenv("FGB_PROF_DETAIL") != nullptr;
+        int sidx = 0;
         for (const Step<T>& st : p.steps) {
-            ProfRec pr{st.name, nullptr, nullptr, st.flops * nb, st.bytes * nb};
+            ProfRec pr{detail ? std::string(st.name) + "." + std::to_string(sidx) : std::string(st.name), nullptr, nullptr,
+                       st.flops * nb, st.bytes * nb};
+            ++sidx;
             if (g_prof) {
                 pr.e0 = pool_event();
                 pr.e1 = pool_event();
@@ -1212,7 +1237,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.W = st.W;
                     a.hp = st.hp;
                     a.batch = nb;
-                    FGB_CUDA(launch_row_sym<T>(a, st.rg, s));
+                    FGB_CUDA(launch_row_sym<T>(a, st.rg, std::getenv("FGB_ROW_SMEM_TAPS") ? nullptr : p.wrow.data() + st.rg.wofs, s));
                     break;
                 }
                 case ST_COL: {
@@ -1230,7 +1255,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.zero_boundary = st.zero_bnd;
                     a.njobs = st.njobs;
                     a.batch = nb;
-                    FGB_CUDA(launch_col<T>(a, st.has_b != 0, s));
+                    FGB_CUDA(launch_col<T>(a, std::getenv("FGB_COL_SMEM_TAPS") ? nullptr : st.pw.data(), s));
                     break;
                 }
                 case ST_IIR: {
@@ -1636,11 +1661,11 @@ int32_t fgb_profile_read(fgb_prof_entry* out, int32_t cap) {
         FGB_CUDA(cudaEventElapsedTime(&ms, r.e0, r.e1));
         fgb_prof_entry* e = nullptr;
         for (auto& a : agg)
-            if (std::strncmp(a.name, r.name, sizeof(a.name)) == 0) e = &a;
+            if (std::strncmp(a.name, r.name.c_str(), sizeof(a.name) - 1) == 0) e = &a;
         if (!e) {
             agg.push_back(fgb_prof_entry{});
             e = &agg.back();
-            std::strncpy(e->name, r.name, sizeof(e->name) - 1);
+            std::strncpy(e->name, r.name.c_str(), sizeof(e->name) - 1);
         }
         e->launches += 1;
         e->ms += ms;

@@ -21,9 +21,16 @@ template <typename T> struct RowArgs {
     int hp;                // half-width padded to a multiple of the row R
     int batch;
 };
-template <typename T> size_t row_sym_smem(int hp, int nd);
+template <typename T, int CAP> struct RowWParam { T w[CAP > 0 ? CAP : 1]; };
+template <typename T> struct RowWCap {
+    static constexpr int kSmall = 4096 / (int)sizeof(T);           // 4 KB
+    static constexpr int kLarge = (30 * 1024) / (int)sizeof(T);    // 30 KB
+};
+template <typename T> size_t row_sym_smem(int hp, int nd, bool taps_in_smem);
 template <typename T> int row_sym_pad(int h);
-template <typename T> cudaError_t launch_row_sym(const RowArgs<T>& a, const RowGroup<T>& g, cudaStream_t s);
+// pw_host: the group's [(hp+1)][NDP][2] tap table (kernel-parameter path) or nullptr
+template <typename T>
+cudaError_t launch_row_sym(const RowArgs<T>& a, const RowGroup<T>& g, const T* pw_host, cudaStream_t s);
 
 // ---- K2: column pass with two real kernels (col_fir.cu) ------------------
 template <typename T> struct ColArgs {
@@ -40,9 +47,18 @@ template <typename T> struct ColArgs {
     int njobs;
     int batch;
     int seg;                 // rows per CTA segment (set by launch_col)
+    int col2;                // fp32: two columns per thread (set by launch_col)
 };
-// Launch all jobs (same taps range/length, same has_b) in one grid.
-template <typename T> cudaError_t launch_col(const ColArgs<T>& a, bool has_b, cudaStream_t s);
+// Tap pairs passed as kernel parameters (constant bank), packed per job:
+// w[job * nt + q].  Two capacity tiers keep the parameter block small.
+template <typename T, int CAP> struct ColWParam { cx_t<T> w[CAP > 0 ? CAP : 1]; };
+template <typename T> struct ColWCap {
+    static constexpr int kSmall = 2048 / (int)sizeof(cx_t<T>) * 2;            // 4 KB
+    static constexpr int kLarge = (31 * 1024) / (int)sizeof(cx_t<T>);         // 31 KB
+};
+// Launch all jobs (same tap range/length) in one grid.  pw_host: the launch's
+// packed tap pairs (nullptr = read them from `weights` through shared memory).
+template <typename T> cudaError_t launch_col(const ColArgs<T>& a, const cx_t<T>* pw_host, cudaStream_t s);
 template <typename T> size_t col_smem(int nt, int groups);
 
 // ---- transposes (transpose.cu) -------------------------------------------

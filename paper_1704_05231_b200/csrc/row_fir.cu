@@ -15,6 +15,8 @@
 // row (256 px per CTA row).  The clamped row segment lives in shared memory
 // split into R residue sub-arrays (element i at (i%R)*S + i/R) so the
 // stride-R register windows load conflict-free with immediate offsets.
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -39,8 +41,13 @@ template <typename T> __host__ __device__ inline int row_sub_len(int need) {
     return s;
 }
 
-template <typename T, int ND>
-__global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, RowGroup<T> g) {
+// CAP > 0: the group's tap table travels in the kernel parameters (constant
+// bank) so the FFMA multipliers are uniform-register operands; CAP == 0:
+// table staged in shared memory.
+template <typename T, int ND, int CAP>
+__global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_constant__ RowArgs<T> a,
+                                                                  const __grid_constant__ RowGroup<T> g,
+                                                                  const __grid_constant__ RowWParam<T, CAP> pw) {
     constexpr int R = kRowR;
     constexpr int NDP = (ND + 1) & ~1;  // weight rows padded to an even count
     using C = cx_t<T>;
@@ -49,7 +56,8 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, 
     const int hp = a.hp;
     const int nseg = kRowSpan + 2 * hp;
     const int S = row_sub_len<T>((nseg + R - 1) / R);
-    T* rows = wsm + (size_t)(hp + 1) * NDP * 2;  // [kRowTY][R][S]
+    T* rows = CAP > 0 ? wsm : wsm + (size_t)(hp + 1) * NDP * 2;  // [kRowTY][R][S]
+    auto W = [&](int i) -> T { if constexpr (CAP > 0) return pw.w[i]; else return wsm[i]; };
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * kRowTX + tx;
@@ -58,7 +66,7 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, 
     const int y = blockIdx.y * kRowTY + ty;
 
     // weights: global table already laid out [(hp+1)][NDP][2]
-    {
+    if (CAP == 0) {
         // [(hp+1)][NDP][2] table: a multiple of 16 bytes, 16-byte aligned
         const T* wg = a.weights + g.wofs;
         constexpr int per16 = 16 / sizeof(T);
@@ -86,7 +94,7 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, 
             T v = my[r * S + base];
 #pragma unroll
             for (int k = 0; k < ND; ++k) {
-                accr[k][r] = wsm[k * 2] * v;
+                accr[k][r] = W(k * 2) * v;
                 acci[k][r] = T(0);
             }
         }
@@ -106,17 +114,22 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, 
         }
 #pragma unroll
         for (int tt = 0; tt < R; ++tt) {
-            const T* wrow = wsm + (size_t)(1 + c * R + tt) * NDP * 2;
+            const int wrow = (1 + c * R + tt) * NDP * 2;
             T wr[NDP], wi[NDP];
+            if constexpr (CAP > 0) {
 #pragma unroll
-            for (int k = 0; k < NDP; k += 2) {
-                if constexpr (sizeof(T) == 4) {
-                    float4 w4 = *reinterpret_cast<const float4*>(wrow + 2 * k);
-                    wr[k] = w4.x; wi[k] = w4.y; wr[k + 1] = w4.z; wi[k + 1] = w4.w;
-                } else {
-                    double2 w0 = *reinterpret_cast<const double2*>(wrow + 2 * k);
-                    double2 w1 = *reinterpret_cast<const double2*>(wrow + 2 * k + 2);
-                    wr[k] = w0.x; wi[k] = w0.y; wr[k + 1] = w1.x; wi[k + 1] = w1.y;
+                for (int k = 0; k < NDP; ++k) { wr[k] = W(wrow + 2 * k); wi[k] = W(wrow + 2 * k + 1); }
+            } else {
+#pragma unroll
+                for (int k = 0; k < NDP; k += 2) {
+                    if constexpr (sizeof(T) == 4) {
+                        float4 w4 = *reinterpret_cast<const float4*>(wsm + wrow + 2 * k);
+                        wr[k] = w4.x; wi[k] = w4.y; wr[k + 1] = w4.z; wi[k + 1] = w4.w;
+                    } else {
+                        double2 w0 = *reinterpret_cast<const double2*>(wsm + wrow + 2 * k);
+                        double2 w1 = *reinterpret_cast<const double2*>(wsm + wrow + 2 * k + 2);
+                        wr[k] = w0.x; wi[k] = w0.y; wr[k + 1] = w1.x; wi[k + 1] = w1.y;
+                    }
                 }
             }
 #pragma unroll
@@ -165,48 +178,62 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(RowArgs<T> a, 
 
 }  // namespace
 
-template <typename T> size_t row_sym_smem(int hp, int nd) {
+template <typename T> size_t row_sym_smem(int hp, int nd, bool taps_in_smem) {
     const int ndp = (nd + 1) & ~1;
     const int nseg = kRowSpan + 2 * hp;
     const int S = row_sub_len<T>((nseg + kRowR - 1) / kRowR);
-    return sizeof(T) * ((size_t)(hp + 1) * ndp * 2 + (size_t)kRowTY * kRowR * S);
+    return sizeof(T) * ((taps_in_smem ? (size_t)(hp + 1) * ndp * 2 : 0) + (size_t)kRowTY * kRowR * S);
 }
 
 template <typename T> int row_sym_pad(int h) { return (h + kRowR - 1) / kRowR * kRowR; }
 
-template <typename T, int ND>
-static cudaError_t launch_nd(const RowArgs<T>& a, const RowGroup<T>& g, cudaStream_t s) {
-    const size_t smem = row_sym_smem<T>(a.hp, ND);
-    auto kern = row_sym_kernel<T, ND>;
+template <typename T, int ND, int CAP>
+static cudaError_t launch_cap(const RowArgs<T>& a, const RowGroup<T>& g, const T* pw_host, cudaStream_t s) {
+    const size_t smem = row_sym_smem<T>(a.hp, ND, CAP == 0);
+    auto kern = row_sym_kernel<T, ND, CAP>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
+    static RowWParam<T, CAP> pw;  // host staging (launches are serialised by the engine lock)
+    constexpr int NDP = (ND + 1) & ~1;
+    if constexpr (CAP > 0) std::memcpy(pw.w, pw_host, sizeof(T) * (size_t)(a.hp + 1) * NDP * 2);
     dim3 grid((a.W + kRowSpan - 1) / kRowSpan, (a.H + kRowTY - 1) / kRowTY, a.batch);
     dim3 block(kRowTX, kRowTY);
-    kern<<<grid, block, smem, s>>>(a, g);
+    kern<<<grid, block, smem, s>>>(a, g, pw);
     return cudaGetLastError();
 }
 
-template <typename T> cudaError_t launch_row_sym(const RowArgs<T>& a, const RowGroup<T>& g, cudaStream_t s) {
+template <typename T, int ND>
+static cudaError_t launch_nd(const RowArgs<T>& a, const RowGroup<T>& g, const T* pw_host, cudaStream_t s) {
+    constexpr int NDP = (ND + 1) & ~1;
+    const size_t need = (size_t)(a.hp + 1) * NDP * 2;
+    if (pw_host && need <= (size_t)RowWCap<T>::kSmall) return launch_cap<T, ND, RowWCap<T>::kSmall>(a, g, pw_host, s);
+    if (pw_host && need <= (size_t)RowWCap<T>::kLarge) return launch_cap<T, ND, RowWCap<T>::kLarge>(a, g, pw_host, s);
+    return launch_cap<T, ND, 0>(a, g, nullptr, s);
+}
+
+template <typename T>
+cudaError_t launch_row_sym(const RowArgs<T>& a, const RowGroup<T>& g, const T* pw_host, cudaStream_t s) {
     switch (g.nd) {
-        case 1: return launch_nd<T, 1>(a, g, s);
-        case 2: return launch_nd<T, 2>(a, g, s);
-        case 3: return launch_nd<T, 3>(a, g, s);
-        case 4: return launch_nd<T, 4>(a, g, s);
-        case 5: return launch_nd<T, 5>(a, g, s);
-        case 6: return launch_nd<T, 6>(a, g, s);
-        case 7: return launch_nd<T, 7>(a, g, s);
-        case 8: return launch_nd<T, 8>(a, g, s);
+        case 1: return launch_nd<T, 1>(a, g, pw_host, s);
+        case 2: return launch_nd<T, 2>(a, g, pw_host, s);
+        case 3: return launch_nd<T, 3>(a, g, pw_host, s);
+        case 4: return launch_nd<T, 4>(a, g, pw_host, s);
+        case 5: return launch_nd<T, 5>(a, g, pw_host, s);
+        case 6: return launch_nd<T, 6>(a, g, pw_host, s);
+        case 7: return launch_nd<T, 7>(a, g, pw_host, s);
+        case 8: return launch_nd<T, 8>(a, g, pw_host, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
-template size_t row_sym_smem<float>(int, int);
-template size_t row_sym_smem<double>(int, int);
+template size_t row_sym_smem<float>(int, int, bool);
+template size_t row_sym_smem<double>(int, int, bool);
 template int row_sym_pad<float>(int);
 template int row_sym_pad<double>(int);
-template cudaError_t launch_row_sym<float>(const RowArgs<float>&, const RowGroup<float>&, cudaStream_t);
-template cudaError_t launch_row_sym<double>(const RowArgs<double>&, const RowGroup<double>&, cudaStream_t);
+template cudaError_t launch_row_sym<float>(const RowArgs<float>&, const RowGroup<float>&, const float*, cudaStream_t);
+template cudaError_t launch_row_sym<double>(const RowArgs<double>&, const RowGroup<double>&, const double*,
+                                            cudaStream_t);
 
 }  // namespace fgb

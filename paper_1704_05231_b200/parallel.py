@@ -78,3 +78,56 @@ def load_balance(parts, costs) -> float:
     loads = [sum(costs[u] for u in p) for p in parts]
     mean = sum(loads) / len(loads)
     return max(loads) / mean if mean > 0 else 1.0
+
+
+def unit_entries(units, n: int) -> list[tuple[int, int]]:
+    """(frequency i, orientation k) of every output of a unit list, in the
+    compact order the C ABI writes them (fgb_bank_desc.units): per unit its
+    direct entry, then the mirror N-k when it exists (bank.py:112-115)."""
+    nh = n // 2
+    out = []
+    for u in units:
+        i, k = divmod(u, nh + 1)
+        out.append((i, k))
+        if nh < n - k < n:
+            out.append((i, n - k))
+    return out
+
+
+def head_bins(heads, m: int) -> list[tuple[int, int]]:
+    """(u, v) of every bin of a pair-head list in the compact SDFT order."""
+    out = []
+    for u in heads:
+        out += [(u, v) for v in range(m)]
+        um = (m - u) % m
+        if um != u:
+            out += [(um, v) for v in range(m)]
+    return out
+
+
+def sharded_bank(img, spec, kind, group=None, compute=None, radius: float = 3.0):
+    """Multi-rank bank of ONE image: rank 0's image is broadcast once
+    (torch.distributed over NCCL on B200s, gloo in CPU tests), every rank
+    computes its LPT share of (frequency, direct k) units, no collective in
+    the data path.  Returns (local outputs [E_local, H, W], entry list).
+
+    ``compute(img, spec, kind, units)`` defaults to the device path
+    (paper_1704_05231_b200.device.compute_bank); tests inject a CPU stand-in.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world > 1:
+        dist.broadcast(img, 0, group=group)
+    sig = [spec.sigma_for(i) for i in range(len(spec.frequencies))]
+    costs = bank_unit_costs(spec.frequencies, sig, spec.orientations_n, radius)
+    units = lpt_assign(costs, world)[rank]
+    if compute is None:
+        from .device import compute_bank as compute_dev
+
+        def compute(im, sp, kd, un):
+            return compute_dev(im, sp, kd, True, un)[0]
+    out = compute(img, spec, kind, units)
+    return out, unit_entries(units, spec.orientations_n)

@@ -1,0 +1,112 @@
+"""GPU: device-tensor API, sharded (compact) layouts, fused-vs-separable SDFT,
+large-sigma IIR in fp32 (fp64 recursion state), batch handling."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import fastgabor_oracle as O
+from .conftest import max_rel_err, random_image
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_1704_05231_b200 as fg
+    from paper_1704_05231_b200 import device as D
+    from paper_1704_05231_b200 import parallel as P
+
+    return torch, fg, D, P
+
+
+def test_units_compact_layout_matches_full(env):
+    torch, fg, D, P = env
+    f = torch.from_numpy(random_image(3, 80, 0.0, 1.0, width=96).astype(np.float32)).cuda()
+    spec = fg.BankSpec((math.pi / 2, math.pi / 8), 16, (2.0, 8.0))
+    full = D.compute_bank(f, spec, fg.ExactFIR(3.0))[0]
+    for units in ([0, 3, 9], [4, 8, 17, 12], list(range(18))):
+        part = D.compute_bank(f, spec, fg.ExactFIR(3.0), True, units)[0]
+        ent = P.unit_entries(units, 16)
+        assert part.shape[0] == len(ent)
+        for e, (i, k) in enumerate(ent):
+            assert torch.equal(part[e], full[i * 16 + k])
+
+
+def test_sdft_heads_compact_layout(env):
+    torch, fg, D, P = env
+    f = torch.from_numpy(random_image(4, 64, 0.0, 1.0, width=64).astype(np.float32)).cuda()
+    spec = fg.SdftSpec(16, 16, fg.ExactFIR(3.0), 4.0)
+    full = D.sdft_full(f, spec)[0]
+    for heads in ([0], [8], [3, 5], [0, 8, 1]):
+        part = D.sdft_full(f, spec, heads)[0]
+        bins = P.head_bins(heads, 16)
+        assert part.shape[0] == len(bins)
+        for e, (u, v) in enumerate(bins):
+            assert torch.equal(part[e], full[u * 16 + v])
+
+
+@pytest.mark.parametrize("m,sigma,radius", [(16, 4.0, 3.0), (8, None, 6.0), (32, 3.0, 3.0), (4, 1.0, 3.0), (16, 2.5, 3.0)])
+def test_sdft_fused_matches_separable_and_oracle(env, m, sigma, radius):
+    torch, fg, D, P = env
+    fimg = random_image(5, 48, 0.0, 1.0, width=56)
+    f = torch.from_numpy(fimg.astype(np.float32)).cuda()
+    spec = fg.SdftSpec(m, m, fg.ExactFIR(radius), sigma)
+    fused = D.sdft_full(f, spec)[0].cpu().numpy()
+    os.environ["FGB_SDFT_UNFUSED"] = "1"
+    try:
+        import ctypes
+
+        from paper_1704_05231_b200 import _native as N
+
+        N.lib.fgb_release_caches()
+        sep = D.sdft_full(f, spec)[0].cpu().numpy()
+    finally:
+        del os.environ["FGB_SDFT_UNFUSED"]
+        N.lib.fgb_release_caches()
+    ref = O.sdft_full(fimg.astype(np.float32).astype(np.float64), m, m, ("fir", radius), sigma)
+    worst_f = worst_s = 0.0
+    for u in range(m):
+        for v in range(m):
+            r = ref[u][v]
+            worst_f = max(worst_f, max_rel_err((fused[u * m + v].real, fused[u * m + v].imag), r))
+            worst_s = max(worst_s, max_rel_err((sep[u * m + v].real, sep[u * m + v].imag), r))
+    assert worst_f <= 1e-5 and worst_s <= 1e-5, (worst_f, worst_s)
+
+
+def test_iir_large_sigma_f32(env):
+    """fp32 storage with fp64 recursion state meets 1e-5 at sigma = 16, 32."""
+    torch, fg, D, P = env
+    fimg = random_image(6, 200, 0.0, 1.0, width=120)
+    for sigma in (16.0, 32.0):
+        p = fg.GaborParams(math.pi / sigma, 3 * math.pi / 8, sigma)
+        out = fg.gabor_filter(fg.RealImage.from_array(fimg), p, fg.RecursiveIIR(), fg.OpCounters(), precision="f32")
+        ref = O.gabor_filter(fimg, p.omega, p.theta, sigma, ("iir",))
+        assert max_rel_err(out, ref) <= 1e-5
+
+
+def test_batched_bank_equals_per_image(env):
+    torch, fg, D, P = env
+    imgs = np.stack([random_image(10 + i, 64, 0.0, 1.0, width=72) for i in range(3)]).astype(np.float32)
+    t = torch.from_numpy(imgs).cuda()
+    spec = fg.BankSpec((math.pi / 4, math.pi / 16), 8, (4.0, 16.0))
+    batched = D.compute_bank(t, spec, fg.ExactFIR(3.0))
+    for i in range(3):
+        single = D.compute_bank(t[i], spec, fg.ExactFIR(3.0))[0]
+        assert torch.equal(batched[i], single)
+
+
+def test_odd_width_and_tiny_images(env):
+    """Edge cases: odd widths (1-column kernel path), 1-pixel-wide and tiny images."""
+    torch, fg, D, P = env
+    for shape in ((37, 53), (5, 3), (1, 9), (9, 1), (2, 2)):
+        fimg = random_image(7, shape[0], 0.0, 1.0, width=shape[1])
+        spec = fg.BankSpec((1.0, 2.5), 4, (1.5, 0.8))
+        out = fg.compute_bank(fg.RealImage.from_array(fimg), spec, fg.ExactFIR(3.0), fg.OpCounters(), precision="f64")
+        ref = O.compute_bank(fimg, spec.frequencies, 4, spec.sigmas, ("fir", 3.0))
+        for (p, img), r in zip(out.entries, ref):
+            assert max_rel_err(img, r[3:]) <= 1e-10, shape
