@@ -162,7 +162,7 @@ def _oracle_sdft_rows(args):
     return m * m
 
 
-def cpu_sample(cfg, rows, cores):
+def cpu_sample(cfg, rows, cores, pool=None):
     """Run the oracle on a `rows`-row strip; returns (units, seconds)."""
     img = make_image(cfg if cfg["kind"] == "sdft" or cfg["size"] <= 2048 else dict(cfg, size=1024), 0,
                      size=min(cfg["size"], 2048))[:rows].astype(np.float64)
@@ -170,21 +170,12 @@ def cpu_sample(cfg, rows, cores):
     if cfg["kind"] == "bank":
         nh = cfg["n"] // 2
         jobs = [(img, w, k, cfg["n"], s) for w, s in zip(cfg["freqs"], cfg["sigmas"]) for k in range(nh + 1)]
-        if cores > 1:
-            import multiprocessing as mp
-
-            with mp.get_context("fork").Pool(cores) as pool:
-                outs = sum(pool.map(_oracle_bank_unit, jobs, chunksize=1))
-        else:
-            outs = sum(map(_oracle_bank_unit, jobs))
+        outs = sum(pool.map(_oracle_bank_unit, jobs, chunksize=1)) if pool else sum(map(_oracle_bank_unit, jobs))
         units = img.shape[0] * img.shape[1] * outs
     else:
-        if cores > 1:
-            import multiprocessing as mp
-
+        if pool:
             strips = np.array_split(img, cores, axis=0)
-            with mp.get_context("fork").Pool(cores) as pool:
-                pool.map(_oracle_sdft_rows, [(s, cfg["m"], cfg["sigma"]) for s in strips])
+            pool.map(_oracle_sdft_rows, [(s, cfg["m"], cfg["sigma"]) for s in strips])
         else:
             _oracle_sdft_rows((img, cfg["m"], cfg["sigma"]))
         units = img.shape[0] * img.shape[1] * cfg["m"] ** 2
@@ -192,19 +183,25 @@ def cpu_sample(cfg, rows, cores):
 
 
 def run_reference(args, cfg, rank, world):
+    """The reference's CPU algorithm (the oracle port: NumPy fp64 restatement of
+    fastgabor's hot path) on the host cores, a bounded strip per step."""
     if rank != 0:
         return
+    import multiprocessing as mp
+
     cores = os.cpu_count() or 1
     rows = 64 if cfg["kind"] == "bank" else 32
-    for _ in range(args.warmup):
-        cpu_sample(cfg, 16, cores)
-    tot_u, tot_s = 0, 0.0
-    for _ in range(args.steps):
-        u, s = cpu_sample(cfg, rows, cores)
-        tot_u += u
-        tot_s += s
+    with mp.get_context("fork").Pool(cores) as pool:
+        for _ in range(args.warmup):
+            cpu_sample(cfg, 16, cores, pool)
+        tot_u, tot_s = 0, 0.0
+        for _ in range(args.steps):
+            u, s = cpu_sample(cfg, rows, cores, pool)
+            tot_u += u
+            tot_s += s
     v = tot_u / tot_s
-    sample = f"oracle port (numpy fp64, FIR r=3), {rows}-row strip of the {cfg['workload'].split(':')[0]} image per step, pool of {cores} processes"
+    sample = (f"oracle port (NumPy fp64 restatement of the reference hot path, FIR r=3), {rows}-row strip of the "
+              f"{cfg['workload'].split(':')[0]} image per step, pool of {cores} processes")
     line = {
         "impl": "reference", "metric": metric_name(cfg), "value": v, "unit": unit_name(cfg), "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
@@ -335,16 +332,26 @@ def run_ours(args, cfg, rank, world, local_rank):
             "gbs": e["bytes"] / (e["ms"] * 1e-3) / 1e9 if e["ms"] > 0 else None,
         }
     top = max(prof, key=lambda e: e["ms"]) if prof else None
+    traffic = None
+    try:  # ncu-measured DRAM bytes per launch of the dominant kernel (profiles/, committed)
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as fh:
+            tr = json.load(fh)
+        if top is not None:
+            traffic = tr.get(f"cfg{args.config}/{top['name']}")
+    except Exception:
+        traffic = None
     roof = None
     if top is not None:
         if cfg["kind"] == "sdft":
             ach = top["bytes"] / (top["ms"] * 1e-3) / 1e9
             roof = {"bound": "hbm", "kernel": top["name"], "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+                    "frac": ach / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": top["bytes"] / top["launches"],
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
         else:
             ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
             roof = {"bound": "fp32", "kernel": top["name"], "achieved": ach, "peak": fp32, "unit": "TFLOP/s",
-                    "frac": ach / fp32 if fp32 > 0 else None, "traffic": None,
+                    "frac": ach / fp32 if fp32 > 0 else None, "traffic": traffic,
+                    "algorithmic_flops_per_launch": top["flops"] / top["launches"],
                     "peak_source": "live FFMA probe (fgb_probe_fp32_tflops); flops = reference OpCounters M+A"}
     # ---- e2e: host buffers through the C ABI (H2D + compute + D2H each step) ----
     e2e = None
