@@ -304,7 +304,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     max_ms = t.item()
     value = units_all * args.steps / (max_ms / 1e3)
 
-    # ---- live per-kernel profile pass (CUDA events on the launching stream) ----
+    # ---- live per-kernel profile pass (CUDA events on the launching stream; the
+    #      library serialises its stream lanes while profiling so each kernel is timed alone) ----
     N.lib.fgb_profile_enable(1)
     N.profile_read()
     nprof = min(20, args.steps)

@@ -281,6 +281,7 @@ enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDF
 
 template <typename T> struct Step {
     int kind = 0;
+    int lane = 0;            // stream lane (independent frequencies run concurrently)
     const char* name = "";
     double flops = 0.0;      // reference-counter flops (M + A) per image
     double bytes = 0.0;      // compulsory bytes per image (input read + output written)
@@ -324,6 +325,7 @@ template <typename T> struct Plan : PlanBase {
     int64_t out_img_c = 0;        // complex elements per output image
     int H = 0, W = 0;
     int chunk = 1;
+    int nlanes = 1;               // concurrent stream lanes used by the steps
 
     int32_t upload() {
         auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -359,7 +361,12 @@ template <typename T> struct Plan : PlanBase {
 template <typename T> struct Builder {
     using C = cx_t<T>;
     Plan<T>& p;
+    int lane = 0;  // lane stamped on every step this builder emits
     explicit Builder(Plan<T>& pl) : p(pl) {}
+    void push(Step<T>& st) {
+        st.lane = lane;
+        p.steps.push_back(st);
+    }
 
     // Row group over symmetric taps w[0..2h] for nd jobs with frequencies
     // f_k and sign s: J_k = phase_k sum_t w[t] e^{-i s f_k t} f[x+t].
@@ -400,7 +407,7 @@ template <typename T> struct Builder {
                 p.wrow.push_back((T)ki);
             }
         }
-        p.steps.push_back(st);
+        push(st);
     }
 
     // Column job with taps t0..t0+nt-1: ka = w cos(f t), kb = w sin(f t).
@@ -458,7 +465,7 @@ template <typename T> struct Builder {
         for (const auto& j : jobs)
             for (int q = 0; q < nt; ++q) st.pw.push_back(p.wcol[j.wofs + q]);
         p.cjobs.insert(p.cjobs.end(), jobs.begin(), jobs.end());
-        p.steps.push_back(st);
+        push(st);
     }
     int64_t table(double f, int lo, int n) {
         const int64_t off = (int64_t)p.tabs.size();
@@ -489,7 +496,7 @@ template <typename T> struct Builder {
         st.coef = c;
         st.scratch_off = scratch_off;
         p.ijobs.insert(p.ijobs.end(), jobs.begin(), jobs.end());
-        p.steps.push_back(st);
+        push(st);
     }
     void tr(int kind, Ref src, Ref dst, int H, int W) {
         Step<T> st;
@@ -500,7 +507,7 @@ template <typename T> struct Builder {
         st.W = W;
         st.src = src;
         st.dst = dst;
-        p.steps.push_back(st);
+        push(st);
     }
 };
 
@@ -708,7 +715,7 @@ static int64_t ws_budget_bytes() {
 }
 
 template <typename T> static void finish_chunking(Plan<T>& p, int batch) {
-    p.scratch_img_t = iir_scratch_need(p);
+    p.scratch_img_t = iir_scratch_need(p) * p.nlanes;
     const int64_t per = p.ws_img_c * (int64_t)sizeof(cx_t<T>) + p.scratch_img_t * (int64_t)sizeof(T);
     int64_t c = per > 0 ? ws_budget_bytes() / per : batch;
     p.chunk = (int)std::max<int64_t>(1, std::min<int64_t>(c, batch));
@@ -750,14 +757,31 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
     }
     p.out_img_c = slot * HW;
     int64_t max_nj = 0;
-    for (auto& v : per_f) max_nj = std::max<int64_t>(max_nj, (int64_t)v.size());
-    const int64_t ws_aux = max_nj * HW;  // transposes after the J planes
-    int64_t need = 0;
-    for (int i = 0; i < d.n_freq; ++i) {
-        FGB_TRY(build_gabor_freq<T>(b, d.smoother, d.sigmas[i], per_f[i], H, W, 0, ws_aux, R(SEL_IMG, 0),
-                                    R(SEL_OUT, 0), false, false, &need));
+    int nfreq_used = 0;
+    for (auto& v : per_f) {
+        max_nj = std::max<int64_t>(max_nj, (int64_t)v.size());
+        nfreq_used += v.empty() ? 0 : 1;
     }
-    p.ws_img_c = need;
+    // Frequencies are independent until their outputs: each runs its row -> column
+    // chain on its own stream lane, so memory/latency-bound small-sigma launches
+    // overlap the FP32-bound large-sigma ones.  Each lane owns its J (and aux) planes.
+    const char* le = std::getenv("FGB_LANES");
+    const int max_lanes = le ? std::max(1, std::atoi(le)) : 4;
+    const int NL = std::max(1, std::min(max_lanes, nfreq_used));
+    const bool plain_fir = d.smoother.kind == FGB_SMOOTH_FIR;
+    const int64_t lane_stride = plain_fir ? max_nj * HW : (2 * max_nj + 1) * HW;
+    int64_t need = 0;
+    int li = 0;
+    for (int i = 0; i < d.n_freq; ++i) {
+        if (per_f[i].empty()) continue;
+        b.lane = li % NL;
+        const int64_t j0 = b.lane * lane_stride;
+        FGB_TRY(build_gabor_freq<T>(b, d.smoother, d.sigmas[i], per_f[i], H, W, j0, j0 + max_nj * HW, R(SEL_IMG, 0),
+                                    R(SEL_OUT, 0), false, false, &need));
+        ++li;
+    }
+    p.nlanes = NL;
+    p.ws_img_c = std::max(need, NL * lane_stride);
     finish_chunking(p, d.img.batch);
     return p.upload();
 }
@@ -1134,6 +1158,14 @@ static int32_t build_sdft_single(Plan<T>& p, const fgb_sdft_desc& d, int u, int 
 // execution
 // ===========================================================================
 struct Ctx {
+    std::vector<cudaStream_t> lanes;
+    std::vector<cudaEvent_t> lane_ev;
+    cudaEvent_t fork_ev = nullptr;
+    ~Ctx() {
+        for (auto st : lanes) cudaStreamDestroy(st);
+        for (auto e : lane_ev) cudaEventDestroy(e);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+    }
     DevBuf ws;
     std::map<std::string, std::shared_ptr<PlanBase>> plans;
     DevBuf hin, hout;  // device staging of the *_host entry points
@@ -1180,9 +1212,31 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     FGB_TRY(cx.ws.ensure((size_t)(ws_img_bytes + scr_bytes) * chunk + 256));
     C* ws = (C*)cx.ws.p;
     T* scratch = (T*)((char*)cx.ws.p + ws_img_bytes * chunk);
+    const int64_t scratch_lane = p.scratch_img_t / std::max(1, p.nlanes) * chunk;
+    // lane streams: lane 0 is the caller's stream; lanes >= 1 are library streams forked
+    // from / joined into it with events, per image chunk
+    // live per-kernel profiling serialises the lanes so each kernel's events time it alone
+    const int nl = g_prof ? 1 : p.nlanes;
+    std::vector<cudaStream_t> lane_s(p.nlanes, s);
+    for (int l = 1; l < nl; ++l) {
+        while ((int)cx.lanes.size() < l) {
+            cudaStream_t ns;
+            FGB_CUDA(cudaStreamCreateWithFlags(&ns, cudaStreamNonBlocking));
+            cx.lanes.push_back(ns);
+            cudaEvent_t e;
+            FGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            cx.lane_ev.push_back(e);
+        }
+        lane_s[l] = cx.lanes[l - 1];
+    }
+    if (!cx.fork_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.fork_ev, cudaEventDisableTiming));
     const int64_t img_bs = (batch > 1) ? im.batch_stride : (int64_t)im.height * im.pitch;
     for (int b0 = 0; b0 < batch; b0 += chunk) {
         const int nb = std::min(chunk, batch - b0);
+        if (nl > 1) {
+            FGB_CUDA(cudaEventRecord(cx.fork_ev, s));
+            for (int l = 1; l < nl; ++l) FGB_CUDA(cudaStreamWaitEvent(lane_s[l], cx.fork_ev, 0));
+        }
         const T* imgb = (const T*)img + (size_t)b0 * img_bs;
         C* imgcb = (C*)img + (size_t)b0 * img_bs;  // complex inputs: strides in complex elements
         C* outb = (C*)out + (size_t)b0 * p.out_img_c;
@@ -1214,6 +1268,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
         static const bool detail = std::getenv("FGB_PROF_DETAIL") != nullptr;
         int sidx = 0;
         for (const Step<T>& st : p.steps) {
+            cudaStream_t s = lane_s[st.lane];  // shadows the caller's stream for this step
             ProfRec pr{detail ? std::string(st.name) + "." + std::to_string(sidx) : std::string(st.name), nullptr, nullptr,
                        st.flops * nb, st.bytes * nb};
             ++sidx;
@@ -1266,14 +1321,14 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.dst_base = baseC(st.dst);
                     a.src_bstride = bsC(st.src);
                     a.dst_bstride = bsC(st.dst);
-                    a.scratch = scratch;
+                    a.scratch = scratch + st.lane * scratch_lane;
                     a.c = st.coef;
                     a.H = st.H;
                     a.W = st.W;
                     a.P = st.P;
                     a.njobs = st.njobs;
                     a.batch = nb;
-                    if ((int64_t)iir_scratch_elems<T>(st.H, st.W, st.P, st.njobs, nb) > p.scratch_img_t * chunk)
+                    if ((int64_t)iir_scratch_elems<T>(st.H, st.W, st.P, st.njobs, nb) > scratch_lane)
                         return fail(FGB_EINVAL, "internal: IIR scratch too small");
                     FGB_CUDA(launch_iir_col<T>(a, s));
                     break;
@@ -1319,6 +1374,12 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
             if (g_prof) {
                 cudaEventRecord(pr.e1, s);
                 g_prof_pending.push_back(pr);
+            }
+        }
+        if (nl > 1) {
+            for (int l = 1; l < nl; ++l) {
+                FGB_CUDA(cudaEventRecord(cx.lane_ev[l - 1], lane_s[l]));
+                FGB_CUDA(cudaStreamWaitEvent(s, cx.lane_ev[l - 1], 0));
             }
         }
     }
