@@ -296,7 +296,8 @@ __global__ void __launch_bounds__(128) col_kernel2(const __grid_constant__ ColAr
     const int wofs = jb->wofs;
     const int has_b = jb->has_b;
     const int nout = jb->nout;
-    // output o: re = Ar + sa*Bi, im = sc*Ai + sd*Br, then * phase (if not 1)
+    const int emode = jb->mode;
+    // output o: re = Ar + sa*Bi, im = sc*Ai + sd*Br, then * phase
     float sa[4], sc[4], sd[4], phr[4], phi[4];
     int64_t doff[4];
 #pragma unroll
@@ -363,28 +364,48 @@ __global__ void __launch_bounds__(128) col_kernel2(const __grid_constant__ ColAr
             else col_accumulate2<R, REM, false, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
         }
         if (x < W) {
+            if (emode == 2) {  // Gabor theta / pi-theta: X = A - iB, conj(Y) = (Ar - Bi, -(Ai + Br))
+                float2* d0 = dst + doff[0];
+                float2* d1 = dst + doff[1];
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int yl = ch * TY + rg * R + r;
-                if (yl >= rows_out) break;
-                float2* drow = dst + (size_t)(ys + yl) * W;
+                for (int r = 0; r < R; ++r) {
+                    const int yl = ch * TY + rg * R + r;
+                    if (yl >= rows_out) break;
+                    const size_t pix = (size_t)(ys + yl) * W;
+                    __stcs(reinterpret_cast<float4*>(d0 + pix),
+                           make_float4(Ar[0][r] + Bi[0][r], Ai[0][r] - Br[0][r], Ar[1][r] + Bi[1][r], Ai[1][r] - Br[1][r]));
+                    __stcs(reinterpret_cast<float4*>(d1 + pix), make_float4(Ar[0][r] - Bi[0][r], -(Ai[0][r] + Br[0][r]),
+                                                                            Ar[1][r] - Bi[1][r], -(Ai[1][r] + Br[1][r])));
+                }
+            } else if (emode == 1) {  // Gabor single orientation: X
+                float2* d0 = dst + doff[0];
 #pragma unroll
-                for (int o = 0; o < 4; ++o) {
-                    if (o >= nout) break;
-                    float v[4];
+                for (int r = 0; r < R; ++r) {
+                    const int yl = ch * TY + rg * R + r;
+                    if (yl >= rows_out) break;
+                    const size_t pix = (size_t)(ys + yl) * W;
+                    __stcs(reinterpret_cast<float4*>(d0 + pix),
+                           make_float4(Ar[0][r] + Bi[0][r], Ai[0][r] - Br[0][r], Ar[1][r] + Bi[1][r], Ai[1][r] - Br[1][r]));
+                }
+            } else {
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        float re = fmaf(sa[o], Bi[q][r], Ar[q][r]);
-                        float im = fmaf(sd[o], Br[q][r], sc[o] * Ai[q][r]);
-                        if (phi[o] != 0.f || phr[o] != 1.f) {
+                for (int r = 0; r < R; ++r) {
+                    const int yl = ch * TY + rg * R + r;
+                    if (yl >= rows_out) break;
+                    float2* drow = dst + (size_t)(ys + yl) * W;
+                    for (int o = 0; o < nout; ++o) {
+                        float v[4];
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            float re = fmaf(sa[o], Bi[q][r], Ar[q][r]);
+                            float im = fmaf(sd[o], Br[q][r], sc[o] * Ai[q][r]);
                             const float orr = phr[o] * re - phi[o] * im;
                             im = phr[o] * im + phi[o] * re;
-                            re = orr;
+                            v[2 * q] = orr;
+                            v[2 * q + 1] = im;
                         }
-                        v[2 * q] = re;
-                        v[2 * q + 1] = im;
+                        __stcs(reinterpret_cast<float4*>(drow + doff[o]), make_float4(v[0], v[1], v[2], v[3]));
                     }
-                    __stcs(reinterpret_cast<float4*>(drow + doff[o]), make_float4(v[0], v[1], v[2], v[3]));
                 }
             }
         }

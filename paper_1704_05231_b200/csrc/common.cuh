@@ -58,7 +58,7 @@ template <typename T> struct ColJob {
     int8_t base[4];          // 0 = X, 1 = Y
     int8_t conj[4];
     int32_t has_b;           // kb != 0 (0 for the theta = 0 / v = 0 jobs: A only)
-    int32_t pad_;
+    int32_t mode;            // epilogue: 0 generic, 1 Gabor X only, 2 Gabor X + conj(Y) (no phase)
 };
 
 // Row job group: up to kMaxND jobs sharing one input row and one symmetric

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -277,7 +278,7 @@ struct Ref {
     int64_t off = 0;  // elements of the referenced type (T for real, C for complex)
 };
 
-enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF };
+enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF, ST_BANKF };
 
 template <typename T> struct Step {
     int kind = 0;
@@ -298,6 +299,13 @@ template <typename T> struct Step {
     int P = 0;
     IirCoef coef{};
     int64_t scratch_off = 0;  // T elements into the workspace scratch region
+    int nseg = 1, seglen = 1;
+    int64_t g_off = 0;        // into Plan::dbls: [seglen][3]
+    double Aseg[9] = {0}, Alast[9] = {0};
+    // ST_BANKF (fp32): tap tables + per-orientation outputs
+    std::vector<float> bf_w;
+    std::vector<BankFusedOut> bf_out;
+    int bf_colw_off = 0;
     // ST_SDFTF
     int M = 0, h = 0, nheads = 0;
     int64_t heads_off = 0, slots_off = 0, w_off = 0;
@@ -317,11 +325,13 @@ template <typename T> struct Plan : PlanBase {
     std::vector<IirJob<T>> ijobs;
     std::vector<double2> tabs;
     std::vector<int32_t> ints;
+    std::vector<double> dbls;
     DevBuf blob;
-    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0, off_ints = 0;
+    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0, off_ints = 0, off_dbls = 0;
     // workspace per image (bytes), scratch (T elements per image-chunk) and chunking
     int64_t ws_img_c = 0;         // complex elements per image
     int64_t scratch_img_t = 0;    // T elements per image (IIR scratch)
+    int64_t state_img_d = 0;      // doubles per image (IIR segment states)
     int64_t out_img_c = 0;        // complex elements per output image
     int H = 0, W = 0;
     int chunk = 1;
@@ -336,6 +346,7 @@ template <typename T> struct Plan : PlanBase {
         off_ijobs = o; o = al(o + ijobs.size() * sizeof(IirJob<T>));
         off_tabs = o; o = al(o + tabs.size() * sizeof(double2));
         off_ints = o; o = al(o + ints.size() * sizeof(int32_t));
+        off_dbls = o; o = al(o + dbls.size() * sizeof(double));
         FGB_TRY(blob.ensure(std::max<size_t>(o, 256)));
         std::vector<char> h(o, 0);
         if (!wrow.empty()) std::memcpy(h.data() + off_wrow, wrow.data(), wrow.size() * sizeof(T));
@@ -344,6 +355,7 @@ template <typename T> struct Plan : PlanBase {
         if (!ijobs.empty()) std::memcpy(h.data() + off_ijobs, ijobs.data(), ijobs.size() * sizeof(IirJob<T>));
         if (!tabs.empty()) std::memcpy(h.data() + off_tabs, tabs.data(), tabs.size() * sizeof(double2));
         if (!ints.empty()) std::memcpy(h.data() + off_ints, ints.data(), ints.size() * sizeof(int32_t));
+        if (!dbls.empty()) std::memcpy(h.data() + off_dbls, dbls.data(), dbls.size() * sizeof(double));
         FGB_CUDA(cudaMemcpy(blob.p, h.data(), o, cudaMemcpyHostToDevice));
         return FGB_OK;
     }
@@ -353,6 +365,7 @@ template <typename T> struct Plan : PlanBase {
     const IirJob<T>* d_ijobs() const { return (const IirJob<T>*)((char*)blob.p + off_ijobs); }
     const double2* d_tabs() const { return (const double2*)((char*)blob.p + off_tabs); }
     const int32_t* d_ints() const { return (const int32_t*)((char*)blob.p + off_ints); }
+    const double* d_dbls() const { return (const double*)((char*)blob.p + off_dbls); }
 };
 
 // ---------------------------------------------------------------------------
@@ -432,6 +445,12 @@ template <typename T> struct Builder {
         j.wofs = wofs;
         j.has_b = has_b;
         j.nout = (int)outs.size();
+        j.mode = 0;
+        bool unit_phase = true;
+        for (const auto& o : outs) unit_phase = unit_phase && o.phase == cd(1.0, 0.0);
+        if (unit_phase && outs.size() == 1 && outs[0].base == 0 && !outs[0].conj) j.mode = 1;
+        if (unit_phase && outs.size() == 2 && outs[0].base == 0 && !outs[0].conj && outs[1].base == 1 && outs[1].conj)
+            j.mode = 2;
         for (size_t o = 0; o < outs.size(); ++o) {
             j.dst_off[o] = outs[o].dst_off;
             j.base[o] = (int8_t)outs[o].base;
@@ -495,6 +514,35 @@ template <typename T> struct Builder {
         st.P = P;
         st.coef = c;
         st.scratch_off = scratch_off;
+        // segment-parallel recursion: enough (column, job, segment) threads to fill the GPU
+        const int L = H + 2 * P;
+        const double threads = (double)W * jobs.size();
+        int nseg = (int)std::ceil(148.0 * 1536.0 / std::max(1.0, threads));
+        nseg = std::max(1, std::min(nseg, std::max(1, L / 24)));
+        nseg = std::min(nseg, 128);
+        const int seglen = (L + nseg - 1) / nseg;
+        nseg = (L + seglen - 1) / seglen;
+        st.nseg = nseg;
+        st.seglen = seglen;
+        // companion matrix A, g_m = first row of A^(m+1), A^seglen, A^last
+        const double A[9] = {-c.a1, -c.a2, -c.a3, 1, 0, 0, 0, 1, 0};
+        double Pm[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};  // A^0
+        auto mul = [](const double* X, const double* Y, double* Z) {
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) Z[3 * i + j] = X[3 * i] * Y[j] + X[3 * i + 1] * Y[3 + j] + X[3 * i + 2] * Y[6 + j];
+        };
+        st.g_off = (int64_t)p.dbls.size();
+        const int last_len = L - (nseg - 1) * seglen;
+        for (int m = 1; m <= seglen; ++m) {
+            double Q[9];
+            mul(A, Pm, Q);
+            std::memcpy(Pm, Q, sizeof(Q));  // Pm = A^m
+            p.dbls.push_back(Pm[0]);
+            p.dbls.push_back(Pm[1]);
+            p.dbls.push_back(Pm[2]);
+            if (m == last_len) std::memcpy(st.Alast, Pm, sizeof(Pm));
+            if (m == seglen) std::memcpy(st.Aseg, Pm, sizeof(Pm));
+        }
         p.ijobs.insert(p.ijobs.end(), jobs.begin(), jobs.end());
         push(st);
     }
@@ -586,6 +634,59 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
         }
         t0 = -h;
         const int nt = 2 * h + 1;
+        // ---- fused small-sigma path: J stays in shared memory ----
+        if constexpr (std::is_same<T, float>::value) {
+            if (!box && !row_only && !col_only && nj <= kMaxND && bank_fused_ok(h, nj) &&
+                std::getenv("FGB_FUSED_BANK") && (int64_t)H * W >= 4096) {
+                Step<T> st;
+                st.kind = ST_BANKF;
+                st.name = "bank_fused";
+                st.H = H;
+                st.W = W;
+                st.src = img;
+                st.dst = out;
+                st.h = h;
+                st.nheads = nj;  // nd
+                const int ndp = (nj + 1) & ~1;
+                const int R = bank_fused_r(h);
+                const int ntp = (nt + R - 1) / R * R;
+                for (int t = 0; t <= h; ++t)
+                    for (int k = 0; k < ndp; ++k) {
+                        double kr = 0.0, ki = 0.0;
+                        if (k < nj) {
+                            kr = w[h + t] * std::cos(jobs[k].wc * t);
+                            ki = -w[h + t] * std::sin(jobs[k].wc * t);
+                        }
+                        st.bf_w.push_back((float)kr);
+                        st.bf_w.push_back((float)ki);
+                    }
+                st.bf_colw_off = (int)st.bf_w.size();
+                int counted = 0;
+                for (int k = 0; k < nj; ++k) {
+                    for (int q = 0; q < ntp; ++q) {
+                        double ka = 0.0, kb = 0.0;
+                        if (q < nt) {
+                            const double t = (double)(q - h);
+                            ka = w[q] * std::cos(jobs[k].ws * t);
+                            kb = w[q] * std::sin(jobs[k].ws * t);
+                        }
+                        st.bf_w.push_back((float)ka);
+                        st.bf_w.push_back((float)kb);
+                    }
+                    BankFusedOut o;
+                    o.direct = jobs[k].out_direct;
+                    o.mirror = jobs[k].out_mirror;
+                    st.bf_out.push_back(o);
+                    counted += 1 + (jobs[k].out_mirror >= 0 ? 1 : 0);
+                }
+                const double sfl = 4.0 * h + 1;
+                st.flops = ((double)nj * (2.0 * sfl + 8.0) + (double)counted * (2.0 * sfl + 12.0)) * H * W;
+                st.bytes = (double)H * W * sizeof(T) + (double)counted * H * W * sizeof(cx_t<T>);
+                b.push(st);
+                *ws_need = std::max(*ws_need, need - (int64_t)nj * HW);
+                return FGB_OK;
+            }
+        }
         // ---- row stage ----
         if (!col_only) {
             if (!box) {
@@ -707,6 +808,12 @@ template <typename T> static int64_t iir_scratch_need(const Plan<T>& p) {
         if (s.kind == ST_IIR) m = std::max<int64_t>(m, (int64_t)iir_scratch_elems<T>(s.H, s.W, s.P, s.njobs, 1));
     return m;
 }
+template <typename T> static int64_t iir_state_need(const Plan<T>& p) {
+    int64_t m = 0;
+    for (const auto& s : p.steps)
+        if (s.kind == ST_IIR) m = std::max<int64_t>(m, (int64_t)iir_state_doubles(s.W, s.nseg, s.njobs, 1));
+    return m;
+}
 
 static int64_t ws_budget_bytes() {
     const char* e = std::getenv("FGB_WS_BUDGET_MB");
@@ -716,7 +823,9 @@ static int64_t ws_budget_bytes() {
 
 template <typename T> static void finish_chunking(Plan<T>& p, int batch) {
     p.scratch_img_t = iir_scratch_need(p) * p.nlanes;
-    const int64_t per = p.ws_img_c * (int64_t)sizeof(cx_t<T>) + p.scratch_img_t * (int64_t)sizeof(T);
+    p.state_img_d = iir_state_need(p) * p.nlanes;
+    const int64_t per = p.ws_img_c * (int64_t)sizeof(cx_t<T>) + p.scratch_img_t * (int64_t)sizeof(T) +
+                        p.state_img_d * (int64_t)sizeof(double);
     int64_t c = per > 0 ? ws_budget_bytes() / per : batch;
     p.chunk = (int)std::max<int64_t>(1, std::min<int64_t>(c, batch));
 }
@@ -1209,10 +1318,13 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     const int chunk = std::min(p.chunk, batch);
     const int64_t ws_img_bytes = p.ws_img_c * (int64_t)sizeof(C);
     const int64_t scr_bytes = p.scratch_img_t * (int64_t)sizeof(T);
-    FGB_TRY(cx.ws.ensure((size_t)(ws_img_bytes + scr_bytes) * chunk + 256));
+    const int64_t stt_bytes = (p.state_img_d * (int64_t)sizeof(double) + 255) / 256 * 256;
+    FGB_TRY(cx.ws.ensure((size_t)(ws_img_bytes + scr_bytes + stt_bytes) * chunk + 512));
     C* ws = (C*)cx.ws.p;
     T* scratch = (T*)((char*)cx.ws.p + ws_img_bytes * chunk);
     const int64_t scratch_lane = p.scratch_img_t / std::max(1, p.nlanes) * chunk;
+    double* states = (double*)((char*)cx.ws.p + ((ws_img_bytes + scr_bytes) * chunk + 255) / 256 * 256);
+    const int64_t state_lane = p.state_img_d / std::max(1, p.nlanes) * chunk;
     // lane streams: lane 0 is the caller's stream; lanes >= 1 are library streams forked
     // from / joined into it with events, per image chunk
     // live per-kernel profiling serialises the lanes so each kernel's events time it alone
@@ -1322,6 +1434,12 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.src_bstride = bsC(st.src);
                     a.dst_bstride = bsC(st.dst);
                     a.scratch = scratch + st.lane * scratch_lane;
+                    a.state = states + st.lane * state_lane;
+                    a.g = p.d_dbls() + st.g_off;
+                    std::memcpy(a.Aseg, st.Aseg, sizeof(a.Aseg));
+                    std::memcpy(a.Alast, st.Alast, sizeof(a.Alast));
+                    a.nseg = st.nseg;
+                    a.seglen = st.seglen;
                     a.c = st.coef;
                     a.H = st.H;
                     a.W = st.W;
@@ -1361,6 +1479,28 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.h = st.h;
                     a.batch = nb;
                     FGB_CUDA(launch_sdft_fused<T>(a, st.M, s));
+                    break;
+                }
+                case ST_BANKF: {
+                    if constexpr (std::is_same<T, float>::value) {
+                        BankFusedArgs a{};
+                        int64_t pitch, bs;
+                        a.img = baseT(st.src, &pitch, &bs);
+                        a.pitch = pitch;
+                        a.img_bstride = bs;
+                        a.dst = baseC(st.dst);
+                        a.dst_bstride = bsC(st.dst);
+                        a.H = st.H;
+                        a.W = st.W;
+                        a.h = st.h;
+                        a.nd = st.nheads;
+                        a.batch = nb;
+                        a.col_w_off = st.bf_colw_off;
+                        for (int k = 0; k < st.nheads; ++k) a.out[k] = st.bf_out[k];
+                        static BankFusedW w;
+                        std::memcpy(w.w, st.bf_w.data(), st.bf_w.size() * sizeof(float));
+                        FGB_CUDA(launch_bank_fused(a, w, s));
+                    }
                     break;
                 }
                 case ST_TR_RR: {

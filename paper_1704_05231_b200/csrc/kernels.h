@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -114,13 +115,42 @@ template <typename T> struct IirArgs {
     const double2* tab_base;
     const cx_t<T>* src_base;
     cx_t<T>* dst_base;
-    T* scratch;              // [njobs*batch][4][H+2P][W]
+    T* scratch;              // [njobs*batch][4][H+2P][W] local forward / backward sequences
+    double* state;           // [2][njobs*batch][nseg][4 planes][3][W] segment boundary states
+    const double* g;         // [seglen][3]: first row of A^(m+1)
+    double Aseg[9];          // A^seglen
+    double Alast[9];         // A^(length of the last segment)
     int64_t src_bstride, dst_bstride;
     IirCoef c;
     int H, W, P;
     int njobs, batch;
+    int nseg, seglen;
 };
 template <typename T> cudaError_t launch_iir_col(const IirArgs<T>& a, cudaStream_t s);
 template <typename T> size_t iir_scratch_elems(int H, int W, int P, int njobs, int batch);
+size_t iir_state_doubles(int W, int nseg, int njobs, int batch);
+
+// ---- fused small-sigma bank stage (bank_fused.cu) ------------------------
+struct BankFusedOut {
+    int64_t direct;  // complex elements from dst (batch 0) of F_theta
+    int64_t mirror;  // of F_{pi - theta}, or -1
+};
+struct BankFusedArgs {
+    const float* img;
+    int64_t pitch, img_bstride;
+    float2* dst;
+    int64_t dst_bstride;
+    int H, W, h, nd, batch;
+    int col_w_off;               // float offset of the column taps in BankFusedW
+    BankFusedOut out[kMaxND];
+};
+struct BankFusedW {
+    static constexpr int kCap = 7168;  // floats (28 KB): row taps [(h+1)][NDP][2], column taps [nd][ntp][2]
+    float w[kCap];
+};
+bool bank_fused_ok(int h, int nd);
+size_t bank_fused_smem(int h, int nd, int TY);
+inline int bank_fused_r(int h) { return h <= 6 ? (std::getenv("FGB_BF_R8") ? 8 : 4) : 4; }
+cudaError_t launch_bank_fused(const BankFusedArgs& a, const BankFusedW& w, cudaStream_t s);
 
 }  // namespace fgb
