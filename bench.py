@@ -224,7 +224,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     from paper_1704_05231_b200 import _native as N
     from paper_1704_05231_b200.device import BankPlan, SdftPlan
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     kind = fg.ExactFIR(3.0) if args.smoother == "fir" else fg.RecursiveIIR()
 
@@ -354,6 +354,20 @@ def run_ours(args, cfg, rank, world, local_rank):
                     "frac": ach / fp32 if fp32 > 0 else None, "traffic": traffic,
                     "algorithmic_flops_per_launch": top["flops"] / top["launches"],
                     "peak_source": "live FFMA probe (fgb_probe_fp32_tflops); flops = reference OpCounters M+A"}
+    # whole-step roofline: algorithmic work of one step (sum over every launch, from the
+    # profile pass) / measured step time of the timed region
+    step_roof = None
+    if prof:
+        per_step = {k: sum(e[k] for e in prof) / nprof for k in ("flops", "bytes")}
+        step_s = max_ms / args.steps / 1e3
+        if cfg["kind"] == "sdft":
+            ach = per_step["bytes"] / step_s / 1e9
+            step_roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+        else:
+            ach = per_step["flops"] / step_s / 1e12
+            step_roof = {"bound": "fp32", "achieved": ach, "peak": fp32, "unit": "TFLOP/s",
+                         "frac": ach / fp32 if fp32 > 0 else None,
+                         "note": "reference OpCounters flops of the whole bank / step time (all launches, lanes overlapped)"}
     # ---- e2e: host buffers through the C ABI (H2D + compute + D2H each step) ----
     e2e = None
     if rank == 0 or True:
@@ -390,7 +404,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE.json shapes)",
             "config": {"workload": cfg["workload"], "smoother": args.smoother, "l2": "256 MiB flush between timed steps",
                        "parallelism": f"{'image' if args.config in (2, 3) else 'unit'}-sharded x{world}"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "kernels": kernels, "fp32_peak_tflops_measured": fp32,
         }
         print(json.dumps(line), flush=True)
@@ -418,8 +432,13 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("FGB_DIST_BACKEND", "nccl")  # gloo: host-logic test with ranks sharing a GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, cfg, rank, world, local_rank)
     finally:
