@@ -159,7 +159,9 @@ int64_t fgb_launch_count(void);      /* kernels launched by this library so far 
 double fgb_probe_fp32_tflops(void);  /* FFMA peak probe (K6), TFLOP/s */
 double fgb_probe_fp64_tflops(void);  /* DFMA peak probe (K6), TFLOP/s */
 /* FMA probe by operand form: mode 0 immediate operands, 1 register operands
- * with a shared multiplier (operand reuse), 2 three distinct registers. */
+ * with a shared multiplier (operand reuse), 2 three distinct registers,
+ * 3 constant-bank multiplier, 4 / 5 packed fp32x2 FFMA2 with a constant /
+ * register multiplier (fp32 only). */
 double fgb_probe_fma(int32_t dtype, int32_t mode);
 
 /* ---- synchronisation helper for hosts without a CUDA binding ----------- */

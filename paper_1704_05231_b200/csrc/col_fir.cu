@@ -210,9 +210,12 @@ __global__ void __launch_bounds__(256) col_kernel(const __grid_constant__ ColArg
 // fp32 variant with two adjacent columns per thread: J pairs move as 16-byte
 // cp.async / LDS.128 / STG.128, halving load, weight and store instructions
 // per FFMA (needs an even W).  CTA = 64 columns x G row groups.
+// Packed-FP32 accumulation (sm_100 FFMA2): (Ar, Ai) += ka * (Jr, Ji) and
+// (Br, Bi) += kb * (Jr, Ji) are one FFMA2 each with the tap broadcast from a
+// uniform register -- half the FMA-pipe instructions of scalar FFMA, so the
+// loads and address arithmetic issue in the FMA pipe's spare slots.
 template <int R, int REM, bool HASB, int RS, typename WF>
-__device__ __forceinline__ void col_accumulate2(const float4* tb, WF wts, int nt, float (&Ar)[2][R], float (&Ai)[2][R],
-                                                float (&Br)[2][R], float (&Bi)[2][R]) {
+__device__ __forceinline__ void col_accumulate2(const float4* tb, WF wts, int nt, float2 (&A)[2][R], float2 (&Bv)[2][R]) {
     const int nfull = (nt - REM) / R;
 #pragma unroll 1
     for (int c = 0; c < nfull; ++c) {
@@ -222,18 +225,16 @@ __device__ __forceinline__ void col_accumulate2(const float4* tb, WF wts, int nt
 #pragma unroll
         for (int tt = 0; tt < R; ++tt) {
             const float2 w = wts(c * R + tt);
+            const float2 wa = make_float2(w.x, w.x), wb = make_float2(w.y, w.y);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const float4 q = v[r + tt];
-                Ar[0][r] = fmaf(w.x, q.x, Ar[0][r]);
-                Ai[0][r] = fmaf(w.x, q.y, Ai[0][r]);
-                Ar[1][r] = fmaf(w.x, q.z, Ar[1][r]);
-                Ai[1][r] = fmaf(w.x, q.w, Ai[1][r]);
+                const float2 lo = make_float2(q.x, q.y), hi = make_float2(q.z, q.w);
+                A[0][r] = __ffma2_rn(wa, lo, A[0][r]);
+                A[1][r] = __ffma2_rn(wa, hi, A[1][r]);
                 if (HASB) {
-                    Br[0][r] = fmaf(w.y, q.x, Br[0][r]);
-                    Bi[0][r] = fmaf(w.y, q.y, Bi[0][r]);
-                    Br[1][r] = fmaf(w.y, q.z, Br[1][r]);
-                    Bi[1][r] = fmaf(w.y, q.w, Bi[1][r]);
+                    Bv[0][r] = __ffma2_rn(wb, lo, Bv[0][r]);
+                    Bv[1][r] = __ffma2_rn(wb, hi, Bv[1][r]);
                 }
             }
         }
@@ -246,18 +247,16 @@ __device__ __forceinline__ void col_accumulate2(const float4* tb, WF wts, int nt
 #pragma unroll
         for (int tt = 0; tt < REM; ++tt) {
             const float2 w = wts(c * R + tt);
+            const float2 wa = make_float2(w.x, w.x), wb = make_float2(w.y, w.y);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const float4 q = v[r + tt];
-                Ar[0][r] = fmaf(w.x, q.x, Ar[0][r]);
-                Ai[0][r] = fmaf(w.x, q.y, Ai[0][r]);
-                Ar[1][r] = fmaf(w.x, q.z, Ar[1][r]);
-                Ai[1][r] = fmaf(w.x, q.w, Ai[1][r]);
+                const float2 lo = make_float2(q.x, q.y), hi = make_float2(q.z, q.w);
+                A[0][r] = __ffma2_rn(wa, lo, A[0][r]);
+                A[1][r] = __ffma2_rn(wa, hi, A[1][r]);
                 if (HASB) {
-                    Br[0][r] = fmaf(w.y, q.x, Br[0][r]);
-                    Bi[0][r] = fmaf(w.y, q.y, Bi[0][r]);
-                    Br[1][r] = fmaf(w.y, q.z, Br[1][r]);
-                    Bi[1][r] = fmaf(w.y, q.w, Bi[1][r]);
+                    Bv[0][r] = __ffma2_rn(wb, lo, Bv[0][r]);
+                    Bv[1][r] = __ffma2_rn(wb, hi, Bv[1][r]);
                 }
             }
         }
@@ -347,22 +346,30 @@ __global__ void __launch_bounds__(128) col_kernel2(const __grid_constant__ ColAr
     for (int ch = 0; ch < nch; ++ch) {
         cp_async_wait_pending(min(nch - 1 - ch, 7));
         __syncthreads();
-        float Ar[2][R], Ai[2][R], Br[2][R], Bi[2][R];
+        float2 A2[2][R], B2[2][R];
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
-            for (int r = 0; r < R; ++r) { Ar[q][r] = Ai[q][r] = Br[q][r] = Bi[q][r] = 0.f; }
+            for (int r = 0; r < R; ++r) { A2[q][r] = make_float2(0.f, 0.f); B2[q][r] = make_float2(0.f, 0.f); }
         const float4* tb = tile + (ch * TY + rg * R) * CP + cx;
         if constexpr (CAP > 0) {
             const int pbase = job * nt;
             auto wf = [&](int i) { return pw.w[pbase + i]; };
-            if (has_b) col_accumulate2<R, REM, true, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
-            else col_accumulate2<R, REM, false, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
+            if (has_b) col_accumulate2<R, REM, true, CP>(tb, wf, nt, A2, B2);
+            else col_accumulate2<R, REM, false, CP>(tb, wf, nt, A2, B2);
         } else {
             auto wf = [&](int i) { return wts[i]; };
-            if (has_b) col_accumulate2<R, REM, true, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
-            else col_accumulate2<R, REM, false, CP>(tb, wf, nt, Ar, Ai, Br, Bi);
+            if (has_b) col_accumulate2<R, REM, true, CP>(tb, wf, nt, A2, B2);
+            else col_accumulate2<R, REM, false, CP>(tb, wf, nt, A2, B2);
         }
+        float Ar[2][R], Ai[2][R], Br[2][R], Bi[2][R];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                Ar[q][r] = A2[q][r].x; Ai[q][r] = A2[q][r].y;
+                Br[q][r] = B2[q][r].x; Bi[q][r] = B2[q][r].y;
+            }
         if (x < W) {
             if (emode == 2) {  // Gabor theta / pi-theta: X = A - iB, conj(Y) = (Ar - Bi, -(Ai + Br))
                 float2* d0 = dst + doff[0];
@@ -393,7 +400,9 @@ __global__ void __launch_bounds__(128) col_kernel2(const __grid_constant__ ColAr
                     const int yl = ch * TY + rg * R + r;
                     if (yl >= rows_out) break;
                     float2* drow = dst + (size_t)(ys + yl) * W;
-                    for (int o = 0; o < nout; ++o) {
+#pragma unroll
+                    for (int o = 0; o < 4; ++o) {
+                        if (o >= nout) break;
                         float v[4];
 #pragma unroll
                         for (int q = 0; q < 2; ++q) {

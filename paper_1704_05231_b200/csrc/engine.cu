@@ -37,6 +37,7 @@ namespace fgb {
 
 template <typename T> double probe_fma_tflops();
 template <typename T> double probe_fma_reg_tflops(int mode);
+double probe_ffma2_tflops(int mode);
 
 // ===========================================================================
 // errors
@@ -1885,6 +1886,7 @@ double fgb_probe_fp32_tflops(void) { return probe_fma_tflops<float>(); }
 double fgb_probe_fp64_tflops(void) { return probe_fma_tflops<double>(); }
 double fgb_probe_fma(int32_t dtype, int32_t mode) {
     if (mode == 0) return dtype == FGB_F64 ? probe_fma_tflops<double>() : probe_fma_tflops<float>();
+    if (mode >= 4) return dtype == FGB_F64 ? -1.0 : probe_ffma2_tflops(mode);
     return dtype == FGB_F64 ? probe_fma_reg_tflops<double>(mode) : probe_fma_reg_tflops<float>(mode);
 }
 

@@ -66,7 +66,73 @@ __global__ void __launch_bounds__(256) fma_probe_reg(T* out, int iters, const T*
     if (s == (T)12345.678) out[threadIdx.x] = s;
 }
 
+// Packed FP32 (sm_100 FFMA2): 8 float2 accumulators; MODE 4 = uniform (constant
+// bank) float2 multiplier, MODE 5 = register multiplier.
+template <int MODE>
+__global__ void __launch_bounds__(256) fma2_probe(float* out, int iters, const float* wp) {
+    float2 acc[8], v[8], w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        acc[i] = make_float2((threadIdx.x + i) * 1e-3f, (threadIdx.x - i) * 1e-3f);
+        v[i] = make_float2(wp[i] + threadIdx.x, wp[i] - threadIdx.x);
+        w[i] = make_float2(wp[8 + i] + (threadIdx.x & 1) * 1e-7f, wp[8 + i]);
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (MODE == 4) {
+                    const float c = c_probe_w32[u & 7];
+                    acc[i] = __ffma2_rn(make_float2(c, c), v[(i + u) & 7], acc[i]);
+                } else {
+                    acc[i] = __ffma2_rn(w[u & 7], v[(i + u) & 7], acc[i]);
+                }
+            }
+        }
+    }
+    float s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i].x + acc[i].y;
+    if (s == 12345.678f) out[threadIdx.x] = s;
+}
+
 }  // namespace
+
+double probe_ffma2_tflops(int mode) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    float *out = nullptr, *wp = nullptr;
+    if (cudaMalloc(&out, 256 * sizeof(float)) != cudaSuccess) return -1.0;
+    if (cudaMalloc(&wp, 16 * sizeof(float)) != cudaSuccess) return -1.0;
+    float hw[16];
+    for (int i = 0; i < 16; ++i) hw[i] = 0.5f + 0.01f * i;
+    cudaMemcpy(wp, hw, sizeof(hw), cudaMemcpyHostToDevice);
+    cudaMemcpyToSymbol(c_probe_w32, hw, sizeof(hw));
+    auto kern = mode == 4 ? fma2_probe<4> : fma2_probe<5>;
+    const int blocks = sms * 8, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    kern<<<blocks, 256>>>(out, 64, wp);
+    double best = 0.0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        kern<<<blocks, 256>>>(out, iters, wp);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double fmas = 2.0 * (double)blocks * 256 * iters * 16 * 8;
+        best = std::max(best, 2.0 * fmas / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    cudaFree(wp);
+    return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
 
 template <typename T> double probe_fma_reg_tflops(int mode) {
     int dev = 0, sms = 0;

@@ -85,7 +85,9 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
     __syncthreads();
     if (y >= a.H) return;
 
-    T accr[ND][R], acci[ND][R];
+    // accumulators (Jr, Ji) per orientation and output: one FFMA2 (fp32) per
+    // orientation per tap pair: (Jr, Ji) += (kr, ki) * (f[x+t] + f[x-t], f[x+t] - f[x-t])
+    C acc[ND][R];
     // centre tap t = 0: sub-array r, index tx + hp/R
     {
         const int base = tx + hp / R;
@@ -93,10 +95,7 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
         for (int r = 0; r < R; ++r) {
             T v = my[r * S + base];
 #pragma unroll
-            for (int k = 0; k < ND; ++k) {
-                accr[k][r] = W(k * 2) * v;
-                acci[k][r] = T(0);
-            }
+            for (int k = 0; k < ND; ++k) acc[k][r] = mk<T>(W(k * 2) * v, T(0));
         }
     }
     const int nch = hp / R;
@@ -135,11 +134,15 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const T p = rv[r + tt], m = lv[r - tt + R - 1];
-                const T s = p + m, d = p - m;
+                const C sd = mk<T>(p + m, p - m);
 #pragma unroll
                 for (int k = 0; k < ND; ++k) {
-                    accr[k][r] = fma(wr[k], s, accr[k][r]);
-                    acci[k][r] = fma(wi[k], d, acci[k][r]);
+                    if constexpr (sizeof(T) == 4) {
+                        acc[k][r] = __ffma2_rn(make_float2(wr[k], wi[k]), sd, acc[k][r]);
+                    } else {
+                        acc[k][r].x = fma(wr[k], sd.x, acc[k][r].x);
+                        acc[k][r].y = fma(wi[k], sd.y, acc[k][r].y);
+                    }
                 }
             }
         }
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
         C v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            T re = accr[k][r], im = acci[k][r];
+            T re = acc[k][r].x, im = acc[k][r].y;
             if (g.has_phase) {
                 const T pr = g.phase_re[k], pi = g.phase_im[k];
                 T nr = pr * re - pi * im;
