@@ -32,7 +32,6 @@ import ctypes as C
 import json
 import math
 import os
-import subprocess
 import sys
 import time
 
@@ -92,49 +91,56 @@ def unit_name(cfg):
 # clocks
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons DURING the timed region: an NVML polling
+    thread (1 ms period, so even sub-second regions get samples); falls back
+    to `nvidia-smi -lms 50` when NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, dev):
         self.dev = dev
-        self.p = None
+        self.samples = []
+        self.mx = None
 
     def __enter__(self):
+        import threading
+
+        self.stop = threading.Event()
+        self.th = None
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def run():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(sm), int(rs)))
+                    except Exception:
+                        pass
+                    self.stop.wait(0.001)
+
+            self.th = threading.Thread(target=run, daemon=True)
+            self.th.start()
         except Exception:
-            self.p = None
+            self.th = None
         return self
 
     def __exit__(self, *a):
-        self.lines = []
-        if self.p is not None:
-            self.p.terminate()
-            try:
-                out, _ = self.p.communicate(timeout=5)
-            except Exception:
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+        if self.th is not None:
+            self.stop.set()
+            self.th.join(2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            f = [x.strip() for x in l.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": [], "samples": 0, "source": "nvml"}
+        reasons = sorted(n for n, bit in self.REASONS.items() if any(r & bit for _, r in self.samples))
+        return {"sm_mhz": float(np.median([s for s, _ in self.samples])), "sm_max_mhz": self.mx, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------
