@@ -18,6 +18,9 @@
  *   fgb_sdft            sdft_full             sdft.py:178-213
  *   fgb_sdft_bin        sdft_bin              sdft.py:169-175
  *   fgb_sdft_horizontal sdft_horizontal       sdft.py:134-150
+ *   fgb_fir_gabor       fir_gabor             oracle.py:53-66   (GPU brute force)
+ *   fgb_localized_dft   localized_dft         oracle.py:69-109  (GPU brute force)
+ *   fgb_gbnk_write_device write_bank_container image_io.py:157-179 (device-fed)
  *   fgb_iir_coeffs      make_coeffs           gaussian.py:164-185
  *   fgb_sampled_gaussian sampled_gaussian     gaussian.py:188-195
  *   fgb_pad_radius      pad_radius            gaussian.py:198-212
@@ -140,6 +143,25 @@ int32_t fgb_horizontal_stage_host(const fgb_filter_desc* d, const void* img_host
 int32_t fgb_vertical_stage_host(const fgb_filter_desc* d, const void* j_host, void* out_host, int32_t conjugate);
 int32_t fgb_sdft_bin_host(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img_host, void* out_host);
 int32_t fgb_sdft_horizontal_host(const fgb_sdft_desc* d, int32_t u, const void* img_host, void* j_host);
+
+/* ---- brute-force references (oracle.py:53-109), direct 2-D tap sums ---- */
+/* fir_gabor(f, p, OracleConfig(radius)): replicate boundary.  localized_dft(f,
+ * u, v, spec, OracleConfig(radius)): Gaussian (replicate) or box (zero)
+ * window.  O(support^2) per pixel; validation / `compare` at full size. */
+int32_t fgb_fir_gabor(const fgb_filter_desc* d, double radius, const void* img, void* out, void* stream);
+int32_t fgb_localized_dft(const fgb_sdft_desc* d, int32_t u, int32_t v, double radius, const void* img, void* out,
+                          void* stream);
+int32_t fgb_fir_gabor_host(const fgb_filter_desc* d, double radius, const void* img_host, void* out_host);
+int32_t fgb_localized_dft_host(const fgb_sdft_desc* d, int32_t u, int32_t v, double radius, const void* img_host,
+                               void* out_host);
+
+/* ---- GBNK container from device outputs (image_io.py:157-179) ---------- */
+/* Writes n_entries interleaved-complex [H][W] device planes (dtype FGB_F32 /
+ * FGB_F64) as float64 re/im planes with params[3*k..3*k+2] = (omega, theta,
+ * sigma) or (u, v, sigma); sdft != 0 sets the SDFT flag bit.  Synchronous:
+ * the D2H of entry k+1 overlaps the file write of entry k. */
+int32_t fgb_gbnk_write_device(const char* path, const double* params, int32_t n_entries, int32_t height, int32_t width,
+                              int32_t dtype, const void* dev_entries, int32_t sdft, void* stream);
 
 /* ---- measurement ------------------------------------------------------- */
 /* Live per-kernel timing: while enabled, every launch is bracketed by CUDA

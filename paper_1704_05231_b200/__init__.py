@@ -13,7 +13,17 @@ for throughput runs.
 """
 
 from ._precision import get_precision, set_precision
-from .image_io import ComplexImage, RealImage
+from .image_io import (
+    ComplexImage,
+    ContainerFormatError,
+    ImageFormatError,
+    RealImage,
+    load_grayscale,
+    read_bank_container,
+    write_bank_container,
+    write_container_from_device,
+    write_magnitude,
+)
 from .gaussian import (
     Box,
     ExactFIR,
@@ -34,7 +44,8 @@ from .bank import (
     vertical_stage_conjugate,
 )
 from .sdft import SdftOutput, SdftSpec, sdft_bin, sdft_full, sdft_horizontal
-from .metrics import OpCounters, per_pixel_counts
+from .metrics import OpCounters, SerReport, fit_affine, fit_features, per_pixel_counts, ser, ser_report
+from .bruteforce import OracleConfig, fir_gabor, localized_dft
 
 __all__ = [
     "RealImage",
@@ -65,6 +76,21 @@ __all__ = [
     "sdft_full",
     "OpCounters",
     "per_pixel_counts",
+    "SerReport",
+    "ser",
+    "ser_report",
+    "fit_affine",
+    "fit_features",
+    "OracleConfig",
+    "fir_gabor",
+    "localized_dft",
+    "load_grayscale",
+    "write_magnitude",
+    "write_bank_container",
+    "read_bank_container",
+    "write_container_from_device",
+    "ImageFormatError",
+    "ContainerFormatError",
     "set_precision",
     "get_precision",
 ]

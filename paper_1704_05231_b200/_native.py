@@ -116,6 +116,12 @@ _SIGS = {
     "fgb_vertical_stage_host": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp, C.c_int32]),
     "fgb_sdft_bin_host": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, C.c_int32, _vp, _vp]),
     "fgb_sdft_horizontal_host": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, _vp, _vp]),
+    "fgb_fir_gabor": (C.c_int32, [_P(fgb_filter_desc), C.c_double, _vp, _vp, _vp]),
+    "fgb_localized_dft": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, C.c_int32, C.c_double, _vp, _vp, _vp]),
+    "fgb_fir_gabor_host": (C.c_int32, [_P(fgb_filter_desc), C.c_double, _vp, _vp]),
+    "fgb_localized_dft_host": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, C.c_int32, C.c_double, _vp, _vp]),
+    "fgb_gbnk_write_device": (C.c_int32, [C.c_char_p, _P(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                          _vp, C.c_int32, _vp]),
     "fgb_profile_enable": (None, [C.c_int32]),
     "fgb_profile_read": (C.c_int32, [_P(fgb_prof_entry), C.c_int32]),
     "fgb_launch_count": (C.c_int64, []),

@@ -469,6 +469,53 @@ cudaError_t launch_rem(const ColArgs<T>& a, const cx_t<T>* pw_host, int G, size_
 
 int g_sm_count = 0;
 
+// Fallback for very long kernels (the (S + nt - 1)-row tile would not fit in
+// shared memory, e.g. sigma = 50 at radius 6 -> 605 taps): each thread reads
+// its column straight from global memory (L1/L2 cached), R rows per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) col_kernel_gmem(ColArgs<T> a) {
+    constexpr int R = 4;
+    using C = cx_t<T>;
+    const int job = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
+    const ColJob<T>* jb = a.jobs + job;
+    const int x = blockIdx.x * 32 + threadIdx.x;
+    const int y0 = (blockIdx.y * blockDim.y + threadIdx.y) * R;
+    if (x >= a.W || y0 >= a.H) return;
+    const C* src = a.src_base + jb->src_off + (size_t)b * a.src_bstride + x;
+    const C* w = a.weights + jb->wofs;
+    T Ar[R] = {}, Ai[R] = {}, Br[R] = {}, Bi[R] = {};
+    for (int q = 0; q < a.nt; ++q) {
+        const C k = __ldg(w + q);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            int yy = y0 + r + a.t0 + q;
+            C v;
+            if (a.zero_boundary && (yy < 0 || yy >= a.H)) {
+                v = mk<T>(T(0), T(0));
+            } else {
+                yy = clampi(yy, 0, a.H - 1);
+                v = __ldg(src + (size_t)yy * a.W);
+            }
+            Ar[r] = fma(k.x, v.x, Ar[r]);
+            Ai[r] = fma(k.x, v.y, Ai[r]);
+            Br[r] = fma(k.y, v.x, Br[r]);
+            Bi[r] = fma(k.y, v.y, Bi[r]);
+        }
+    }
+    const size_t ob = (size_t)b * a.dst_bstride;
+    for (int r = 0; r < R; ++r) {
+        const int y = y0 + r;
+        if (y >= a.H) break;
+        const T xr = Ar[r] + Bi[r], xi = Ai[r] - Br[r], yr = Ar[r] - Bi[r], yi = Ai[r] + Br[r];
+        for (int o = 0; o < jb->nout; ++o) {
+            T re = jb->base[o] ? yr : xr, im = jb->base[o] ? yi : xi;
+            if (jb->conj[o]) im = -im;
+            const T pr = jb->phase_re[o], pi = jb->phase_im[o];
+            a.dst_base[jb->dst_off[o] + ob + (size_t)y * a.W + x] = mk<T>(pr * re - pi * im, pr * im + pi * re);
+        }
+    }
+}
+
 }  // namespace
 
 template <typename T> size_t col_smem(int nt, int rows) {  // tile only (+ taps when not in params)
@@ -526,7 +573,11 @@ template <typename T> cudaError_t launch_col(const ColArgs<T>& a_in, const cx_t<
     const int G = bestG;
     const int TY = bestMode == 0 ? G * R : (bestMode == 2 ? 4 : 2) * G * R;
     if (bestS == 0) {
-        if (col_smem<T>(a.nt, TY) > 220 * 1024) return cudaErrorInvalidConfiguration;
+        if (col_smem<T>(a.nt, TY) > 200 * 1024) {
+            dim3 grid((a.W + 31) / 32, (a.H + 4 * 8 - 1) / (4 * 8), a.njobs * a.batch);
+            col_kernel_gmem<T><<<grid, dim3(32, 8), 0, s>>>(a);
+            return cudaGetLastError();
+        }
         bestS = TY;
     }
     a.seg = bestS;

@@ -36,6 +36,8 @@
 namespace fgb {
 
 template <typename T> double probe_fma_tflops();
+int gbnk_write_device(const char* path, const double* params, int n_entries, int H, int W, int dtype,
+                      const void* dev_entries, int sdft, cudaStream_t s, std::string* err);
 template <typename T> double probe_fma_reg_tflops(int mode);
 double probe_ffma2_tflops(int mode);
 
@@ -882,7 +884,16 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
     const int64_t lane_stride = plain_fir ? max_nj * HW : (2 * max_nj + 1) * HW;
     int64_t need = 0;
     int li = 0;
-    for (int i = 0; i < d.n_freq; ++i) {
+    // emit the heaviest frequency first: the longest lane chain starts first and the
+    // small-sigma kernels fill its gaps (FGB_FREQ_ORDER=asc restores reference order)
+    std::vector<int> order;
+    for (int i = 0; i < d.n_freq; ++i) order.push_back(i);
+    const char* fo = std::getenv("FGB_FREQ_ORDER");
+    if (!(fo && std::string(fo) == "asc"))
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+            return d.sigmas[x] * (double)per_f[x].size() > d.sigmas[y] * (double)per_f[y].size();
+        });
+    for (int i : order) {
         if (per_f[i].empty()) continue;
         b.lane = li % NL;
         const int64_t j0 = b.lane * lane_stride;
@@ -1633,6 +1644,94 @@ static int32_t sdft_t(const fgb_sdft_desc* d, int u, int v, const void* img, voi
     return execute<T>(*p, cx, d->img, img, out, s);
 }
 
+// ===========================================================================
+// brute-force 2-D oracles on the GPU (oracle.py:53-109)
+// ===========================================================================
+template <typename T>
+static int32_t direct2d_run(const fgb_image& im, const std::vector<cd>& k, int ky, int kx, int oy, int ox, int zero,
+                            const void* img, void* out, cudaStream_t s) {
+    using C = cx_t<T>;
+    std::vector<C> hk(k.size());
+    for (size_t i = 0; i < k.size(); ++i) hk[i] = mk<T>((T)k[i].real(), (T)k[i].imag());
+    C* dk = nullptr;
+    FGB_CUDA(cudaMallocAsync((void**)&dk, hk.size() * sizeof(C), s));
+    FGB_CUDA(cudaMemcpyAsync(dk, hk.data(), hk.size() * sizeof(C), cudaMemcpyHostToDevice, s));
+    Direct2DArgs<T> a{};
+    a.img = (const T*)img;
+    a.pitch = im.pitch;
+    a.img_bstride = im.batch > 1 ? im.batch_stride : (int64_t)im.height * im.pitch;
+    a.out = (C*)out;
+    a.out_bstride = (int64_t)im.height * im.width;
+    a.kern = dk;
+    a.ky = ky;
+    a.kx = kx;
+    a.oy = oy;
+    a.ox = ox;
+    a.zero_boundary = zero;
+    a.H = im.height;
+    a.W = im.width;
+    a.batch = im.batch;
+    cudaError_t e = launch_direct2d<T>(a, s);
+    cudaFreeAsync(dk, s);
+    if (e == cudaErrorInvalidConfiguration) return fail(FGB_EINVAL, "oracle kernel support too large for the direct GPU path");
+    FGB_CUDA(e);
+    FGB_CUDA(cudaStreamSynchronize(s));  // the host kernel table must outlive the H2D copy
+    return FGB_OK;
+}
+
+// fir_gabor (oracle.py:53-66): env * e^{i w (dx cos + dy sin)}, reversed, replicate pad by half
+static void fir_gabor_kernel(const fgb_filter_desc& d, double radius, std::vector<cd>* k, int* half) {
+    int h;
+    std::vector<double> g = sampled_gaussian(d.sigma, radius, &h);
+    const double th = norm_theta(d.theta);
+    const int n = 2 * h + 1;
+    k->assign((size_t)n * n, cd(0, 0));
+    for (int iy = 0; iy < n; ++iy)
+        for (int ix = 0; ix < n; ++ix) {
+            // reversed: kernel row iy holds dy = h - iy, column ix holds dx = h - ix
+            const double dy = (double)(h - iy), dx = (double)(h - ix);
+            const double ph = d.omega * (std::cos(th) * dx + std::sin(th) * dy);
+            const double env = g[h - iy + h] * g[h - ix + h];
+            (*k)[(size_t)iy * n + ix] = cd(env * std::cos(ph), env * std::sin(ph));
+        }
+    *half = h;
+}
+
+// localized_dft (oracle.py:69-109)
+static void ldft_kernel(const fgb_sdft_desc& d, int u, int v, double radius, std::vector<cd>* k, int* ky, int* kx,
+                        int* oy, int* ox, int* zero) {
+    const int mx = d.mx, my = d.my;
+    std::vector<double> gx, gy;
+    int lox, hix, loy, hiy;
+    if (d.smoother.kind == FGB_SMOOTH_BOX) {
+        lox = -(mx / 2); hix = mx - 1 - mx / 2;
+        loy = -(my / 2); hiy = my - 1 - my / 2;
+        gx.assign(hix - lox + 1, 1.0);
+        gy.assign(hiy - loy + 1, 1.0);
+        *zero = 1;
+    } else {
+        int hx, hy;
+        const double s = sdft_sigma(d);
+        gx = sampled_gaussian(s, radius, &hx);
+        gy = sampled_gaussian(s, radius, &hy);
+        lox = -hx; hix = hx; loy = -hy; hiy = hy;
+        *zero = 0;
+    }
+    *ky = hiy - loy + 1;
+    *kx = hix - lox + 1;
+    *oy = -loy;
+    *ox = -lox;
+    const double w0x = 2.0 * M_PI / mx, w0y = 2.0 * M_PI / my;
+    k->assign((size_t)(*ky) * (*kx), cd(0, 0));
+    for (int iy = 0; iy < *ky; ++iy)
+        for (int ix = 0; ix < *kx; ++ix) {
+            const double dm = (double)(lox + ix), dn = (double)(loy + iy);
+            const double ph = w0x * u * (mx / 2 + dm) + w0y * v * (my / 2 + dn);
+            const double env = gy[iy] * gx[ix];
+            (*k)[(size_t)iy * (*kx) + ix] = cd(env * std::cos(ph), env * std::sin(ph));
+        }
+}
+
 }  // namespace fgb
 
 // ===========================================================================
@@ -1840,6 +1939,61 @@ int32_t fgb_sdft_horizontal_host(const fgb_sdft_desc* d, int32_t u, const void* 
     return host_call(d->img, n, img_host, j_host, [&](void* i, void* o, cudaStream_t s) {
         return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, -1, i, o, s) : sdft_t<double>(d, u, -1, i, o, s);
     });
+}
+
+int32_t fgb_fir_gabor(const fgb_filter_desc* d, double radius, const void* img, void* out, void* stream) {
+    FGB_TRY(validate_filter(d, false));
+    if (radius < 3) return fail(FGB_EINVAL, "truncation radius must be at least 3 sigma");
+    std::vector<cd> k;
+    int h;
+    fir_gabor_kernel(*d, radius, &k, &h);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int n = 2 * h + 1;
+    return d->img.dtype == FGB_F32 ? direct2d_run<float>(d->img, k, n, n, h, h, 0, img, out, s)
+                                   : direct2d_run<double>(d->img, k, n, n, h, h, 0, img, out, s);
+}
+
+int32_t fgb_localized_dft(const fgb_sdft_desc* d, int32_t u, int32_t v, double radius, const void* img, void* out,
+                          void* stream) {
+    FGB_TRY(validate_sdft(d));
+    if (u < 0 || u >= d->mx || v < 0 || v >= d->my) return fail(FGB_EINVAL, "bin indices outside the window grid");
+    if (radius < 3) return fail(FGB_EINVAL, "truncation radius must be at least 3 sigma");
+    std::vector<cd> k;
+    int ky, kx, oy, ox, zero;
+    ldft_kernel(*d, u, v, radius, &k, &ky, &kx, &oy, &ox, &zero);
+    cudaStream_t s = (cudaStream_t)stream;
+    return d->img.dtype == FGB_F32 ? direct2d_run<float>(d->img, k, ky, kx, oy, ox, zero, img, out, s)
+                                   : direct2d_run<double>(d->img, k, ky, kx, oy, ox, zero, img, out, s);
+}
+
+int32_t fgb_fir_gabor_host(const fgb_filter_desc* d, double radius, const void* img_host, void* out_host) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
+        return fgb_fir_gabor(d, radius, i, o, s);
+    });
+}
+
+int32_t fgb_localized_dft_host(const fgb_sdft_desc* d, int32_t u, int32_t v, double radius, const void* img_host,
+                               void* out_host) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t n = (int64_t)d->img.height * d->img.width * d->img.batch;
+    return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
+        return fgb_localized_dft(d, u, v, radius, i, o, s);
+    });
+}
+
+int32_t fgb_gbnk_write_device(const char* path, const double* params, int32_t n_entries, int32_t height, int32_t width,
+                              int32_t dtype, const void* dev_entries, int32_t sdft, void* stream) {
+    if (!path || !params || !dev_entries) return fail(FGB_EINVAL, "null argument");
+    if (n_entries < 1) return fail(FGB_EINVAL, "container must hold at least one entry");
+    if (height < 1 || width < 1) return fail(FGB_EINVAL, "image dimensions must be at least 1x1");
+    std::string err;
+    const int rc = gbnk_write_device(path, params, n_entries, height, width, dtype, dev_entries, sdft,
+                                     (cudaStream_t)stream, &err);
+    if (rc == -1) return fail(FGB_EINVAL, err);
+    if (rc == -2) return fail(FGB_ECUDA, err);
+    return FGB_OK;
 }
 
 int32_t fgb_stream_synchronize(void* stream) {

@@ -130,6 +130,20 @@ template <typename T> cudaError_t launch_iir_col(const IirArgs<T>& a, cudaStream
 template <typename T> size_t iir_scratch_elems(int H, int W, int P, int njobs, int batch);
 size_t iir_state_doubles(int W, int nseg, int njobs, int batch);
 
+// ---- brute-force 2-D references (bruteforce.cu) ---------------------------
+template <typename T> struct Direct2DArgs {
+    const T* img;
+    int64_t pitch, img_bstride;
+    cx_t<T>* out;
+    int64_t out_bstride;
+    const cx_t<T>* kern;   // [ky][kx] complex kernel (device)
+    int ky, kx, oy, ox;    // input row/col = y + iy - oy, x + ix - ox
+    int zero_boundary;
+    int H, W, batch;
+};
+template <typename T> cudaError_t launch_direct2d(const Direct2DArgs<T>& a, cudaStream_t s);
+template <typename T> size_t direct2d_smem(int ky, int kx);
+
 // ---- fused small-sigma bank stage (bank_fused.cu) ------------------------
 struct BankFusedOut {
     int64_t direct;  // complex elements from dst (batch 0) of F_theta

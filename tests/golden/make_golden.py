@@ -160,6 +160,24 @@ for kn, k in (("fir6", ("fir", 6.0)), ("box1", ("box", 1))):
     spec = fg.SdftSpec(4, 4, kind_obj(k))
     put(f"ldft.{kn}", fg.localized_dft(fg.RealImage.from_array(f3), 1, 3, spec))
 
+# 8. I/O and metrics (image_io.py:136-212, metrics.py:63-83): bytes written by the
+#    reference for known inputs, SER of known pairs.
+import tempfile  # noqa: E402
+
+_ents = [(fg.GaborParams(1.0 + i, 0.3 * i, 2.0), fg.ComplexImage.from_planes(f3 * (i + 1), -f3 / (i + 2)))
+         for i in range(3)]
+with tempfile.TemporaryDirectory() as td:
+    pth = os.path.join(td, "b.gbnk")
+    fg.write_bank_container(_ents, pth)
+    arrays["io.gbnk_bytes"] = np.frombuffer(open(pth, "rb").read(), dtype=np.uint8).copy()
+    fg.write_bank_container([((1.0, 2.0, 0.5), _ents[0][1])], pth, sdft=True)
+    arrays["io.gbnk_sdft_bytes"] = np.frombuffer(open(pth, "rb").read(), dtype=np.uint8).copy()
+    pg = os.path.join(td, "m.pgm")
+    fg.write_magnitude(_ents[1][1], pg)
+    arrays["io.magnitude_pgm_bytes"] = np.frombuffer(open(pg, "rb").read(), dtype=np.uint8).copy()
+_a, _b = _ents[0][1], fg.ComplexImage.from_planes(f3 * 1.01 + 0.3, -f3 / 2 + 0.01)
+meta["ser"] = {"real": fg.ser(_b, _a, "real"), "imag": fg.ser(_b, _a, "imag")}
+
 np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
 with open(os.path.join(HERE, "golden.json"), "w") as fh:
     json.dump(meta, fh, indent=1, sort_keys=True)

@@ -110,3 +110,13 @@ def test_odd_width_and_tiny_images(env):
         ref = O.compute_bank(fimg, spec.frequencies, 4, spec.sigmas, ("fir", 3.0))
         for (p, img), r in zip(out.entries, ref):
             assert max_rel_err(img, r[3:]) <= 1e-10, shape
+
+
+def test_very_long_kernels_fallback(env):
+    """sigma = 50 at radius 6 (605 taps): column tile beyond shared memory -> global-memory path."""
+    torch, fg, D, P = env
+    fimg = random_image(8, 96, 0.0, 1.0, width=64)
+    p = fg.GaborParams(0.125, 0.7, 2 * math.pi / 0.125)
+    out = fg.gabor_filter(fg.RealImage.from_array(fimg), p, fg.ExactFIR(), fg.OpCounters(), precision="f64")
+    ref = O.gabor_filter(fimg, p.omega, p.theta, p.sigma, ("fir", 6.0))
+    assert max_rel_err(out, ref) <= 1e-10
