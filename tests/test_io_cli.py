@@ -212,3 +212,78 @@ def test_config4_bins_vs_gpu_bruteforce(fg):
             err = torch.maximum((got.real - ref.real).abs().max(), (got.imag - ref.imag).abs().max()) / scale
             worst = max(worst, err.item())
     assert worst <= 1e-5, worst
+
+
+def _bruteforce_worst(fg, img_t64, spec, out, entries, radius=3.0):
+    """max over entries of max|got-ref|/max|ref| with the fp64 GPU brute force (on device)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1704_05231_b200 import _native as N
+    from paper_1704_05231_b200.gabor import _filter_desc
+
+    H, W = img_t64.shape
+    ref = torch.empty((H, W), dtype=torch.complex128, device="cuda")
+    worst = 0.0
+    for e, (i, k) in enumerate(entries):
+        p = fg.GaborParams(spec.frequencies[i], k * math.pi / spec.orientations_n, spec.sigma_for(i))
+        d = _filter_desc(H, W, p, fg.ExactFIR(radius), "f64")
+        N.check(N.lib.fgb_fir_gabor(C.byref(d), radius, C.c_void_p(img_t64.data_ptr()), C.c_void_p(ref.data_ptr()),
+                                    C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        got = out[e].to(torch.complex128)
+        scale = torch.maximum(ref.real.abs().max(), ref.imag.abs().max())
+        err = torch.maximum((got.real - ref.real).abs().max(), (got.imag - ref.imag).abs().max()) / scale
+        worst = max(worst, err.item())
+    return worst
+
+
+@pytest.mark.gpu
+def test_config3_images_vs_gpu_bruteforce(fg):
+    """BASELINE config 3 (batched 64 x 1024^2, N=8 x 5 freqs, sigma up to 32): images
+    0, 31, 63 of the batched fp32 run, all 40 entries each, vs fp64 brute force."""
+    import sys
+
+    import torch
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_1704_05231_b200.device import compute_bank
+
+    cfg = bench.CONFIGS[3]
+    imgs = np.stack([bench.make_image(cfg, i) for i in (0, 31, 63)])
+    spec = fg.BankSpec(tuple(cfg["freqs"]), 8, tuple(cfg["sigmas"]))
+    out = compute_bank(torch.from_numpy(imgs).cuda(), spec, fg.ExactFIR(3.0))
+    ent = [(i, k) for i in range(5) for k in range(8)]
+    worst = max(_bruteforce_worst(fg, torch.from_numpy(imgs[b].astype(np.float64)).cuda(), spec, out[b], ent)
+                for b in range(3))
+    assert worst <= 1e-5, worst
+
+
+@pytest.mark.gpu
+def test_config5_all_entries_vs_gpu_bruteforce(fg):
+    """BASELINE config 5 (8192^2 + gratings, N=16 x 5 freqs, sigma up to 32): all 80
+    entries of the fp32 bank, computed as LPT shards of 8 GPUs' unit lists (compact
+    layouts), against the fp64 brute force on the GPU."""
+    import sys
+
+    import torch
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_1704_05231_b200 import parallel as P
+    from paper_1704_05231_b200.device import compute_bank
+
+    cfg = bench.CONFIGS[5]
+    f = bench.make_image(cfg, 0)
+    spec = fg.BankSpec(tuple(cfg["freqs"]), 16, tuple(cfg["sigmas"]))
+    t32 = torch.from_numpy(f).cuda()
+    t64 = torch.from_numpy(f.astype(np.float64)).cuda()
+    costs = P.bank_unit_costs(cfg["freqs"], cfg["sigmas"], 16, 3.0)
+    worst = 0.0
+    for units in P.lpt_assign(costs, 8):
+        out = compute_bank(t32, spec, fg.ExactFIR(3.0), True, units)[0]
+        worst = max(worst, _bruteforce_worst(fg, t64, spec, out, P.unit_entries(units, 16)))
+        del out
+        torch.cuda.empty_cache()
+    assert worst <= 1e-5, worst
