@@ -25,6 +25,7 @@
 // parameter so no taps are padded.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -568,6 +569,15 @@ template <typename T> cudaError_t launch_col(const ColArgs<T>& a_in, const cx_t<
                 bestG = G;
             }
         }
+    }
+    if (const char* e = std::getenv("FGB_COL_MODE")) {  // experiment knobs: force mode / segment rows
+        const int m = std::atoi(e);
+        if (m >= 0 && m <= 2 && (m == 0 || c2ok)) { bestMode = m; bestG = m == 0 ? 8 : 4; }
+    }
+    if (const char* e = std::getenv("FGB_COL_SEG")) {
+        const int TY = bestMode == 0 ? bestG * R : (bestMode == 2 ? 4 : 2) * bestG * R;
+        const int S = std::atoi(e) / TY * TY;
+        if (S > 0) bestS = S;
     }
     a.col2 = bestMode;
     const int G = bestG;

@@ -120,3 +120,45 @@ def test_very_long_kernels_fallback(env):
     out = fg.gabor_filter(fg.RealImage.from_array(fimg), p, fg.ExactFIR(), fg.OpCounters(), precision="f64")
     ref = O.gabor_filter(fimg, p.omega, p.theta, p.sigma, ("fir", 6.0))
     assert max_rel_err(out, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("kn,shape", [("fir", (2, 48, 80)), ("iir", (2, 33, 71)), ("box", (1, 17, 30)),
+                                      ("sdft", (1, 40, 48)), ("sdft", (1, 23, 31))])
+def test_outputs_fully_written_within_bounds(env, kn, shape):
+    """NaN-poisoned outputs with NaN guard bands on both sides: every output
+    element is written (parity would fail on a left-over NaN) and nothing
+    outside the output is touched (compute-sanitizer is not available on the
+    GPU pool, so this is the out-of-bounds-write check)."""
+    torch, fg, D, P = env
+    b, h, w = shape
+    imgs = np.random.default_rng(11).uniform(0.0, 1.0, size=(b, h, w)).astype(np.float32)
+    t = torch.from_numpy(imgs).cuda()
+    if kn == "sdft":
+        plan = D.SdftPlan(shape, fg.SdftSpec(16, 16, fg.ExactFIR(3.0), 4.0), "f32")
+        n_out = 256
+    else:
+        kind = {"fir": fg.ExactFIR(3.0), "iir": fg.RecursiveIIR(), "box": fg.Box(2)}[kn]
+        spec = fg.BankSpec((math.pi / 2, math.pi / 8), 8, (2.0, 8.0))
+        plan = D.BankPlan(shape, spec, kind, "f32")
+        n_out = plan.entries
+    guard = 4096
+    n = b * n_out * h * w
+    buf = torch.empty((n + 2 * guard,), dtype=torch.complex64, device="cuda")
+    torch.view_as_real(buf).fill_(float("nan"))
+    out = buf[guard:guard + n].view(b, n_out, h, w)
+    plan(t, out)
+    torch.cuda.synchronize()
+    assert torch.isnan(torch.view_as_real(buf[:guard])).all() and torch.isnan(torch.view_as_real(buf[guard + n:])).all()
+    o = out.cpu().numpy()
+    assert np.isfinite(o.view(np.float32)).all()
+    for bi in range(b):
+        f64 = imgs[bi].astype(np.float64)
+        if kn == "sdft":
+            ref = O.sdft_full(f64, 16, 16, ("fir", 3.0), 4.0)
+            err = max(max_rel_err((o[bi, u * 16 + v].real, o[bi, u * 16 + v].imag), ref[u][v])
+                      for u in range(16) for v in range(16))
+        else:
+            ok = {"fir": ("fir", 3.0), "iir": ("iir",), "box": ("box", 2)}[kn]
+            ref = O.compute_bank(f64, spec.frequencies, 8, spec.sigmas, ok)
+            err = max(max_rel_err((o[bi, e].real, o[bi, e].imag), r[3:]) for e, r in enumerate(ref))
+        assert err <= 1e-5

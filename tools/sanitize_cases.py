@@ -1,0 +1,142 @@
+"""Small cases over every kernel family, for compute-sanitizer runs:
+
+    compute-sanitizer --tool memcheck  python tools/sanitize_cases.py
+    compute-sanitizer --tool racecheck python tools/sanitize_cases.py --quick
+
+Covers the bank (FIR/IIR/box, f32/f64, even/odd/ragged widths, batched device
+plans, no-reuse), single filters and stages, the SDFT (fused, generic, IIR,
+box, Mx != My), brute-force oracles on the GPU and the device GBNK writer.
+Each case is also compared with the CPU oracle so a sanitizer-clean run is a
+parity run too.
+"""
+
+import argparse
+import math
+import os
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1704_05231_b200 as fg  # noqa: E402
+from oracle import fastgabor_oracle as O  # noqa: E402
+from paper_1704_05231_b200.device import BankPlan, SdftPlan  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--quick", action="store_true")
+args = ap.parse_args()
+
+rng = np.random.default_rng(7)
+worst = {}
+
+
+def note(name, err, tol):
+    worst[name] = err
+    flag = "ok" if err <= tol else "FAIL"
+    print(f"{flag:4s} {name:40s} {err:.2e}", flush=True)
+
+
+def rel(a, b):
+    if isinstance(b, tuple):  # oracle planes: (re, im) or (omega, theta, sigma, re, im)
+        b = b[-2] + 1j * b[-1]
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+GUARD = 4096  # complex elements of NaN on both sides of every device output
+
+
+def guarded(plan, img, shape, name):
+    """Run a device plan into a NaN-poisoned output with NaN guard bands: any
+    element left unwritten fails the parity check, any write outside the
+    output shows up as a non-NaN guard element."""
+    n = int(np.prod(shape))
+    buf = torch.empty((n + 2 * GUARD,), dtype=torch.complex64, device="cuda")
+    torch.view_as_real(buf).fill_(float("nan"))
+    out = buf[GUARD:GUARD + n].view(shape)
+    plan(img, out)
+    torch.cuda.synchronize()
+    g = torch.cat([buf[:GUARD], buf[GUARD + n:]])
+    note(f"guard {name}", 0.0 if bool(torch.isnan(g.real).all() and torch.isnan(g.imag).all()) else 1.0, 0.5)
+    return out.cpu().numpy()
+
+
+kinds = {"fir": (fg.ExactFIR(3.0), ("fir", 3.0)), "iir": (fg.RecursiveIIR(), ("iir",)), "box": (fg.Box(2), ("box", 2))}
+shapes = [(37, 53), (64, 96), (5, 3)] if args.quick else [(37, 53), (64, 96), (5, 3), (130, 257), (1, 40)]
+
+for (h, w) in shapes:
+    f = rng.uniform(0, 1, size=(h, w))
+    for kn, (k, ok) in kinds.items():
+        if kn == "box" and h < 5:
+            continue
+        for prec, tol in (("f32", 1e-5), ("f64", 1e-10)):
+            out = fg.compute_bank(fg.RealImage.from_array(f), fg.BankSpec((math.pi / 2, math.pi / 4), 4, (2.0, 3.0)), k,
+                                  fg.OpCounters(), precision=prec)
+            ref = O.compute_bank(f, (math.pi / 2, math.pi / 4), 4, (2.0, 3.0), ok)
+            e = max(rel(img.to_complex(), r) for (_, img), r in zip(out.entries, ref))
+            note(f"bank {kn} {prec} {h}x{w}", e, tol)
+        out = fg.compute_bank_noreuse(fg.RealImage.from_array(f), fg.BankSpec((math.pi / 3,), 3, (2.5,)), k,
+                                      fg.OpCounters(), precision="f64")
+        ref = O.compute_bank_noreuse(f, (math.pi / 3,), 3, (2.5,), ok)
+        note(f"noreuse {kn} {h}x{w}", max(rel(i.to_complex(), r) for (_, i), r in zip(out.entries, ref)), 1e-10)
+        p = fg.GaborParams(math.pi / 5, 0.7, 2.0)
+        st = fg.horizontal_stage(fg.RealImage.from_array(f), p, k, fg.OpCounters(), precision="f64")
+        out = fg.vertical_stage(st, fg.OpCounters(), precision="f64")
+        note(f"filter {kn} {h}x{w}", rel(out.to_complex(), O.gabor_filter(f, p.omega, p.theta, p.sigma, ok)), 1e-10)
+
+# batched device plans (batch 2, fp32)
+for (h, w) in ((48, 80), (33, 71)):
+    imgs = rng.uniform(0, 1, size=(2, h, w)).astype(np.float32)
+    spec = fg.BankSpec((math.pi / 2, math.pi / 8), 8, (2.0, 8.0))
+    for kn, (k, ok) in kinds.items():
+        plan = BankPlan((2, h, w), spec, k, "f32")
+        t = torch.from_numpy(imgs).cuda()
+        o = guarded(plan, t, (2, plan.entries, h, w), f"plan {kn} {h}x{w}")
+        for b in range(2):
+            ref = O.compute_bank(imgs[b].astype(np.float64), spec.frequencies, 8, spec.sigmas, ok)
+            note(f"plan {kn} b{b} {h}x{w}", max(rel(o[b, e], r) for e, r in enumerate(ref)), 1e-5)
+
+# SDFT: fused (FIR, square), generic (IIR, box, Mx != My)
+for (h, w) in ((40, 48), (23, 31)):
+    f = rng.uniform(0, 1, size=(h, w))
+    for mx, my, (k, ok), sg in ((8, 8, kinds["fir"], 2.0), (4, 8, kinds["fir"], 1.5), (8, 8, kinds["iir"], 2.0),
+                               (4, 4, (fg.Box(1), ("box", 1)), None)):
+        if isinstance(k, fg.Box):
+            spec = fg.SdftSpec(mx, my, k)
+        else:
+            spec = fg.SdftSpec(mx, my, k, sg)
+        for prec, tol in (("f32", 1e-5), ("f64", 1e-10)):
+            out = fg.sdft_full(fg.RealImage.from_array(f), spec, fg.OpCounters(), precision=prec)
+            ref = O.sdft_full(f, mx, my, ok, spec.sigma)
+            e = max(rel(out.bins[u][v].to_complex(), ref[u][v]) for u in range(mx) for v in range(my))
+            note(f"sdft {mx}x{my} {type(k).__name__} {prec} {h}x{w}", e, tol)
+    plan = SdftPlan((1, h, w), fg.SdftSpec(16, 16, fg.ExactFIR(3.0), 4.0), "f32")
+    o = guarded(plan, torch.from_numpy(f.astype(np.float32)[None]).cuda(), (1, 256, h, w), f"sdft plan {h}x{w}")
+    ref = O.sdft_full(f.astype(np.float32).astype(np.float64), 16, 16, ("fir", 3.0), 4.0)
+    note(f"sdft plan 16x16 {h}x{w}", max(rel(o[0, u * 16 + v], ref[u][v]) for u in range(16) for v in range(16)), 1e-5)
+
+# brute-force GPU oracles
+f = rng.uniform(0, 1, size=(30, 41))
+cfg = fg.OracleConfig(3.0)
+bf = fg.fir_gabor(fg.RealImage.from_array(f), fg.GaborParams(math.pi / 4, 0.3, 2.0), cfg)
+note("fir_gabor", rel(bf.to_complex(), O.fir_gabor(f, math.pi / 4, 0.3, 2.0, 3.0)), 1e-10)
+ld = fg.localized_dft(fg.RealImage.from_array(f), 2, 3, fg.SdftSpec(8, 8, fg.ExactFIR(3.0), 2.0), cfg)
+note("localized_dft", rel(ld.to_complex(), O.localized_dft(f, 2, 3, 8, 8, ("fir", 3.0), 2.0, 3.0)), 1e-10)
+
+# device GBNK writer
+plan = BankPlan((1, 24, 40), fg.BankSpec((math.pi / 4,), 4, (2.0,)), fg.ExactFIR(3.0), "f32")
+o = plan(torch.from_numpy(rng.uniform(0, 1, size=(1, 24, 40)).astype(np.float32)).cuda(), plan.new_output())
+with tempfile.TemporaryDirectory() as d:
+    path = os.path.join(d, "b.gbnk")
+    fg.write_container_from_device(o[0], [(math.pi / 4, k * math.pi / 4, 2.0) for k in range(4)], path)
+    ents, _ = fg.read_bank_container(path)
+    note("gbnk device writer", max(rel(img.to_complex(), o[0, e].cpu().numpy().astype(np.complex128))
+                                   for e, (_, img) in enumerate(ents)), 1e-7)
+torch.cuda.synchronize()
+bad = [k for k, v in worst.items()
+       if not v <= (0.5 if k.startswith("guard") else 1e-5 if "f32" in k or "plan" in k else 1e-7 if "gbnk" in k else 1e-10)]
+print("cases", len(worst), "fails", bad)
+sys.exit(1 if bad else 0)
