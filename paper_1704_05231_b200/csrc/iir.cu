@@ -30,6 +30,7 @@ namespace fgb {
 namespace {
 
 constexpr int kIirTX = 32;
+constexpr int kIirU = 3;  // samples per load batch
 
 __device__ __forceinline__ void mat3_apply(const double* A, const double* s, double* o) {
     o[0] = A[0] * s[0] + A[1] * s[1] + A[2] * s[2];
@@ -75,19 +76,29 @@ __global__ void __launch_bounds__(128) iir_fwd(IirArgs<T> a) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) p[q][0] = p[q][1] = p[q][2] = 0.0;
     }
-#pragma unroll 2
-    for (int n = n0; n < n1; ++n) {
-        const int yy = clampi(n - P, 0, H - 1);
-        modulate<T>(job, src[(size_t)yy * W], tabm[n], z);
+    // kIirU input samples are loaded before the dependent recursion consumes
+    // them (the stores into scratch would otherwise keep the compiler from
+    // hoisting the next loads: one load in flight per thread)
+    for (int nb = n0; nb < n1; nb += kIirU) {
+        cx_t<T> v[kIirU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!plane_used(need, q)) continue;
-            const double t = fma(B, z[q], -(a2 * p[q][1] + a3 * p[q][2]));
-            const double yv = fma(-a1, p[q][0], t);
-            p[q][2] = p[q][1];
-            p[q][1] = p[q][0];
-            p[q][0] = yv;
-            sc[q * plane + (size_t)n * W] = (T)yv;
+        for (int u = 0; u < kIirU; ++u)
+            if (nb + u < n1) v[u] = src[(size_t)clampi(nb + u - P, 0, H - 1) * W];
+#pragma unroll
+        for (int u = 0; u < kIirU; ++u) {
+            const int n = nb + u;
+            if (n >= n1) break;
+            modulate<T>(job, v[u], tabm[n], z);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!plane_used(need, q)) continue;
+                const double t = fma(B, z[q], -(a2 * p[q][1] + a3 * p[q][2]));
+                const double yv = fma(-a1, p[q][0], t);
+                p[q][2] = p[q][1];
+                p[q][1] = p[q][0];
+                p[q][0] = yv;
+                sc[q * plane + (size_t)n * W] = (T)yv;
+            }
         }
     }
     // local end state (y[end], y[end-1], y[end-2]) per plane
@@ -142,19 +153,30 @@ __global__ void __launch_bounds__(128) iir_bwd(IirArgs<T> a) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) u[q][0] = u[q][1] = u[q][2] = 0.0;
     }
-    for (int n = n1 - 1; n >= n0; --n) {
-        const double* g = a.g + 3 * (n - n0);
+    for (int nb = n1 - 1; nb >= n0; nb -= kIirU) {
+        T ys[kIirU][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!plane_used(need, q)) continue;
-            const double yl = (double)sc[q * plane + (size_t)n * W];
-            const double yv = seg == 0 ? yl : yl + g[0] * s_in[q][0] + g[1] * s_in[q][1] + g[2] * s_in[q][2];
-            const double t = fma(B, yv, -(a2 * u[q][1] + a3 * u[q][2]));
-            const double uv = fma(-a1, u[q][0], t);
-            u[q][2] = u[q][1];
-            u[q][1] = u[q][0];
-            u[q][0] = uv;
-            sc[q * plane + (size_t)n * W] = (T)uv;
+        for (int u = 0; u < kIirU; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (nb - u >= n0 && plane_used(need, q)) ys[u][q] = sc[q * plane + (size_t)(nb - u) * W];
+#pragma unroll
+        for (int uu = 0; uu < kIirU; ++uu) {
+            const int n = nb - uu;
+            if (n < n0) break;
+            const double* g = a.g + 3 * (n - n0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!plane_used(need, q)) continue;
+                const double yl = (double)ys[uu][q];
+                const double yv = seg == 0 ? yl : yl + g[0] * s_in[q][0] + g[1] * s_in[q][1] + g[2] * s_in[q][2];
+                const double t = fma(B, yv, -(a2 * u[q][1] + a3 * u[q][2]));
+                const double uv = fma(-a1, u[q][0], t);
+                u[q][2] = u[q][1];
+                u[q][1] = u[q][0];
+                u[q][0] = uv;
+                sc[q * plane + (size_t)n * W] = (T)uv;
+            }
         }
     }
     // local start state (u[start], u[start+1], u[start+2]) -> the backward half of the state buffer
@@ -200,13 +222,24 @@ __global__ void __launch_bounds__(128) iir_out(IirArgs<T> a) {
     const double2* tabr = a.tab_base + job.tabr_off;
     const size_t ob = (size_t)b * a.dst_bstride + x;
     const int lo = max(n0, P), hi = min(n1, P + H);
-    for (int n = lo; n < hi; ++n) {
+    const int need = job.need;
+    for (int nb = lo; nb < hi; nb += kIirU) {
+      T us[kIirU][4];
+#pragma unroll
+      for (int u = 0; u < kIirU; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+              if (nb + u < hi && plane_used(need, q)) us[u][q] = sc[q * plane + (size_t)(nb + u) * W];
+#pragma unroll
+      for (int uu = 0; uu < kIirU; ++uu) {
+        const int n = nb + uu;
+        if (n >= hi) break;
         const double* g = a.g + 3 * (n1 - 1 - n);
         double sv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            if (!plane_used(job.need, q)) { sv[q] = 0.0; continue; }
-            const double ul = (double)sc[q * plane + (size_t)n * W];
+            if (!plane_used(need, q)) { sv[q] = 0.0; continue; }
+            const double ul = (double)us[uu][q];
             sv[q] = last ? ul : ul + g[0] * t_in[q][0] + g[1] * t_in[q][1] + g[2] * t_in[q][2];
         }
         const int yo = n - P;
@@ -219,6 +252,7 @@ __global__ void __launch_bounds__(128) iir_out(IirArgs<T> a) {
             if (job.conj[o]) im = -im;
             a.dst_base[job.dst_off[o] + ob + (size_t)yo * W] = mk<T>((T)re, (T)im);
         }
+      }
     }
 }
 
