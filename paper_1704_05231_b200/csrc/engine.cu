@@ -303,6 +303,8 @@ template <typename T> struct Step {
     IirCoef coef{};
     int64_t scratch_off = 0;  // T elements into the workspace scratch region
     int nseg = 1, seglen = 1;
+    int iir_row = 0;          // lines are image rows (horizontal stage): strided in place, no transposes
+    int iir_real = 0;         // real source (the image) instead of complex J
     int64_t g_off = 0;        // into Plan::dbls: [seglen][3]
     double Aseg[9] = {0}, Alast[9] = {0};
     // ST_BANKF (fp32): tap tables + per-orientation outputs
@@ -497,9 +499,29 @@ template <typename T> struct Builder {
         }
         return off;
     }
-    void iir_step(const std::vector<IirJob<T>>& jobs, Ref src, Ref dst, int H, int W, int P, const IirCoef& c,
-                  int64_t scratch_off, int counted = -1, bool real_in = false) {
-        if (jobs.empty()) return;
+    // H = samples per line (unpadded), W = number of lines.  row_mode: lines
+    // are image rows read / written in place (source real when real_in).
+    void iir_step(const std::vector<IirJob<T>>& jobs_in, Ref src, Ref dst, int H, int W, int P, const IirCoef& c,
+                  int64_t scratch_off, int counted = -1, bool real_in = false, bool row_mode = false) {
+        if (jobs_in.empty()) return;
+        // one modulation pair per kernel job: a two-pair job (Gabor theta and
+        // pi - theta, SDFT bin and mirror) becomes two jobs sharing the source
+        std::vector<IirJob<T>> jobs;
+        for (const auto& j : jobs_in)
+            for (int pr = 0; pr < 2; ++pr) {
+                if (!((j.need >> pr) & 1)) continue;
+                IirJob<T> q = j;
+                q.nout = 0;
+                q.need = 1 << pr;
+                for (int o = 0; o < j.nout; ++o)
+                    if (j.pair[o] == pr) {
+                        q.dst_off[q.nout] = j.dst_off[o];
+                        q.pair[q.nout] = (int8_t)pr;
+                        q.conj[q.nout] = j.conj[o];
+                        q.nout++;
+                    }
+                if (q.nout > 0) jobs.push_back(q);
+            }
         Step<T> st;
         st.kind = ST_IIR;
         st.name = "iir";
@@ -517,6 +539,8 @@ template <typename T> struct Builder {
         st.P = P;
         st.coef = c;
         st.scratch_off = scratch_off;
+        st.iir_row = row_mode ? 1 : 0;
+        st.iir_real = real_in ? 1 : 0;
         // segment-parallel recursion: enough (column, job, segment) threads to fill the GPU
         const int L = H + 2 * P;
         const double threads = (double)W * jobs.size();
@@ -748,16 +772,13 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
         const int P = pad_radius(sm, sigma);
         int64_t scratch = 0;  // T elements, region after all complex regions (set by caller via ws_need)
         if (!col_only) {
-            const int64_t t_img = ws_aux, t_j = ws_aux + HW;
-            need = std::max(need, t_j + (int64_t)nj * HW);
-            b.tr(ST_TR_RC, img, R(SEL_WS, t_img), H, W);
             std::vector<IirJob<T>> ij;
             for (int j = 0; j < nj; ++j) {
                 IirJob<T> q{};
                 q.src_off = 0;
                 q.tabm_off = b.table(jobs[j].wc, -P, W + 2 * P);
                 q.tabr_off = q.tabm_off + P;
-                q.dst_off[0] = t_j + (int64_t)j * HW;
+                q.dst_off[0] = row_only ? jobs[j].out_direct : ws_j0 + (int64_t)j * HW;
                 q.pair[0] = 0;
                 q.conj[0] = 0;
                 q.nout = 1;
@@ -765,11 +786,8 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 q.sdft = 0;
                 ij.push_back(q);
             }
-            // transposed geometry: "rows" = x (W of them), "columns" = y (H)
-            b.iir_step(ij, R(SEL_WS, t_img), R(SEL_WS, 0), W, H, P, c, scratch, -1, true);
-            for (int j = 0; j < nj; ++j)
-                b.tr(ST_TR_CC, R(SEL_WS, t_j + (int64_t)j * HW),
-                     row_only ? R(out.sel, jobs[j].out_direct) : R(SEL_WS, ws_j0 + (int64_t)j * HW), W, H);
+            // lines = image rows (H of them), W samples each, straight from the image
+            b.iir_step(ij, img, row_only ? out : R(SEL_WS, 0), W, H, P, c, scratch, -1, true, true);
         }
         if (!row_only) {
             std::vector<IirJob<T>> ij;
@@ -1101,8 +1119,6 @@ static int32_t build_sdft_core(Builder<T>& b, const fgb_sdft_desc& d, const BinM
         FGB_TRY(iir_coeffs(sigma, cf));
         IirCoef c{cf[0], cf[1], cf[2], cf[3]};
         const int P = pad_radius(sm, sigma);
-        need = std::max(need, aux + HW + (int64_t)nh * HW);
-        b.tr(ST_TR_RC, img, R(SEL_WS, ws0 + aux), H, W);
         std::vector<IirJob<T>> ij;
         for (int i = 0; i < nh; ++i) {
             const double phi = w0x * bm.heads[i];
@@ -1110,15 +1126,14 @@ static int32_t build_sdft_core(Builder<T>& b, const fgb_sdft_desc& d, const BinM
             q.src_off = 0;
             q.tabm_off = b.table(phi, -P, W + 2 * P);
             q.tabr_off = b.table(phi, -cx, W);
-            q.dst_off[0] = aux + HW + (int64_t)i * HW;
+            q.dst_off[0] = (int64_t)i * HW;
             q.pair[0] = 1;
             q.nout = 1;
             q.need = 2;
             q.sdft = 1;
             ij.push_back(q);
         }
-        b.iir_step(ij, R(SEL_WS, ws0 + aux), R(SEL_WS, ws0 + 0), W, H, P, c, 0, -1, true);
-        for (int i = 0; i < nh; ++i) b.tr(ST_TR_CC, R(SEL_WS, ws0 + aux + HW + (int64_t)i * HW), R(SEL_WS, ws0 + (int64_t)i * HW), W, H);
+        b.iir_step(ij, img, R(SEL_WS, ws0 + 0), W, H, P, c, 0, -1, true, true);
         std::vector<IirJob<T>> cj;
         int cnt = 0;
         for (int i = 0; i < nh; ++i) {
@@ -1231,19 +1246,15 @@ static int32_t build_sdft_single(Plan<T>& p, const fgb_sdft_desc& d, int u, int 
         FGB_TRY(iir_coeffs(sigma, cf));
         IirCoef c{cf[0], cf[1], cf[2], cf[3]};
         const int P = pad_radius(sm, sigma);
-        const int64_t aux = need;
-        need = aux + 2 * HW;
-        b.tr(ST_TR_RC, R(SEL_IMG, 0), R(SEL_WS, aux), H, W);
         IirJob<T> q{};
         q.tabm_off = b.table(phx, -P, W + 2 * P);
         q.tabr_off = b.table(phx, -cx, W);
-        q.dst_off[0] = aux + HW;
+        q.dst_off[0] = jdst.off;
         q.pair[0] = 1;
         q.nout = 1;
         q.need = 2;
         q.sdft = 1;
-        b.iir_step({q}, R(SEL_WS, aux), R(SEL_WS, 0), W, H, P, c, 0);
-        b.tr(ST_TR_CC, R(SEL_WS, aux + HW), jdst, W, H);
+        b.iir_step({q}, R(SEL_IMG, 0), R(jdst.sel, 0), W, H, P, c, 0, -1, true, true);
     }
     if (!only_h) {
         const double phy = 2.0 * M_PI / d.my * v;
@@ -1441,26 +1452,40 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     IirArgs<T> a{};
                     a.jobs = p.d_ijobs() + st.job0;
                     a.tab_base = p.d_tabs();
-                    a.src_base = baseC(st.src);
+                    if (st.iir_real) {
+                        int64_t pitch = 0, bs = 0;
+                        a.src_base = baseT(st.src, &pitch, &bs);
+                        if (st.src.sel == SEL_WSR) pitch = st.H;
+                        a.src_bstride = bs;
+                        a.src_ls = st.iir_row ? pitch : 1;
+                        a.src_ss = st.iir_row ? 1 : pitch;
+                    } else {
+                        a.src_base = baseC(st.src);
+                        a.src_bstride = bsC(st.src);
+                        a.src_ls = st.iir_row ? st.H : 1;
+                        a.src_ss = st.iir_row ? 1 : st.W;
+                    }
                     a.dst_base = baseC(st.dst);
-                    a.src_bstride = bsC(st.src);
                     a.dst_bstride = bsC(st.dst);
+                    a.dst_ls = st.iir_row ? st.H : 1;
+                    a.dst_ss = st.iir_row ? 1 : st.W;
+                    a.real_in = st.iir_real;
                     a.scratch = scratch + st.lane * scratch_lane;
                     a.state = states + st.lane * state_lane;
-                    a.g = p.d_dbls() + st.g_off;
                     std::memcpy(a.Aseg, st.Aseg, sizeof(a.Aseg));
                     std::memcpy(a.Alast, st.Alast, sizeof(a.Alast));
                     a.nseg = st.nseg;
                     a.seglen = st.seglen;
                     a.c = st.coef;
-                    a.H = st.H;
-                    a.W = st.W;
+                    a.len = st.H;
+                    a.lines = st.W;
                     a.P = st.P;
                     a.njobs = st.njobs;
                     a.batch = nb;
                     if ((int64_t)iir_scratch_elems<T>(st.H, st.W, st.P, st.njobs, nb) > scratch_lane)
                         return fail(FGB_EINVAL, "internal: IIR scratch too small");
-                    FGB_CUDA(launch_iir_col<T>(a, s));
+                    a.g = p.d_dbls() + st.g_off;
+                    FGB_CUDA(launch_iir<T>(a, s));
                     break;
                 }
                 case ST_TR_RC: {

@@ -1,9 +1,9 @@
-// K4: recursive-Gaussian (RecursiveIIR) column stage, fp64 recursion state,
-// segment-parallel.
+// K4: recursive-Gaussian (RecursiveIIR) stage, fp64 recursion state,
+// segment-parallel, for both directions of the separable pipeline.
 //
 // Restates gaussian.py:215-228 (_iir_lines with assume_padded: the stage
 // already replicate-padded by P = ceil(5 sigma)+2, gaussian.py:211) inside
-// the modulate / smooth / recombine stage of gabor.py:135-164 and
+// the modulate / smooth / recombine stages of gabor.py:107-164 and
 // sdft.py:75-131:
 //   forward : y[n] = B z[n] - a1 y[n-1] - a2 y[n-2] - a3 y[n-3],
 //             y[-1] = y[-2] = y[-3] = z[0]  (lfilter_zi * x[0] steady state)
@@ -12,9 +12,16 @@
 // The recursion runs in fp64 (an fp32 recursion misses 1e-5 by up to 125x
 // at sigma = 32).
 //
-// Parallelisation is EXACT (no warm-up approximation): each column is cut
-// into NS segments.  A segment runs its recursion from a zero state; with
-// the companion matrix A = [[-a1,-a2,-a3],[1,0,0],[0,1,0]] the true output is
+// A "line" is one independent recursion (an image column for the vertical
+// stage, an image row for the horizontal stage); lines are adjacent threads
+// and the source / destination are addressed through (line, sample) strides,
+// so the horizontal stage reads the image rows and writes J in place -- no
+// transposes.  Scratch is [z][plane][sample][line] (lines contiguous) in
+// both modes.
+//
+// Parallelisation is EXACT (no warm-up approximation): each line is cut into
+// NS segments.  A segment runs its recursion from a zero state; with the
+// companion matrix A = [[-a1,-a2,-a3],[1,0,0],[0,1,0]] the true output is
 //     y[a+m] = y_loc[a+m] + g_m . s_in,   g_m = first row of A^(m+1),
 // where s_in is the true 3-sample state entering the segment, and the states
 // chain as s_out = s_loc_end + A^len s_in (a 3x3 scan over segments).  The
@@ -22,6 +29,8 @@
 //   fwd  : modulate, local forward recursion -> y_loc (storage type), end states
 //   bwd  : carry-in, correct y, local backward recursion -> u_loc, start states
 //   out  : carry-in, correct u, recombine -> outputs
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -29,8 +38,10 @@ namespace fgb {
 
 namespace {
 
-constexpr int kIirTX = 32;
-constexpr int kIirU = 3;  // samples per load batch
+constexpr int kIirTX = 32;  // lines per block (one warp)
+constexpr int kIirSY = 4;   // segments per block
+constexpr int kIirU = 3;    // samples per load batch
+
 
 __device__ __forceinline__ void mat3_apply(const double* A, const double* s, double* o) {
     o[0] = A[0] * s[0] + A[1] * s[1] + A[2] * s[2];
@@ -38,237 +49,258 @@ __device__ __forceinline__ void mat3_apply(const double* A, const double* s, dou
     o[2] = A[6] * s[0] + A[7] * s[1] + A[8] * s[2];
 }
 
-template <typename T>
-__device__ __forceinline__ void modulate(const IirJob<T>& job, cx_t<T> v, double2 cs, double* z) {
-    const double jr = v.x, ji = v.y;
-    z[0] = jr * cs.x + ji * cs.y;  // pair 0
-    z[1] = jr * cs.y - ji * cs.x;
-    z[2] = jr * cs.x - ji * cs.y;  // pair 1
-    z[3] = jr * cs.y + ji * cs.x;
+// one recursion step on a (y[n-1], y[n-2], y[n-3]) state; returns y[n]
+__device__ __forceinline__ double rec_step(double* p, double zin, const IirCoef& c) {
+    const double t = fma(c.B, zin, -(c.a2 * p[1] + c.a3 * p[2]));
+    const double y = fma(-c.a1, p[0], t);
+    p[2] = p[1];
+    p[1] = p[0];
+    p[0] = y;
+    return y;
 }
 
-__device__ __forceinline__ bool plane_used(int need, int q) { return (need >> (q >> 1)) & 1; }
+
+template <typename T, bool REAL> struct SrcT;
+template <typename T> struct SrcT<T, true> { using type = T; };
+template <typename T> struct SrcT<T, false> { using type = cx_t<T>; };
+
+__device__ __forceinline__ double2 ld_d2(const float* p) { return make_double2((double)*p, 0.0); }
+__device__ __forceinline__ double2 ld_d2(const double* p) { return make_double2(*p, 0.0); }
+__device__ __forceinline__ double2 ld_d2(const float2* p) { const float2 v = *p; return make_double2(v.x, v.y); }
+__device__ __forceinline__ double2 ld_d2(const double2* p) { return *p; }
+
+// Every job is ONE modulation pair (two real planes a, b); the host splits a
+// Gabor theta / pi - theta job into its two pairs, so a thread carries 2 x 3
+// fp64 states and the kernels stay at a high occupancy.
+__device__ __forceinline__ void modulate_pair(int pair, double jr, double ji, double2 cs, double& za, double& zb) {
+    if (pair == 0) {
+        za = fma(jr, cs.x, ji * cs.y);
+        zb = fma(jr, cs.y, -ji * cs.x);
+    } else {
+        za = fma(jr, cs.x, -ji * cs.y);
+        zb = fma(jr, cs.y, ji * cs.x);
+    }
+}
 
 // ---- pass 1: modulate + zero-state forward recursion per segment ----
-template <typename T>
-__global__ void __launch_bounds__(128) iir_fwd(IirArgs<T> a) {
+template <typename T, bool REAL>
+__global__ void __launch_bounds__(128) iir_fwd(const IirArgs<T> a) {
+    using S = typename SrcT<T, REAL>::type;
     const int x = blockIdx.x * kIirTX + threadIdx.x;
-    const int seg = blockIdx.y * blockDim.y + threadIdx.y;
+    const int seg = blockIdx.y * kIirSY + threadIdx.y;
     const int jb = blockIdx.z % a.njobs;
     const int b = blockIdx.z / a.njobs;
-    if (x >= a.W || seg >= a.nseg) return;
+    if (x >= a.lines || seg >= a.nseg) return;
     const IirJob<T>& job = a.jobs[jb];
-    const int H = a.H, W = a.W, P = a.P, L = H + 2 * P;
+    const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
     const int n0 = seg * a.seglen, n1 = min(L, n0 + a.seglen);
-    const cx_t<T>* src = a.src_base + job.src_off + (size_t)b * a.src_bstride + x;
+    const S* src = reinterpret_cast<const S*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride +
+                   (int64_t)x * a.src_ls;
+    const int64_t ss = a.src_ss;
     const double2* tabm = a.tab_base + job.tabm_off;
-    T* sc = a.scratch + (size_t)blockIdx.z * 4 * L * W + x;
-    const size_t plane = (size_t)L * W;
-    const double B = a.c.B, a1 = a.c.a1, a2 = a.c.a2, a3 = a.c.a3;
-    const int need = job.need;
-    double p[4][3];
-    double z[4];
+    const int64_t plane = (int64_t)L * NL;
+    T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
+    const IirCoef c = a.c;
+    const int pair = job.need >> 1;
+    double pa[3], pb[3];
     if (seg == 0) {  // the reference's steady-state init on the first padded sample
-        modulate<T>(job, src[0], tabm[0], z);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) p[q][0] = p[q][1] = p[q][2] = z[q];
+        const double2 v = ld_d2(src);
+        double za, zb;
+        modulate_pair(pair, v.x, v.y, tabm[0], za, zb);
+        pa[0] = pa[1] = pa[2] = za;
+        pb[0] = pb[1] = pb[2] = zb;
     } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) p[q][0] = p[q][1] = p[q][2] = 0.0;
+        pa[0] = pa[1] = pa[2] = pb[0] = pb[1] = pb[2] = 0.0;
     }
     // kIirU input samples are loaded before the dependent recursion consumes
-    // them (the stores into scratch would otherwise keep the compiler from
+    // them (the scratch stores would otherwise keep the compiler from
     // hoisting the next loads: one load in flight per thread)
     for (int nb = n0; nb < n1; nb += kIirU) {
-        cx_t<T> v[kIirU];
+        double2 v[kIirU];
 #pragma unroll
         for (int u = 0; u < kIirU; ++u)
-            if (nb + u < n1) v[u] = src[(size_t)clampi(nb + u - P, 0, H - 1) * W];
+            if (nb + u < n1) v[u] = ld_d2(src + clampi(nb + u - P, 0, len - 1) * ss);
 #pragma unroll
         for (int u = 0; u < kIirU; ++u) {
             const int n = nb + u;
             if (n >= n1) break;
-            modulate<T>(job, v[u], tabm[n], z);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (!plane_used(need, q)) continue;
-                const double t = fma(B, z[q], -(a2 * p[q][1] + a3 * p[q][2]));
-                const double yv = fma(-a1, p[q][0], t);
-                p[q][2] = p[q][1];
-                p[q][1] = p[q][0];
-                p[q][0] = yv;
-                sc[q * plane + (size_t)n * W] = (T)yv;
-            }
+            double za, zb;
+            modulate_pair(pair, v[u].x, v[u].y, tabm[n], za, zb);
+            T* o = sc + (int64_t)n * NL;
+            o[0] = (T)rec_step(pa, za, c);
+            o[plane] = (T)rec_step(pb, zb, c);
         }
     }
     // local end state (y[end], y[end-1], y[end-2]) per plane
-    double* st = a.state + (((size_t)blockIdx.z * a.nseg + seg) * 12) * W + x;
+    double* st = a.state + (((int64_t)blockIdx.z * a.nseg + seg) * 6) * NL + x;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) st[(size_t)(q * 3 + k) * W] = p[q][k];
+    for (int k = 0; k < 3; ++k) {
+        st[(int64_t)k * NL] = pa[k];
+        st[(int64_t)(3 + k) * NL] = pb[k];
+    }
 }
 
 // ---- pass 2: forward carry + correction, zero-state backward recursion ----
 template <typename T>
-__global__ void __launch_bounds__(128) iir_bwd(IirArgs<T> a) {
+__global__ void __launch_bounds__(128) iir_bwd(const IirArgs<T> a) {
     const int x = blockIdx.x * kIirTX + threadIdx.x;
-    const int seg = blockIdx.y * blockDim.y + threadIdx.y;
-    const int jb = blockIdx.z % a.njobs;
-    if (x >= a.W || seg >= a.nseg) return;
-    const IirJob<T>& job = a.jobs[jb];
-    const int H = a.H, W = a.W, P = a.P, L = H + 2 * P;
+    const int seg = blockIdx.y * kIirSY + threadIdx.y;
+    if (x >= a.lines || seg >= a.nseg) return;
+    const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
     const int n0 = seg * a.seglen, n1 = min(L, n0 + a.seglen);
-    T* sc = a.scratch + (size_t)blockIdx.z * 4 * L * W + x;
-    const size_t plane = (size_t)L * W;
-    const double B = a.c.B, a1 = a.c.a1, a2 = a.c.a2, a3 = a.c.a3;
-    const int need = job.need;
-    double* st_all = a.state + ((size_t)blockIdx.z * a.nseg * 12) * W + x;
+    const int64_t plane = (int64_t)L * NL;
+    T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
+    const IirCoef c = a.c;
+    const double* st_all = a.state + ((int64_t)blockIdx.z * a.nseg * 6) * NL + x;
     // true state entering this segment: scan the local end states of segments < seg
-    double s_in[4][3];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) s_in[q][0] = s_in[q][1] = s_in[q][2] = 0.0;
+    double sa[3] = {0.0, 0.0, 0.0}, sb[3] = {0.0, 0.0, 0.0};
     for (int j = 0; j < seg; ++j) {
-        const double* sj = st_all + (size_t)j * 12 * W;
+        const double* sj = st_all + (int64_t)j * 6 * NL;
+        double oa[3], ob[3];
+        mat3_apply(a.Aseg, sa, oa);  // segments < last are full length
+        mat3_apply(a.Aseg, sb, ob);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            double o[3];
-            mat3_apply(a.Aseg, s_in[q], o);  // segments < last are full length
-#pragma unroll
-            for (int k = 0; k < 3; ++k) s_in[q][k] = o[k] + sj[(size_t)(q * 3 + k) * W];
+        for (int k = 0; k < 3; ++k) {
+            sa[k] = oa[k] + sj[(int64_t)k * NL];
+            sb[k] = ob[k] + sj[(int64_t)(3 + k) * NL];
         }
     }
+    const double* gt = a.g;
+    const bool first = seg == 0;
     // backward local recursion from the segment end, on the corrected forward output
-    double u[4][3];
+    double ua[3], ub[3];
     if (seg == a.nseg - 1) {  // u[L..L+2] = y[L-1] (true value)
-        const int m = n1 - 1 - n0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double yl = plane_used(need, q) ? (double)sc[q * plane + (size_t)(n1 - 1) * W] : 0.0;
-            const double* g = a.g + 3 * m;
-            const double yv = seg == 0 ? yl : yl + g[0] * s_in[q][0] + g[1] * s_in[q][1] + g[2] * s_in[q][2];
-            u[q][0] = u[q][1] = u[q][2] = yv;
-        }
+        const T* o = sc + (int64_t)(n1 - 1) * NL;
+        const double* g = gt + 3 * (n1 - 1 - n0);
+        const double ya = first ? (double)o[0] : (double)o[0] + g[0] * sa[0] + g[1] * sa[1] + g[2] * sa[2];
+        const double yb = first ? (double)o[plane] : (double)o[plane] + g[0] * sb[0] + g[1] * sb[1] + g[2] * sb[2];
+        ua[0] = ua[1] = ua[2] = ya;
+        ub[0] = ub[1] = ub[2] = yb;
     } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) u[q][0] = u[q][1] = u[q][2] = 0.0;
+        ua[0] = ua[1] = ua[2] = ub[0] = ub[1] = ub[2] = 0.0;
     }
     for (int nb = n1 - 1; nb >= n0; nb -= kIirU) {
-        T ys[kIirU][4];
+        T ya[kIirU], yb[kIirU];
 #pragma unroll
-        for (int u = 0; u < kIirU; ++u)
+        for (int k = 0; k < kIirU; ++k) {
+            const T* o = sc + (int64_t)(nb - k) * NL;
+            if (nb - k >= n0) { ya[k] = o[0]; yb[k] = o[plane]; }
+        }
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (nb - u >= n0 && plane_used(need, q)) ys[u][q] = sc[q * plane + (size_t)(nb - u) * W];
-#pragma unroll
-        for (int uu = 0; uu < kIirU; ++uu) {
-            const int n = nb - uu;
+        for (int k = 0; k < kIirU; ++k) {
+            const int n = nb - k;
             if (n < n0) break;
-            const double* g = a.g + 3 * (n - n0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (!plane_used(need, q)) continue;
-                const double yl = (double)ys[uu][q];
-                const double yv = seg == 0 ? yl : yl + g[0] * s_in[q][0] + g[1] * s_in[q][1] + g[2] * s_in[q][2];
-                const double t = fma(B, yv, -(a2 * u[q][1] + a3 * u[q][2]));
-                const double uv = fma(-a1, u[q][0], t);
-                u[q][2] = u[q][1];
-                u[q][1] = u[q][0];
-                u[q][0] = uv;
-                sc[q * plane + (size_t)n * W] = (T)uv;
+            T* o = sc + (int64_t)n * NL;
+            double va = ya[k], vb = yb[k];
+            if (!first) {
+                const double* g = gt + 3 * (n - n0);
+                const double g0 = g[0], g1 = g[1], g2 = g[2];
+                va += g0 * sa[0] + g1 * sa[1] + g2 * sa[2];
+                vb += g0 * sb[0] + g1 * sb[1] + g2 * sb[2];
             }
+            o[0] = (T)rec_step(ua, va, c);
+            o[plane] = (T)rec_step(ub, vb, c);
         }
     }
     // local start state (u[start], u[start+1], u[start+2]) -> the backward half of the state buffer
-    double* st = st_all + ((size_t)a.njobs * a.batch * a.nseg * 12) * W + (size_t)seg * 12 * W;
+    double* st = a.state + ((int64_t)a.njobs * a.batch * a.nseg * 6) * NL +
+                 (((int64_t)blockIdx.z * a.nseg + seg) * 6) * NL + x;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) st[(size_t)(q * 3 + k) * W] = u[q][k];
+    for (int k = 0; k < 3; ++k) {
+        st[(int64_t)k * NL] = ua[k];
+        st[(int64_t)(3 + k) * NL] = ub[k];
+    }
 }
 
 // ---- pass 3: backward carry + correction, recombination, outputs ----
 template <typename T>
-__global__ void __launch_bounds__(128) iir_out(IirArgs<T> a) {
+__global__ void __launch_bounds__(128) iir_out(const IirArgs<T> a) {
     const int x = blockIdx.x * kIirTX + threadIdx.x;
-    const int seg = blockIdx.y * blockDim.y + threadIdx.y;
+    const int seg = blockIdx.y * kIirSY + threadIdx.y;
     const int jb = blockIdx.z % a.njobs;
     const int b = blockIdx.z / a.njobs;
-    if (x >= a.W || seg >= a.nseg) return;
+    if (x >= a.lines || seg >= a.nseg) return;
     const IirJob<T>& job = a.jobs[jb];
-    const int H = a.H, W = a.W, P = a.P, L = H + 2 * P;
+    const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
     const int n0 = seg * a.seglen, n1 = min(L, n0 + a.seglen);
-    if (n1 <= P || n0 >= P + H) return;  // nothing of this segment survives the crop
-    T* sc = a.scratch + (size_t)blockIdx.z * 4 * L * W + x;
-    const size_t plane = (size_t)L * W;
-    const double* st_all = a.state + ((size_t)a.njobs * a.batch * a.nseg * 12) * W +
-                           ((size_t)blockIdx.z * a.nseg * 12) * W + x;
+    if (n1 <= P || n0 >= P + len) return;  // nothing of this segment survives the crop
+    const int64_t plane = (int64_t)L * NL;
+    const T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
+    const double* st_all = a.state + ((int64_t)a.njobs * a.batch * a.nseg * 6) * NL +
+                           ((int64_t)blockIdx.z * a.nseg * 6) * NL + x;
     // true state entering this segment from above: scan local start states of segments > seg
-    double t_in[4][3];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) t_in[q][0] = t_in[q][1] = t_in[q][2] = 0.0;
+    double ta[3] = {0.0, 0.0, 0.0}, tb[3] = {0.0, 0.0, 0.0};
     for (int j = a.nseg - 1; j > seg; --j) {
-        const double* sj = st_all + (size_t)j * 12 * W;
+        const double* sj = st_all + (int64_t)j * 6 * NL;
         const double* A = (j == a.nseg - 1) ? a.Alast : a.Aseg;
+        double oa[3], ob[3];
+        mat3_apply(A, ta, oa);
+        mat3_apply(A, tb, ob);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            double o[3];
-            mat3_apply(A, t_in[q], o);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) t_in[q][k] = o[k] + sj[(size_t)(q * 3 + k) * W];
+        for (int k = 0; k < 3; ++k) {
+            ta[k] = oa[k] + sj[(int64_t)k * NL];
+            tb[k] = ob[k] + sj[(int64_t)(3 + k) * NL];
         }
     }
     const bool last = seg == a.nseg - 1;
+    // outputs (all of this job's pair): pointers + conjugation flags in registers
+    const int nout = job.nout;
+    const double isg = job.sdft ? -1.0 : 1.0;  // Gabor im = s Sa - c Sb; SDFT im = c Sb - s Sa
+    cx_t<T>* dptr[4];
+    double osg[4];
+    const int64_t dss = a.dst_ss;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        dptr[o] = a.dst_base + (o < nout ? job.dst_off[o] : 0) + (int64_t)b * a.dst_bstride + (int64_t)x * a.dst_ls;
+        osg[o] = (o < nout && job.conj[o]) ? -isg : isg;
+    }
     const double2* tabr = a.tab_base + job.tabr_off;
-    const size_t ob = (size_t)b * a.dst_bstride + x;
-    const int lo = max(n0, P), hi = min(n1, P + H);
-    const int need = job.need;
+    const int lo = max(n0, P), hi = min(n1, P + len);
+    const double* gt = a.g;
     for (int nb = lo; nb < hi; nb += kIirU) {
-      T us[kIirU][4];
+        T ua[kIirU], ub[kIirU];
 #pragma unroll
-      for (int u = 0; u < kIirU; ++u)
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-              if (nb + u < hi && plane_used(need, q)) us[u][q] = sc[q * plane + (size_t)(nb + u) * W];
-#pragma unroll
-      for (int uu = 0; uu < kIirU; ++uu) {
-        const int n = nb + uu;
-        if (n >= hi) break;
-        const double* g = a.g + 3 * (n1 - 1 - n);
-        double sv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!plane_used(need, q)) { sv[q] = 0.0; continue; }
-            const double ul = (double)us[uu][q];
-            sv[q] = last ? ul : ul + g[0] * t_in[q][0] + g[1] * t_in[q][1] + g[2] * t_in[q][2];
+        for (int k = 0; k < kIirU; ++k) {
+            const T* o = sc + (int64_t)(nb + k) * NL;
+            if (nb + k < hi) { ua[k] = o[0]; ub[k] = o[plane]; }
         }
-        const int yo = n - P;
-        const double2 cs = tabr[yo];
-        for (int o = 0; o < job.nout; ++o) {
-            const int pr = job.pair[o];
-            const double sa = sv[2 * pr], sb = sv[2 * pr + 1];
-            double re = cs.x * sa + cs.y * sb;
-            double im = job.sdft ? (cs.x * sb - cs.y * sa) : (cs.y * sa - cs.x * sb);
-            if (job.conj[o]) im = -im;
-            a.dst_base[job.dst_off[o] + ob + (size_t)yo * W] = mk<T>((T)re, (T)im);
+#pragma unroll
+        for (int k = 0; k < kIirU; ++k) {
+            const int n = nb + k;
+            if (n >= hi) break;
+            const int yo = n - P;
+            const double2 cs = tabr[yo];
+            double va = ua[k], vb = ub[k];
+            if (!last) {
+                const double* g = gt + 3 * (n1 - 1 - n);
+                const double g0 = g[0], g1 = g[1], g2 = g[2];
+                va += g0 * ta[0] + g1 * ta[1] + g2 * ta[2];
+                vb += g0 * tb[0] + g1 * tb[1] + g2 * tb[2];
+            }
+            const T re = (T)fma(cs.x, va, cs.y * vb);
+            const double im = fma(cs.y, va, -cs.x * vb);
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                if (o >= nout) break;
+                dptr[o][(int64_t)yo * dss] = mk<T>(re, (T)(osg[o] * im));
+            }
         }
-      }
     }
 }
 
 }  // namespace
 
-template <typename T> size_t iir_scratch_elems(int H, int W, int P, int njobs, int batch) {
-    return (size_t)njobs * batch * 4 * (size_t)(H + 2 * P) * W;
+template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch) {
+    return (size_t)njobs * batch * 2 * (size_t)(len + 2 * P) * lines;
 }
 
-size_t iir_state_doubles(int W, int nseg, int njobs, int batch) { return 2 * (size_t)njobs * batch * nseg * 12 * W; }
+size_t iir_state_doubles(int lines, int nseg, int njobs, int batch) { return 2 * (size_t)njobs * batch * nseg * 6 * lines; }
 
-template <typename T> cudaError_t launch_iir_col(const IirArgs<T>& a, cudaStream_t s) {
-    const int SY = 4;  // segments per block (blockDim.y)
-    dim3 block(kIirTX, SY);
-    dim3 grid((a.W + kIirTX - 1) / kIirTX, (a.nseg + SY - 1) / SY, a.njobs * a.batch);
-    iir_fwd<T><<<grid, block, 0, s>>>(a);
+template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s) {
+    dim3 block(kIirTX, kIirSY);
+    dim3 grid((a.lines + kIirTX - 1) / kIirTX, (a.nseg + kIirSY - 1) / kIirSY, a.njobs * a.batch);
+    if (a.real_in) iir_fwd<T, true><<<grid, block, 0, s>>>(a);
+    else iir_fwd<T, false><<<grid, block, 0, s>>>(a);
     iir_bwd<T><<<grid, block, 0, s>>>(a);
     iir_out<T><<<grid, block, 0, s>>>(a);
     return cudaGetLastError();
@@ -276,7 +308,7 @@ template <typename T> cudaError_t launch_iir_col(const IirArgs<T>& a, cudaStream
 
 template size_t iir_scratch_elems<float>(int, int, int, int, int);
 template size_t iir_scratch_elems<double>(int, int, int, int, int);
-template cudaError_t launch_iir_col<float>(const IirArgs<float>&, cudaStream_t);
-template cudaError_t launch_iir_col<double>(const IirArgs<double>&, cudaStream_t);
+template cudaError_t launch_iir<float>(const IirArgs<float>&, cudaStream_t);
+template cudaError_t launch_iir<double>(const IirArgs<double>&, cudaStream_t);
 
 }  // namespace fgb

@@ -106,29 +106,32 @@ template <typename T> struct IirJob {
     int8_t pair[4];
     int8_t conj[4];
     int32_t nout;
-    int32_t need;            // bit 0: pair 0 used, bit 1: pair 1 used
+    int32_t need;            // bit 0: pair 0 used, bit 1: pair 1 used (kernel jobs: exactly one)
     int32_t sdft;
     int32_t pad_;
 };
 template <typename T> struct IirArgs {
     const IirJob<T>* jobs;
     const double2* tab_base;
-    const cx_t<T>* src_base;
+    const void* src_base;    // T (real_in) or cx_t<T> elements
     cx_t<T>* dst_base;
-    T* scratch;              // [njobs*batch][4][H+2P][W] local forward / backward sequences
-    double* state;           // [2][njobs*batch][nseg][4 planes][3][W] segment boundary states
+    T* scratch;              // [njobs*batch][2][len+2P][lines] local forward / backward sequences
+    double* state;           // [2][njobs*batch][nseg][2 planes][3][lines] segment boundary states
     const double* g;         // [seglen][3]: first row of A^(m+1)
     double Aseg[9];          // A^seglen
     double Alast[9];         // A^(length of the last segment)
-    int64_t src_bstride, dst_bstride;
+    int64_t src_bstride, dst_bstride;  // per image, in source / complex elements
+    int64_t src_ls, src_ss;  // source element strides per line / per sample
+    int64_t dst_ls, dst_ss;  // destination strides per line / per sample
     IirCoef c;
-    int H, W, P;
+    int len, lines, P;       // samples per line (unpadded), independent lines, pad
     int njobs, batch;
     int nseg, seglen;
+    int real_in;
 };
-template <typename T> cudaError_t launch_iir_col(const IirArgs<T>& a, cudaStream_t s);
-template <typename T> size_t iir_scratch_elems(int H, int W, int P, int njobs, int batch);
-size_t iir_state_doubles(int W, int nseg, int njobs, int batch);
+template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s);
+template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch);
+size_t iir_state_doubles(int lines, int nseg, int njobs, int batch);
 
 // ---- brute-force 2-D references (bruteforce.cu) ---------------------------
 template <typename T> struct Direct2DArgs {
