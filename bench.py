@@ -389,9 +389,25 @@ def run_ours(args, cfg, rank, world, local_rank):
         for _ in range(ne):
             N.check(call(C.byref(desc), C.c_void_p(hin.data_ptr()), C.c_void_p(hout.data_ptr())))
         e2e_s = (time.perf_counter() - t0) / ne
+        # the PCIe link itself: the same H2D + D2H bytes as plain pinned copies
+        # (no compute), so e2e can be read as a fraction of what the link moves
+        dev_in = torch.empty(hin.shape, dtype=hin.dtype, device=dev)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(ne):
+            dev_in.copy_(hin, non_blocking=True)
+            hout.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+        link_s = (time.perf_counter() - t1) / ne
+        del dev_in
+        nbytes = int(hin.numel() * hin.element_size()) + int(hout.numel() * hout.element_size())
         e2e = {"value": units_step * world / e2e_s if world == 1 else None, "unit": unit_name(cfg),
                "h2d_bytes_per_step": int(hin.numel() * hin.element_size()),
-               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()), "ms_per_step": e2e_s * 1e3}
+               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()), "ms_per_step": e2e_s * 1e3,
+               "link_copy_ms": link_s * 1e3, "link_gbs": nbytes / link_s / 1e9,
+               "frac_of_link": link_s / e2e_s,
+               "note": "host buffers through fgb_*_host (H2D, compute, D2H per step); link_copy_ms = the same "
+                       "bytes as bare pinned copies, so frac_of_link ~ 1 means the step is PCIe-bound"}
         if world > 1:
             et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(et, op=dist.ReduceOp.MAX)

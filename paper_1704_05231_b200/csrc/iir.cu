@@ -25,10 +25,12 @@
 //     y[a+m] = y_loc[a+m] + g_m . s_in,   g_m = first row of A^(m+1),
 // where s_in is the true 3-sample state entering the segment, and the states
 // chain as s_out = s_loc_end + A^len s_in (a 3x3 scan over segments).  The
-// backward pass is the same recursion on reversed indices.  Three kernels:
-//   fwd  : modulate, local forward recursion -> y_loc (storage type), end states
-//   bwd  : carry-in, correct y, local backward recursion -> u_loc, start states
-//   out  : carry-in, correct u, recombine -> outputs
+// backward pass is the same recursion on reversed indices.  Five kernels:
+//   fwd    : modulate, local forward recursion -> y_loc (storage type), end states
+//   scan<0>: end states -> carry-ins (grouped affine scan over segments)
+//   bwd    : correct y, local backward recursion -> u_loc, start states
+//   scan<1>: start states -> carry-ins from above
+//   out    : correct u, recombine -> outputs
 #include <cstring>
 
 #include "common.cuh"
@@ -41,6 +43,10 @@ namespace {
 constexpr int kIirTX = 32;  // lines per block (one warp)
 constexpr int kIirSY = 4;   // segments per block
 constexpr int kIirU = 3;    // samples per load batch
+
+struct IirScanMats {
+    double Aseg[9], Alast[9];
+};
 
 
 __device__ __forceinline__ void mat3_apply(const double* A, const double* s, double* o) {
@@ -152,17 +158,14 @@ __global__ void __launch_bounds__(128) iir_bwd(const IirArgs<T> a) {
     T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
     const IirCoef c = a.c;
     const double* st_all = a.state + ((int64_t)blockIdx.z * a.nseg * 6) * NL + x;
-    // true state entering this segment: scan the local end states of segments < seg
-    double sa[3] = {0.0, 0.0, 0.0}, sb[3] = {0.0, 0.0, 0.0};
-    for (int j = 0; j < seg; ++j) {
-        const double* sj = st_all + (int64_t)j * 6 * NL;
-        double oa[3], ob[3];
-        mat3_apply(a.Aseg, sa, oa);  // segments < last are full length
-        mat3_apply(a.Aseg, sb, ob);
+    // true state entering this segment (iir_scan<0> turned the local end states into carry-ins)
+    double sa[3], sb[3];
+    {
+        const double* sj = st_all + (int64_t)seg * 6 * NL;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            sa[k] = oa[k] + sj[(int64_t)k * NL];
-            sb[k] = ob[k] + sj[(int64_t)(3 + k) * NL];
+            sa[k] = sj[(int64_t)k * NL];
+            sb[k] = sj[(int64_t)(3 + k) * NL];
         }
     }
     const double* gt = a.g;
@@ -228,18 +231,14 @@ __global__ void __launch_bounds__(128) iir_out(const IirArgs<T> a) {
     const T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
     const double* st_all = a.state + ((int64_t)a.njobs * a.batch * a.nseg * 6) * NL +
                            ((int64_t)blockIdx.z * a.nseg * 6) * NL + x;
-    // true state entering this segment from above: scan local start states of segments > seg
-    double ta[3] = {0.0, 0.0, 0.0}, tb[3] = {0.0, 0.0, 0.0};
-    for (int j = a.nseg - 1; j > seg; --j) {
-        const double* sj = st_all + (int64_t)j * 6 * NL;
-        const double* A = (j == a.nseg - 1) ? a.Alast : a.Aseg;
-        double oa[3], ob[3];
-        mat3_apply(A, ta, oa);
-        mat3_apply(A, tb, ob);
+    // true state entering this segment from above (iir_scan<1> turned the local start states into carry-ins)
+    double ta[3], tb[3];
+    {
+        const double* sj = st_all + (int64_t)seg * 6 * NL;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            ta[k] = oa[k] + sj[(int64_t)k * NL];
-            tb[k] = ob[k] + sj[(int64_t)(3 + k) * NL];
+            ta[k] = sj[(int64_t)k * NL];
+            tb[k] = sj[(int64_t)(3 + k) * NL];
         }
     }
     const bool last = seg == a.nseg - 1;
@@ -288,6 +287,90 @@ __global__ void __launch_bounds__(128) iir_out(const IirArgs<T> a) {
     }
 }
 
+// ---- carry scans: local segment states -> true incoming states, in place ----
+// DIR 0 (after iir_fwd): s_in[0] = 0, s_in[j+1] = Aseg s_in[j] + end_loc[j]
+// DIR 1 (after iir_bwd): t_in[n-1] = 0, t_in[j-1] = A_j t_in[j] + start_loc[j]
+//                        (A_j = Alast for the shorter last segment)
+// Block = 32 lines x kScanG segment groups.  Each group folds its run of
+// segments into one affine map (P_g, v_g), the groups are chained through
+// shared memory, then each group re-walks its run writing the carry-ins.
+constexpr int kScanG = 8;
+
+__device__ __forceinline__ void mat3_mul(const double* X, const double* Y, double* Z) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Z[3 * i + j] = X[3 * i] * Y[j] + X[3 * i + 1] * Y[3 + j] + X[3 * i + 2] * Y[6 + j];
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(32 * kScanG) iir_scan(double* state, int64_t sec_off, int lines, int nseg,
+                                                       const __grid_constant__ IirScanMats m) {
+    __shared__ double sP[kScanG][9];
+    __shared__ double sv[kScanG][6][32];
+    const int lane = threadIdx.x, grp = threadIdx.y;
+    const int x = blockIdx.x * 32 + lane;
+    const int NL = lines, ns = nseg;
+    const int k = (ns + kScanG - 1) / kScanG;
+    const int r0 = grp * k, r1 = min(ns, r0 + k);
+    const bool live = x < lines;
+    double* st = state + sec_off + ((int64_t)blockIdx.z * ns * 6) * NL + (live ? x : 0);
+    auto seg_of = [&](int r) { return DIR == 0 ? r : ns - 1 - r; };
+    auto mat_of = [&](int j) -> const double* { return (DIR == 1 && j == ns - 1) ? m.Alast : m.Aseg; };
+    // 1) fold the group's run: v = M_j v + l_j, P = M_j P
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    double P[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    for (int r = r0; r < r1; ++r) {
+        const int j = seg_of(r);
+        const double* M = mat_of(j);
+        const double* sj = st + (int64_t)j * 6 * NL;
+        double l[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) l[q] = live ? sj[(int64_t)q * NL] : 0.0;
+        double o[6];
+        mat3_apply(M, v, o);
+        mat3_apply(M, v + 3, o + 3);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v[q] = o[q] + l[q];
+        double Q[9];
+        mat3_mul(M, P, Q);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) P[q] = Q[q];
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 9; ++q) sP[grp][q] = P[q];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sv[grp][q][lane] = v[q];
+    __syncthreads();
+    // 2) incoming state of this group: X_0 = 0, X_{g+1} = P_g X_g + v_g
+    double X[6] = {0, 0, 0, 0, 0, 0};
+    for (int g = 0; g < grp; ++g) {
+        double o[6];
+        mat3_apply(sP[g], X, o);
+        mat3_apply(sP[g], X + 3, o + 3);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) X[q] = o[q] + sv[g][q][lane];
+    }
+    // 3) re-walk: write the carry-in of each segment, then step past it
+    if (!live) return;
+    for (int r = r0; r < r1; ++r) {
+        const int j = seg_of(r);
+        const double* M = mat_of(j);
+        double* sj = st + (int64_t)j * 6 * NL;
+        double l[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) l[q] = sj[(int64_t)q * NL];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) sj[(int64_t)q * NL] = X[q];
+        double o[6];
+        mat3_apply(M, X, o);
+        mat3_apply(M, X + 3, o + 3);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) X[q] = o[q] + l[q];
+    }
+}
+
 }  // namespace
 
 template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch) {
@@ -299,9 +382,16 @@ size_t iir_state_doubles(int lines, int nseg, int njobs, int batch) { return 2 *
 template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s) {
     dim3 block(kIirTX, kIirSY);
     dim3 grid((a.lines + kIirTX - 1) / kIirTX, (a.nseg + kIirSY - 1) / kIirSY, a.njobs * a.batch);
+    IirScanMats m;
+    std::memcpy(m.Aseg, a.Aseg, sizeof(m.Aseg));
+    std::memcpy(m.Alast, a.Alast, sizeof(m.Alast));
+    const dim3 sgrid((a.lines + 31) / 32, 1, a.njobs * a.batch), sblock(32, kScanG);
+    const int64_t bwd_sec = (int64_t)a.njobs * a.batch * a.nseg * 6 * a.lines;
     if (a.real_in) iir_fwd<T, true><<<grid, block, 0, s>>>(a);
     else iir_fwd<T, false><<<grid, block, 0, s>>>(a);
+    iir_scan<0><<<sgrid, sblock, 0, s>>>(a.state, 0, a.lines, a.nseg, m);
     iir_bwd<T><<<grid, block, 0, s>>>(a);
+    iir_scan<1><<<sgrid, sblock, 0, s>>>(a.state, bwd_sec, a.lines, a.nseg, m);
     iir_out<T><<<grid, block, 0, s>>>(a);
     return cudaGetLastError();
 }
