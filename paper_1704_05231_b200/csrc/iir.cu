@@ -42,7 +42,8 @@ namespace {
 
 constexpr int kIirTX = 32;  // lines per block (one warp)
 constexpr int kIirSY = 4;   // segments per block
-constexpr int kIirU = 3;    // samples per load batch
+constexpr int kIirU = 3;    // samples per load batch (forward pass)
+constexpr int kIirUB = 3;   // scratch samples per load batch (backward / output passes)
 
 struct IirScanMats {
     double Aseg[9], Alast[9];
@@ -182,15 +183,15 @@ __global__ void __launch_bounds__(128) iir_bwd(const IirArgs<T> a) {
     } else {
         ua[0] = ua[1] = ua[2] = ub[0] = ub[1] = ub[2] = 0.0;
     }
-    for (int nb = n1 - 1; nb >= n0; nb -= kIirU) {
-        T ya[kIirU], yb[kIirU];
+    for (int nb = n1 - 1; nb >= n0; nb -= kIirUB) {
+        T ya[kIirUB], yb[kIirUB];
 #pragma unroll
-        for (int k = 0; k < kIirU; ++k) {
+        for (int k = 0; k < kIirUB; ++k) {
             const T* o = sc + (int64_t)(nb - k) * NL;
             if (nb - k >= n0) { ya[k] = o[0]; yb[k] = o[plane]; }
         }
 #pragma unroll
-        for (int k = 0; k < kIirU; ++k) {
+        for (int k = 0; k < kIirUB; ++k) {
             const int n = nb - k;
             if (n < n0) break;
             T* o = sc + (int64_t)n * NL;
@@ -256,15 +257,15 @@ __global__ void __launch_bounds__(128) iir_out(const IirArgs<T> a) {
     const double2* tabr = a.tab_base + job.tabr_off;
     const int lo = max(n0, P), hi = min(n1, P + len);
     const double* gt = a.g;
-    for (int nb = lo; nb < hi; nb += kIirU) {
-        T ua[kIirU], ub[kIirU];
+    for (int nb = lo; nb < hi; nb += kIirUB) {
+        T ua[kIirUB], ub[kIirUB];
 #pragma unroll
-        for (int k = 0; k < kIirU; ++k) {
+        for (int k = 0; k < kIirUB; ++k) {
             const T* o = sc + (int64_t)(nb + k) * NL;
             if (nb + k < hi) { ua[k] = o[0]; ub[k] = o[plane]; }
         }
 #pragma unroll
-        for (int k = 0; k < kIirU; ++k) {
+        for (int k = 0; k < kIirUB; ++k) {
             const int n = nb + k;
             if (n >= hi) break;
             const int yo = n - P;
@@ -294,7 +295,8 @@ __global__ void __launch_bounds__(128) iir_out(const IirArgs<T> a) {
 // Block = 32 lines x kScanG segment groups.  Each group folds its run of
 // segments into one affine map (P_g, v_g), the groups are chained through
 // shared memory, then each group re-walks its run writing the carry-ins.
-constexpr int kScanG = 8;
+constexpr int kScanG = 16;  // segment groups per CTA
+constexpr int kScanKC = 4;  // register-cached segments per group
 
 __device__ __forceinline__ void mat3_mul(const double* X, const double* Y, double* Z) {
 #pragma unroll
@@ -317,25 +319,48 @@ __global__ void __launch_bounds__(32 * kScanG) iir_scan(double* state, int64_t s
     double* st = state + sec_off + ((int64_t)blockIdx.z * ns * 6) * NL + (live ? x : 0);
     auto seg_of = [&](int r) { return DIR == 0 ? r : ns - 1 - r; };
     auto mat_of = [&](int j) -> const double* { return (DIR == 1 && j == ns - 1) ? m.Alast : m.Aseg; };
-    // 1) fold the group's run: v = M_j v + l_j, P = M_j P
-    double v[6] = {0, 0, 0, 0, 0, 0};
-    double P[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-    for (int r = r0; r < r1; ++r) {
-        const int j = seg_of(r);
-        const double* M = mat_of(j);
-        const double* sj = st + (int64_t)j * 6 * NL;
-        double l[6];
+    auto load = [&](int r, double* l) {
+        const double* sj = st + (int64_t)seg_of(r) * 6 * NL;
 #pragma unroll
         for (int q = 0; q < 6; ++q) l[q] = live ? sj[(int64_t)q * NL] : 0.0;
+    };
+    auto step = [&](int r, double* v, const double* l) {  // v = M_j v + l
+        const double* M = mat_of(seg_of(r));
         double o[6];
         mat3_apply(M, v, o);
         mat3_apply(M, v + 3, o + 3);
 #pragma unroll
         for (int q = 0; q < 6; ++q) v[q] = o[q] + l[q];
+    };
+    // runs of up to kScanKC segments keep their states in registers: one load
+    // round trip per thread instead of one per segment and pass
+    const bool cached = r1 - r0 <= kScanKC;
+    double lc[kScanKC][6];
+    if (cached) {
+#pragma unroll
+        for (int i = 0; i < kScanKC; ++i)
+            if (r0 + i < r1) load(r0 + i, lc[i]);
+    }
+    // 1) fold the group's run: v = M_j v + l_j, P = M_j P
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    double P[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    auto fold_P = [&](int r) {
         double Q[9];
-        mat3_mul(M, P, Q);
+        mat3_mul(mat_of(seg_of(r)), P, Q);
 #pragma unroll
         for (int q = 0; q < 9; ++q) P[q] = Q[q];
+    };
+    if (cached) {
+#pragma unroll
+        for (int i = 0; i < kScanKC; ++i)
+            if (r0 + i < r1) { step(r0 + i, v, lc[i]); fold_P(r0 + i); }
+    } else {
+        for (int r = r0; r < r1; ++r) {
+            double l[6];
+            load(r, l);
+            step(r, v, l);
+            fold_P(r);
+        }
     }
     if (lane == 0)
 #pragma unroll
@@ -354,20 +379,22 @@ __global__ void __launch_bounds__(32 * kScanG) iir_scan(double* state, int64_t s
     }
     // 3) re-walk: write the carry-in of each segment, then step past it
     if (!live) return;
-    for (int r = r0; r < r1; ++r) {
-        const int j = seg_of(r);
-        const double* M = mat_of(j);
-        double* sj = st + (int64_t)j * 6 * NL;
-        double l[6];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) l[q] = sj[(int64_t)q * NL];
+    auto store = [&](int r) {
+        double* sj = st + (int64_t)seg_of(r) * 6 * NL;
 #pragma unroll
         for (int q = 0; q < 6; ++q) sj[(int64_t)q * NL] = X[q];
-        double o[6];
-        mat3_apply(M, X, o);
-        mat3_apply(M, X + 3, o + 3);
+    };
+    if (cached) {
 #pragma unroll
-        for (int q = 0; q < 6; ++q) X[q] = o[q] + l[q];
+        for (int i = 0; i < kScanKC; ++i)
+            if (r0 + i < r1) { store(r0 + i); step(r0 + i, X, lc[i]); }
+    } else {
+        for (int r = r0; r < r1; ++r) {
+            double l[6];
+            load(r, l);  // read before this thread overwrites the slot
+            store(r);
+            step(r, X, l);
+        }
     }
 }
 
