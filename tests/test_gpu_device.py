@@ -162,3 +162,35 @@ def test_outputs_fully_written_within_bounds(env, kn, shape):
             ref = O.compute_bank(f64, spec.frequencies, 8, spec.sigmas, ok)
             err = max(max_rel_err((o[bi, e].real, o[bi, e].imag), r[3:]) for e, r in enumerate(ref))
         assert err <= 1e-5
+
+
+def test_randomized_sweep_f64(env):
+    """Seeded random shapes / orientation counts / sigmas / smoothers / windows
+    (incl. 1-pixel extents, N = 1..9, odd windows, sigma below one pixel) through
+    the drop-in API in the fp64 build vs the oracle at 1e-10."""
+    torch, fg, D, P = env
+    rng = np.random.default_rng(2024)
+    kinds = [(fg.ExactFIR(3.0), ("fir", 3.0)), (fg.ExactFIR(), ("fir", 6.0)), (fg.RecursiveIIR(), ("iir",))]
+    for case in range(16):
+        h, w = int(rng.integers(1, 90)), int(rng.integers(1, 90))
+        f = rng.uniform(0.0, 1.0, size=(h, w))
+        k, ok = kinds[case % 3]
+        nf = int(rng.integers(1, 3))
+        freqs = tuple(float(x) for x in rng.uniform(0.2, 2.5, size=nf))
+        sig = tuple(float(x) for x in rng.uniform(0.6, 5.0, size=nf))
+        n = int(rng.integers(1, 10))
+        out = fg.compute_bank(fg.RealImage.from_array(f), fg.BankSpec(freqs, n, sig), k, fg.OpCounters(),
+                              precision="f64")
+        ref = O.compute_bank(f, freqs, n, sig, ok)
+        for e, ((p, img), r) in enumerate(zip(out.entries, ref)):
+            assert max_rel_err(img, r[3:]) <= 1e-10, (case, h, w, n, e)
+        mx, my = int(rng.integers(1, 10)), int(rng.integers(1, 10))
+        if case % 4 == 3:
+            spec, sk = fg.SdftSpec(mx, my, fg.Box(1)), ("box", 1)
+        else:
+            spec, sk = fg.SdftSpec(mx, my, k, float(rng.uniform(0.6, 3.0))), ok
+        sd = fg.sdft_full(fg.RealImage.from_array(f), spec, fg.OpCounters(), precision="f64")
+        sref = O.sdft_full(f, mx, my, sk, spec.sigma)
+        for u in range(mx):
+            for v in range(my):
+                assert max_rel_err(sd.bins[u][v], sref[u][v]) <= 1e-10, (case, h, w, mx, my, u, v)
