@@ -544,7 +544,8 @@ template <typename T> struct Builder {
         // segment-parallel recursion: enough (column, job, segment) threads to fill the GPU
         const int L = H + 2 * P;
         const double threads = (double)W * jobs.size();
-        int nseg = (int)std::ceil(148.0 * 1536.0 / std::max(1.0, threads));
+        static const double iir_threads = std::getenv("FGB_IIR_THREADS") ? std::atof(std::getenv("FGB_IIR_THREADS")) : 3072.0;
+        int nseg = (int)std::ceil(148.0 * iir_threads / std::max(1.0, threads));
         nseg = std::max(1, std::min(nseg, std::max(1, L / 24)));
         nseg = std::min(nseg, 128);
         const int seglen = (L + nseg - 1) / nseg;

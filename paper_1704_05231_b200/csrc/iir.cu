@@ -42,6 +42,7 @@ namespace {
 
 constexpr int kIirTX = 32;  // lines per block (one warp)
 constexpr int kIirSY = 4;   // segments per block
+constexpr int kIirMinBlocks = 8;  // 64 registers: more resident warps for the latency-bound passes
 constexpr int kIirU = 3;    // samples per load batch (forward pass)
 constexpr int kIirUB = 3;   // scratch samples per load batch (backward / output passes)
 
@@ -91,7 +92,7 @@ __device__ __forceinline__ void modulate_pair(int pair, double jr, double ji, do
 
 // ---- pass 1: modulate + zero-state forward recursion per segment ----
 template <typename T, bool REAL>
-__global__ void __launch_bounds__(128) iir_fwd(const IirArgs<T> a) {
+__global__ void __launch_bounds__(128, kIirMinBlocks) iir_fwd(const IirArgs<T> a) {
     using S = typename SrcT<T, REAL>::type;
     const int x = blockIdx.x * kIirTX + threadIdx.x;
     const int seg = blockIdx.y * kIirSY + threadIdx.y;
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(128) iir_fwd(const IirArgs<T> a) {
 
 // ---- pass 2: forward carry + correction, zero-state backward recursion ----
 template <typename T>
-__global__ void __launch_bounds__(128) iir_bwd(const IirArgs<T> a) {
+__global__ void __launch_bounds__(128, kIirMinBlocks) iir_bwd(const IirArgs<T> a) {
     const int x = blockIdx.x * kIirTX + threadIdx.x;
     const int seg = blockIdx.y * kIirSY + threadIdx.y;
     if (x >= a.lines || seg >= a.nseg) return;
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(128) iir_bwd(const IirArgs<T> a) {
 
 // ---- pass 3: backward carry + correction, recombination, outputs ----
 template <typename T>
-__global__ void __launch_bounds__(128) iir_out(const IirArgs<T> a) {
+__global__ void __launch_bounds__(128, kIirMinBlocks) iir_out(const IirArgs<T> a) {
     const int x = blockIdx.x * kIirTX + threadIdx.x;
     const int seg = blockIdx.y * kIirSY + threadIdx.y;
     const int jb = blockIdx.z % a.njobs;
