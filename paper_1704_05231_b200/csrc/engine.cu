@@ -1471,6 +1471,8 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.dst_ls = st.iir_row ? st.H : 1;
                     a.dst_ss = st.iir_row ? 1 : st.W;
                     a.real_in = st.iir_real;
+                    a.one_out = 1;
+                    for (int j = 0; j < st.njobs; ++j) a.one_out &= p.ijobs[st.job0 + j].nout == 1;
                     a.scratch = scratch + st.lane * scratch_lane;
                     a.state = states + st.lane * state_lane;
                     std::memcpy(a.Aseg, st.Aseg, sizeof(a.Aseg));

@@ -91,20 +91,41 @@ __device__ __forceinline__ void modulate_pair(int pair, double jr, double ji, do
 }
 
 // ---- pass 1: modulate + zero-state forward recursion per segment ----
-template <typename T, bool REAL>
+// STAGE (horizontal stage: lines are image rows, real input): the CTA's
+// 32 rows x (kIirSY * seglen) samples are fetched row-contiguously into shared
+// memory first instead of one strided element per thread and sample.
+template <typename T, bool REAL, bool STAGE>
 __global__ void __launch_bounds__(128, kIirMinBlocks) iir_fwd(const IirArgs<T> a) {
     using S = typename SrcT<T, REAL>::type;
+    static_assert(!STAGE || REAL, "staging is for the real-input horizontal stage");
     const int x = blockIdx.x * kIirTX + threadIdx.x;
     const int seg = blockIdx.y * kIirSY + threadIdx.y;
     const int jb = blockIdx.z % a.njobs;
     const int b = blockIdx.z / a.njobs;
-    if (x >= a.lines || seg >= a.nseg) return;
     const IirJob<T>& job = a.jobs[jb];
     const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
     const int n0 = seg * a.seglen, n1 = min(L, n0 + a.seglen);
     const S* src = reinterpret_cast<const S*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride +
                    (int64_t)x * a.src_ls;
-    const int64_t ss = a.src_ss;
+    int64_t ss = a.src_ss;
+    if constexpr (STAGE) {
+        extern __shared__ __align__(16) unsigned char smem_raw[];
+        T* tile = reinterpret_cast<T*>(smem_raw);
+        const int sw = kIirSY * a.seglen, swp = sw | 1;  // odd row pitch: conflict-free column reads
+        const int nb0 = blockIdx.y * kIirSY * a.seglen;
+        const S* base = reinterpret_cast<const S*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
+        const int tid = threadIdx.y * kIirTX + threadIdx.x;
+        for (int i = tid; i < kIirTX * sw; i += kIirTX * kIirSY) {
+            const int r = i / sw, cc = i - r * sw;
+            const int line = blockIdx.x * kIirTX + r, n = nb0 + cc;
+            if (line < NL && n < L) tile[r * swp + cc] = base[(int64_t)line * a.src_ls + clampi(n - P, 0, len - 1)];
+        }
+        __syncthreads();
+        // thread view: sample n of this line at tile[threadIdx.x * swp + (n - nb0)]
+        src = reinterpret_cast<const S*>(tile) + threadIdx.x * swp - nb0 + P;
+        ss = 1;
+    }
+    if (x >= a.lines || seg >= a.nseg) return;
     const double2* tabm = a.tab_base + job.tabm_off;
     const int64_t plane = (int64_t)L * NL;
     T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
@@ -112,7 +133,7 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_fwd(const IirArgs<T> a
     const int pair = job.need >> 1;
     double pa[3], pb[3];
     if (seg == 0) {  // the reference's steady-state init on the first padded sample
-        const double2 v = ld_d2(src);
+        const double2 v = ld_d2(src + (STAGE ? -P : 0));
         double za, zb;
         modulate_pair(pair, v.x, v.y, tabm[0], za, zb);
         pa[0] = pa[1] = pa[2] = za;
@@ -127,7 +148,7 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_fwd(const IirArgs<T> a
         double2 v[kIirU];
 #pragma unroll
         for (int u = 0; u < kIirU; ++u)
-            if (nb + u < n1) v[u] = ld_d2(src + clampi(nb + u - P, 0, len - 1) * ss);
+            if (nb + u < n1) v[u] = ld_d2(src + (STAGE ? nb + u - P : clampi(nb + u - P, 0, len - 1) * ss));
 #pragma unroll
         for (int u = 0; u < kIirU; ++u) {
             const int n = nb + u;
@@ -217,17 +238,84 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_bwd(const IirArgs<T> a
     }
 }
 
-// ---- pass 3: backward carry + correction, recombination, outputs ----
+// ---- pass 3 for the horizontal stage: staged, row-contiguous output ----
 template <typename T>
+__device__ __forceinline__ void iir_out_rows(const IirArgs<T>& a, const IirJob<T>& job, int x, int seg, int b, int n0,
+                                             int n1) {
+    using C = cx_t<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* tile = reinterpret_cast<C*>(smem_raw);
+    const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
+    const int sw = kIirSY * a.seglen, swp = sw | 1;
+    const int nb0 = blockIdx.y * kIirSY * a.seglen;
+    const bool live = x < NL && seg < a.nseg && n1 > P && n0 < P + len;
+    if (live) {
+        const int64_t plane = (int64_t)L * NL;
+        const T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
+        const double* sj = a.state + ((int64_t)a.njobs * a.batch * a.nseg * 6) * NL +
+                           (((int64_t)blockIdx.z * a.nseg + seg) * 6) * NL + x;
+        double ta[3], tb[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            ta[k] = sj[(int64_t)k * NL];
+            tb[k] = sj[(int64_t)(3 + k) * NL];
+        }
+        const bool last = seg == a.nseg - 1;
+        const double osg = (job.sdft ? -1.0 : 1.0) * (job.conj[0] ? -1.0 : 1.0);
+        const double2* tabr = a.tab_base + job.tabr_off;
+        const int lo = max(n0, P), hi = min(n1, P + len);
+        C* trow = tile + threadIdx.x * swp - nb0;
+        for (int nb = lo; nb < hi; nb += kIirUB) {
+            T ua[kIirUB], ub[kIirUB];
+#pragma unroll
+            for (int k = 0; k < kIirUB; ++k) {
+                const T* o = sc + (int64_t)(nb + k) * NL;
+                if (nb + k < hi) { ua[k] = o[0]; ub[k] = o[plane]; }
+            }
+#pragma unroll
+            for (int k = 0; k < kIirUB; ++k) {
+                const int n = nb + k;
+                if (n >= hi) break;
+                double va = ua[k], vb = ub[k];
+                if (!last) {
+                    const double* g = a.g + 3 * (n1 - 1 - n);
+                    const double g0 = g[0], g1 = g[1], g2 = g[2];
+                    va += g0 * ta[0] + g1 * ta[1] + g2 * ta[2];
+                    vb += g0 * tb[0] + g1 * tb[1] + g2 * tb[2];
+                }
+                const double2 cs = tabr[n - P];
+                trow[n] = mk<T>((T)fma(cs.x, va, cs.y * vb), (T)(osg * fma(cs.y, va, -cs.x * vb)));
+            }
+        }
+    }
+    __syncthreads();
+    // row-contiguous write-out of the CTA's 32 rows x sw samples (crop window only)
+    C* dst = a.dst_base + job.dst_off[0] + (int64_t)b * a.dst_bstride;
+    const int tid = threadIdx.y * kIirTX + threadIdx.x;
+    for (int i = tid; i < kIirTX * sw; i += kIirTX * kIirSY) {
+        const int r = i / sw, cc = i - r * sw;
+        const int line = blockIdx.x * kIirTX + r, n = nb0 + cc;
+        if (line < NL && n >= P && n < P + len && n < L) dst[(int64_t)line * a.dst_ls + (n - P)] = tile[r * swp + cc];
+    }
+}
+
+// ---- pass 3: backward carry + correction, recombination, outputs ----
+// STAGE (horizontal stage, one output per job): results go to a shared tile
+// and leave row-contiguously instead of one strided element per thread.
+template <typename T, bool STAGE>
 __global__ void __launch_bounds__(128, kIirMinBlocks) iir_out(const IirArgs<T> a) {
     const int x = blockIdx.x * kIirTX + threadIdx.x;
     const int seg = blockIdx.y * kIirSY + threadIdx.y;
     const int jb = blockIdx.z % a.njobs;
     const int b = blockIdx.z / a.njobs;
-    if (x >= a.lines || seg >= a.nseg) return;
     const IirJob<T>& job = a.jobs[jb];
     const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
     const int n0 = seg * a.seglen, n1 = min(L, n0 + a.seglen);
+    if constexpr (STAGE) {
+        iir_out_rows<T>(a, job, x, seg, b, n0, n1);
+        return;
+    }
+    if (x >= a.lines || seg >= a.nseg) return;
     if (n1 <= P || n0 >= P + len) return;  // nothing of this segment survives the crop
     const int64_t plane = (int64_t)L * NL;
     const T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
@@ -415,12 +503,18 @@ template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s
     std::memcpy(m.Alast, a.Alast, sizeof(m.Alast));
     const dim3 sgrid((a.lines + 31) / 32, 1, a.njobs * a.batch), sblock(32, kScanG);
     const int64_t bwd_sec = (int64_t)a.njobs * a.batch * a.nseg * 6 * a.lines;
-    if (a.real_in) iir_fwd<T, true><<<grid, block, 0, s>>>(a);
-    else iir_fwd<T, false><<<grid, block, 0, s>>>(a);
+    // horizontal stage (real rows in, one output per job): stage through shared memory
+    const size_t sw = (size_t)(kIirSY * a.seglen) | 1;
+    const size_t in_smem = kIirTX * sw * sizeof(T), out_smem = kIirTX * sw * sizeof(cx_t<T>);
+    const bool stage = a.real_in && a.src_ss == 1 && a.dst_ss == 1 && a.one_out && out_smem <= 48 * 1024;
+    if (stage) iir_fwd<T, true, true><<<grid, block, in_smem, s>>>(a);
+    else if (a.real_in) iir_fwd<T, true, false><<<grid, block, 0, s>>>(a);
+    else iir_fwd<T, false, false><<<grid, block, 0, s>>>(a);
     iir_scan<0><<<sgrid, sblock, 0, s>>>(a.state, 0, a.lines, a.nseg, m);
     iir_bwd<T><<<grid, block, 0, s>>>(a);
     iir_scan<1><<<sgrid, sblock, 0, s>>>(a.state, bwd_sec, a.lines, a.nseg, m);
-    iir_out<T><<<grid, block, 0, s>>>(a);
+    if (stage) iir_out<T, true><<<grid, block, out_smem, s>>>(a);
+    else iir_out<T, false><<<grid, block, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -128,6 +128,7 @@ template <typename T> struct IirArgs {
     int njobs, batch;
     int nseg, seglen;
     int real_in;
+    int one_out;             // every job has exactly one output
 };
 template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s);
 template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch);
