@@ -180,7 +180,8 @@ def int_array(vals):
 
 
 def profile_read() -> list[dict]:
-    buf = (fgb_prof_entry * 32)()
-    n = check(lib.fgb_profile_read(buf, 32))
+    cap = 4096  # distinct step names (FGB_PROF_DETAIL names every step of a plan)
+    buf = (fgb_prof_entry * cap)()
+    n = check(lib.fgb_profile_read(buf, cap))
     return [dict(name=e.name.decode(), launches=e.launches, ms=e.ms, flops=e.flops, bytes=e.bytes)
-            for e in buf[: min(n, 32)]]
+            for e in buf[: min(n, cap)]]
