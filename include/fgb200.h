@@ -143,6 +143,13 @@ int32_t fgb_horizontal_stage_host(const fgb_filter_desc* d, const void* img_host
 int32_t fgb_vertical_stage_host(const fgb_filter_desc* d, const void* j_host, void* out_host, int32_t conjugate);
 int32_t fgb_sdft_bin_host(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img_host, void* out_host);
 int32_t fgb_sdft_horizontal_host(const fgb_sdft_desc* d, int32_t u, const void* img_host, void* j_host);
+/* Same calls returning the reference's ComplexImage layout directly:
+ * [batch][entries][2][H][W] float64 (re plane, im plane per entry), converted
+ * on the GPU; *nonfinite = 1 if any output value is NaN / inf (the reference
+ * rejects such images, image_io.py:65-66).  Used by the Python drop-in API. */
+int32_t fgb_bank_host_planar(const fgb_bank_desc* d, const void* img_host, double* out_host, int32_t* nonfinite);
+int32_t fgb_filter_host_planar(const fgb_filter_desc* d, const void* img_host, double* out_host, int32_t* nonfinite);
+int32_t fgb_sdft_host_planar(const fgb_sdft_desc* d, const void* img_host, double* out_host, int32_t* nonfinite);
 
 /* ---- brute-force references (oracle.py:53-109), direct 2-D tap sums ---- */
 /* fir_gabor(f, p, OracleConfig(radius)): replicate boundary.  localized_dft(f,

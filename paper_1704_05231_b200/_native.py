@@ -112,6 +112,9 @@ _SIGS = {
     "fgb_bank_host": (C.c_int32, [_P(fgb_bank_desc), _vp, _vp]),
     "fgb_filter_host": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp]),
     "fgb_sdft_host": (C.c_int32, [_P(fgb_sdft_desc), _vp, _vp]),
+    "fgb_bank_host_planar": (C.c_int32, [_P(fgb_bank_desc), _vp, _vp, _P(C.c_int32)]),
+    "fgb_filter_host_planar": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp, _P(C.c_int32)]),
+    "fgb_sdft_host_planar": (C.c_int32, [_P(fgb_sdft_desc), _vp, _vp, _P(C.c_int32)]),
     "fgb_horizontal_stage_host": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp]),
     "fgb_vertical_stage_host": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp, C.c_int32]),
     "fgb_sdft_bin_host": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, C.c_int32, _vp, _vp]),

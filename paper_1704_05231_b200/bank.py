@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from ._precision import cplx_dtype, real_dtype, resolve
+from ._precision import real_dtype, resolve
 from .gabor import GaborParams, HorizontalStage, _vertical
 from .gaussian import SmootherKind, native_smoother
 from .image_io import ComplexImage, RealImage
@@ -111,8 +111,10 @@ def _run_bank(f: RealImage, spec: BankSpec, kind, counters: OpCounters, reuse: b
             raise ValueError("sigma must be positive")
     src = np.ascontiguousarray(f.data, dtype=real_dtype(prec))
     n = spec.orientations_n
-    out = np.empty((len(spec.frequencies) * n, h, w), dtype=cplx_dtype(prec))
-    N.check(N.lib.fgb_bank_host(C.byref(d), src.ctypes.data, out.ctypes.data))
+    # float64 re/im planes straight from the GPU (ComplexImage layout, no host conversion)
+    out = np.empty((len(spec.frequencies) * n, 2, h, w), dtype=np.float64)
+    bad = C.c_int32(0)
+    N.check(N.lib.fgb_bank_host_planar(C.byref(d), src.ctypes.data, out.ctypes.data, C.byref(bad)))
     del keep
     _charge_bank(counters, spec, kind, h, w, reuse)
     thetas = spec.thetas()
@@ -120,7 +122,7 @@ def _run_bank(f: RealImage, spec: BankSpec, kind, counters: OpCounters, reuse: b
     for i, omega in enumerate(spec.frequencies):
         s = spec.sigma_for(i)
         for k in range(n):
-            entries.append((GaborParams(omega, thetas[k], s), ComplexImage.from_interleaved(out[i * n + k])))
+            entries.append((GaborParams(omega, thetas[k], s), ComplexImage.from_planar(out[i * n + k], bad.value == 0)))
     return BankOutput(entries, counters)
 
 

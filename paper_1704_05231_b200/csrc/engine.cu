@@ -1302,6 +1302,7 @@ struct Ctx {
     DevBuf ws;
     std::map<std::string, std::shared_ptr<PlanBase>> plans;
     DevBuf hin, hout;  // device staging of the *_host entry points
+    DevBuf hpl, hflag; // planar f64 staging + non-finite flag of the *_host_planar entry points
 };
 static std::mutex g_mu;
 static std::map<int, std::unique_ptr<Ctx>> g_ctx;
@@ -1790,6 +1791,39 @@ static int32_t host_call(const fgb_image& im, int64_t out_elems_c, const void* i
     return FGB_OK;
 }
 
+// Same as host_call, but the result reaches the host as the reference's
+// ComplexImage layout: [entries][2][plane] float64 (re plane, im plane),
+// converted on the GPU, with a finiteness flag so the host can skip its own
+// per-element checks.
+template <typename F>
+static int32_t host_call_planar(const fgb_image& im, int64_t out_elems_c, int64_t plane, const void* in_h,
+                                double* out_h, int32_t* nonfinite, F compute) {
+    Ctx& cx = ctx();
+    const size_t in_b = img_bytes(im);
+    const size_t out_b = (size_t)out_elems_c * 2 * elem_size(im.dtype);
+    const size_t pl_b = (size_t)out_elems_c * 2 * sizeof(double);
+    FGB_TRY(cx.hin.ensure(in_b));
+    FGB_TRY(cx.hout.ensure(out_b));
+    FGB_TRY(cx.hpl.ensure(pl_b));
+    FGB_TRY(cx.hflag.ensure(sizeof(int)));
+    cudaStream_t s = 0;
+    FGB_CUDA(cudaMemsetAsync(cx.hflag.p, 0, sizeof(int), s));
+    FGB_CUDA(cudaMemcpyAsync(cx.hin.p, in_h, in_b, cudaMemcpyHostToDevice, s));
+    FGB_TRY(compute(cx.hin.p, cx.hout.p, s));
+    if (im.dtype == FGB_F32)
+        FGB_CUDA(launch_entries_planar<float>((const float2*)cx.hout.p, out_elems_c, plane, (double*)cx.hpl.p,
+                                              (int*)cx.hflag.p, s));
+    else
+        FGB_CUDA(launch_entries_planar<double>((const double2*)cx.hout.p, out_elems_c, plane, (double*)cx.hpl.p,
+                                               (int*)cx.hflag.p, s));
+    int flag = 0;
+    FGB_CUDA(cudaMemcpyAsync(out_h, cx.hpl.p, pl_b, cudaMemcpyDeviceToHost, s));
+    FGB_CUDA(cudaMemcpyAsync(&flag, cx.hflag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FGB_CUDA(cudaStreamSynchronize(s));
+    if (nonfinite) *nonfinite = flag;
+    return FGB_OK;
+}
+
 }  // namespace fgb
 
 extern "C" {
@@ -1923,6 +1957,42 @@ int32_t fgb_sdft_host(const fgb_sdft_desc* d, const void* img_host, void* out_ho
     return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
         return d->img.dtype == FGB_F32 ? sdft_t<float>(d, -1, -1, i, o, s) : sdft_t<double>(d, -1, -1, i, o, s);
     });
+}
+
+int32_t fgb_bank_host_planar(const fgb_bank_desc* d, const void* img_host, double* out_host, int32_t* nonfinite) {
+    FGB_TRY(validate_bank(d));
+    const int64_t ne = fgb_bank_entries(d);
+    if (ne < 0) return (int32_t)ne;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t plane = (int64_t)d->img.height * d->img.width;
+    return host_call_planar(d->img, ne * plane * d->img.batch, plane, img_host, out_host, nonfinite,
+                            [&](void* i, void* o, cudaStream_t s) {
+                                return d->img.dtype == FGB_F32 ? bank_t<float>(d, i, o, s) : bank_t<double>(d, i, o, s);
+                            });
+}
+
+int32_t fgb_filter_host_planar(const fgb_filter_desc* d, const void* img_host, double* out_host, int32_t* nonfinite) {
+    FGB_TRY(validate_filter(d, false));
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t plane = (int64_t)d->img.height * d->img.width;
+    return host_call_planar(d->img, plane * d->img.batch, plane, img_host, out_host, nonfinite,
+                            [&](void* i, void* o, cudaStream_t s) {
+                                return d->img.dtype == FGB_F32 ? filter_t<float>(d, 0, i, o, s)
+                                                               : filter_t<double>(d, 0, i, o, s);
+                            });
+}
+
+int32_t fgb_sdft_host_planar(const fgb_sdft_desc* d, const void* img_host, double* out_host, int32_t* nonfinite) {
+    FGB_TRY(validate_sdft(d));
+    const int64_t nb = fgb_sdft_bins(d);
+    if (nb < 0) return (int32_t)nb;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t plane = (int64_t)d->img.height * d->img.width;
+    return host_call_planar(d->img, nb * plane * d->img.batch, plane, img_host, out_host, nonfinite,
+                            [&](void* i, void* o, cudaStream_t s) {
+                                return d->img.dtype == FGB_F32 ? sdft_t<float>(d, -1, -1, i, o, s)
+                                                               : sdft_t<double>(d, -1, -1, i, o, s);
+                            });
 }
 
 int32_t fgb_horizontal_stage_host(const fgb_filter_desc* d, const void* img_host, void* j_host) {

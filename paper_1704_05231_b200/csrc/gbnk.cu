@@ -9,6 +9,7 @@
 // entry is converted and copied.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -29,7 +30,34 @@ __global__ void planar_f64(const cx_t<T>* in, int64_t n, double* re, double* im)
     }
 }
 
+// [entries][H*W] interleaved complex -> [entries][2][H*W] f64 planes (re then
+// im per entry, the reference's ComplexImage layout) + a non-finite flag.
+template <typename T>
+__global__ void entries_planar_f64(const cx_t<T>* in, int64_t n, int64_t plane, double* out, int* nonfinite) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const cx_t<T> v = in[i];
+        const int64_t e = i / plane, q = i - e * plane;
+        const double re = (double)v.x, im = (double)v.y;
+        __stcs(out + 2 * e * plane + q, re);
+        __stcs(out + (2 * e + 1) * plane + q, im);
+        bad |= !(isfinite(re) && isfinite(im));
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
 }  // namespace
+
+template <typename T>
+cudaError_t launch_entries_planar(const cx_t<T>* in, int64_t n, int64_t plane, double* out, int* nonfinite,
+                                  cudaStream_t s) {
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+    entries_planar_f64<T><<<blocks, threads, 0, s>>>(in, n, plane, out, nonfinite);
+    return cudaGetLastError();
+}
+template cudaError_t launch_entries_planar<float>(const float2*, int64_t, int64_t, double*, int*, cudaStream_t);
+template cudaError_t launch_entries_planar<double>(const double2*, int64_t, int64_t, double*, int*, cudaStream_t);
 
 // Returns 0 on success, -1 on I/O failure, -2 on CUDA failure (message in *err).
 int gbnk_write_device(const char* path, const double* params, int n_entries, int H, int W, int dtype,

@@ -134,6 +134,13 @@ template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s
 template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch);
 size_t iir_state_doubles(int lines, int nseg, int njobs, int batch);
 
+// ---- output layout conversion (gbnk.cu) -----------------------------------
+// [entries][plane] interleaved complex -> [entries][2][plane] f64 (re plane,
+// im plane), *nonfinite |= 1 if any value is NaN / inf.
+template <typename T>
+cudaError_t launch_entries_planar(const cx_t<T>* in, int64_t n, int64_t plane, double* out, int* nonfinite,
+                                  cudaStream_t s);
+
 // ---- brute-force 2-D references (bruteforce.cu) ---------------------------
 template <typename T> struct Direct2DArgs {
     const T* img;

@@ -102,8 +102,9 @@ def gabor_filter(f: RealImage, p: GaborParams, kind: SmootherKind, counters: OpC
     h, w = f.data.shape
     d = _filter_desc(h, w, p, kind, prec)
     src = _as_real(f, prec)
-    out = np.empty((h, w), dtype=cplx_dtype(prec))
-    N.check(N.lib.fgb_filter_host(C.byref(d), src.ctypes.data, out.ctypes.data))
+    out = np.empty((2, h, w), dtype=np.float64)
+    bad = C.c_int32(0)
+    N.check(N.lib.fgb_filter_host_planar(C.byref(d), src.ctypes.data, out.ctypes.data, C.byref(bad)))
     charge_gabor_row(counters, kind, p.sigma, h, w)
     charge_gabor_col(counters, kind, p.sigma, h, w)
-    return ComplexImage.from_interleaved(out)
+    return ComplexImage.from_planar(out, bad.value == 0)

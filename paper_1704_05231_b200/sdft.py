@@ -133,8 +133,10 @@ def sdft_full(f: RealImage, spec: SdftSpec, counters: OpCounters, precision: str
     h, w = f.data.shape
     d, keep = sdft_desc(h, w, spec, prec)
     src = np.ascontiguousarray(f.data, dtype=real_dtype(prec))
-    out = np.empty((spec.mx * spec.my, h, w), dtype=cplx_dtype(prec))
-    N.check(N.lib.fgb_sdft_host(C.byref(d), src.ctypes.data, out.ctypes.data))
+    out = np.empty((spec.mx * spec.my, 2, h, w), dtype=np.float64)
+    bad = C.c_int32(0)
+    N.check(N.lib.fgb_sdft_host_planar(C.byref(d), src.ctypes.data, out.ctypes.data, C.byref(bad)))
     _charge_full(counters, spec, h, w)
-    bins = [[ComplexImage.from_interleaved(out[u * spec.my + v]) for v in range(spec.my)] for u in range(spec.mx)]
+    bins = [[ComplexImage.from_planar(out[u * spec.my + v], bad.value == 0) for v in range(spec.my)]
+            for u in range(spec.mx)]
     return SdftOutput(bins, counters)

@@ -194,3 +194,14 @@ def test_randomized_sweep_f64(env):
         for u in range(mx):
             for v in range(my):
                 assert max_rel_err(sd.bins[u][v], sref[u][v]) <= 1e-10, (case, h, w, mx, my, u, v)
+
+
+def test_non_finite_outputs_raise_like_reference(env):
+    """Outputs that overflow (1e308-valued fp64 input) are rejected with the
+    reference's ComplexImage error, through the GPU finiteness flag."""
+    torch, fg, D, P = env
+    f = fg.RealImage.from_array(np.full((16, 16), 1e308))
+    with pytest.raises(ValueError, match="finite"):
+        fg.compute_bank(f, fg.BankSpec((1.0,), 2, (1.0,)), fg.ExactFIR(3.0), fg.OpCounters(), precision="f64")
+    with pytest.raises(ValueError, match="finite"):
+        fg.gabor_filter(f, fg.GaborParams(1.0, 0.3, 1.0), fg.ExactFIR(3.0), fg.OpCounters(), precision="f64")

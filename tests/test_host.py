@@ -199,6 +199,19 @@ def test_images_and_conjugate(fg):
         fg.RealImage.from_array(np.zeros(3))
 
 
+def test_complex_image_from_planar(fg):
+    """*_host_planar results: GPU-checked planes become views without a copy;
+    unchecked (non-finite) ones go through the reference constructor's check."""
+    planes = np.arange(24, dtype=np.float64).reshape(2, 3, 4)
+    img = fg.ComplexImage.from_planar(planes, True)
+    assert (img.width, img.height) == (4, 3) and np.shares_memory(img.re, planes)
+    assert np.array_equal(img.im, planes[1])
+    bad = planes.copy()
+    bad[1, 0, 0] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        fg.ComplexImage.from_planar(bad, False)
+
+
 def test_entry_and_bin_counts(fg):
     """Output sizing of sharded calls (compact layouts) computed by the library."""
     import ctypes as C
