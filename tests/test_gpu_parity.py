@@ -151,3 +151,27 @@ def test_config2_full_f32(fg):
             ref = O.gabor_filter(f, om, k * math.pi / 8, s, ("fir", 3.0))
             worst = max(worst, max_rel_err(out.entries[i * 8 + k][1], ref))
     assert worst <= TOL32, worst
+
+
+def test_config2_full_iir_f32(fg):
+    """Config 2's image and bank with RecursiveIIR (the reference CLI's default
+    smoother) at full size, fp32 build (fp64 recursion state) vs the oracle's
+    float64 lfilter restatement: every frequency, a direct / mirror pair and the
+    theta = pi/2 entry (the near-DC row pass, SURVEY App. B's worst case)."""
+    import scipy.ndimage as ndi
+
+    f64 = np.random.default_rng(1).uniform(0.0, 1.0, size=(1024, 1024)).astype(np.float32).astype(np.float64)
+    f32 = ndi.uniform_filter(f64, size=5, mode="nearest").astype(np.float32)
+    freqs = (math.pi / 2, math.pi / 4, math.pi / 8, math.pi / 16)
+    sig = (2.0, 4.0, 8.0, 16.0)
+    out = fg.compute_bank(fg.RealImage.from_array(f32), fg.BankSpec(freqs, 8, sig), fg.RecursiveIIR(),
+                          fg.OpCounters(), precision="f32")
+    f = f32.astype(np.float64)
+    worst = 0.0
+    for i, (om, s) in enumerate(zip(freqs, sig)):
+        jr, ji = O.horizontal_stage(f, om, 3 * math.pi / 8, s, ("iir",))
+        worst = max(worst, max_rel_err(out.entries[i * 8 + 3][1], O.vertical_stage(jr, ji, om, 3 * math.pi / 8, s, ("iir",))))
+        worst = max(worst, max_rel_err(out.entries[i * 8 + 5][1],
+                                       O.vertical_stage(jr, ji, om, 3 * math.pi / 8, s, ("iir",), conjugate=True)))
+        worst = max(worst, max_rel_err(out.entries[i * 8 + 4][1], O.gabor_filter(f, om, math.pi / 2, s, ("iir",))))
+    assert worst <= TOL32, worst
