@@ -109,7 +109,9 @@ class ClockSampler:
         self.th = None
         try:
             import pynvml
-
+        except ImportError:  # no NVML bindings: clocks are reported as unavailable
+            return self
+        try:
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
             self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
@@ -120,13 +122,13 @@ class ClockSampler:
                         sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                         rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                         self.samples.append((float(sm), int(rs)))
-                    except Exception:
+                    except pynvml.NVMLError:  # a missed sample is not fatal
                         pass
                     self.stop.wait(0.001)
 
             self.th = threading.Thread(target=run, daemon=True)
             self.th.start()
-        except Exception:
+        except pynvml.NVMLError:
             self.th = None
         return self
 
@@ -326,7 +328,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             peaks = json.load(fh)
-    except Exception:
+    except (OSError, ValueError):  # absent / unreadable: fall back to the recipe's figure
         pass
     hbm = peaks.get("hbm_gbs", 6650.0)
     kernels = {}
@@ -345,7 +347,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             tr = json.load(fh)
         if top is not None:
             traffic = tr.get(f"cfg{args.config}/{top['name']}")
-    except Exception:
+    except (OSError, ValueError):
         traffic = None
     roof = None
     if top is not None:

@@ -1,3 +1,9 @@
+"""The README usage snippet, runnable: python tools/readme_example.py"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
 import numpy as np, paper_1704_05231_b200 as fg
 
 f = fg.RealImage.from_array(np.random.default_rng(0).uniform(size=(1024, 1024)))
