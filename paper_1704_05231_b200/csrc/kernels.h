@@ -170,12 +170,12 @@ struct BankFusedArgs {
     BankFusedOut out[kMaxND];
 };
 struct BankFusedW {
-    static constexpr int kCap = 7168;  // floats (28 KB): row taps [(h+1)][NDP][2], column taps [nd][ntp][2]
+    static constexpr int kCap = 7168;  // floats (28 KB): row taps [(hp+1)][NDP][2], column taps [nd][ntp][2]
     float w[kCap];
 };
 bool bank_fused_ok(int h, int nd);
 size_t bank_fused_smem(int h, int nd, int TY);
-inline int bank_fused_r(int h) { return h <= 6 ? (std::getenv("FGB_BF_R8") ? 8 : 4) : 4; }
+inline int bank_fused_pad(int n) { return (n + 3) & ~3; }  // row taps (hp) / column taps (ntp) in 4-tap chunks
 cudaError_t launch_bank_fused(const BankFusedArgs& a, const BankFusedW& w, cudaStream_t s);
 
 }  // namespace fgb
