@@ -1420,7 +1420,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                 pr.e1 = pool_event();
                 cudaEventRecord(pr.e0, s);
             }
-            ++g_launches;
+            g_launches += st.kind == ST_IIR ? 5 : 1;  // kernels per step: IIR = fwd, scan, bwd, scan, out
             switch (st.kind) {
                 case ST_ROW: {
                     RowArgs<T> a{};
