@@ -1301,6 +1301,8 @@ struct Ctx {
     std::vector<cudaEvent_t> lane_ev;
     cudaEvent_t fork_ev = nullptr;
     ~Ctx() {
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        for (auto e : piece_ev) cudaEventDestroy(e);
         for (auto st : lanes) cudaStreamDestroy(st);
         for (auto e : lane_ev) cudaEventDestroy(e);
         if (fork_ev) cudaEventDestroy(fork_ev);
@@ -1308,6 +1310,8 @@ struct Ctx {
     DevBuf ws;
     std::map<std::string, std::shared_ptr<PlanBase>> plans;
     DevBuf hin, hout;  // device staging of the *_host entry points
+    cudaStream_t copy_stream = nullptr;    // D2H of finished pieces while later pieces compute
+    std::vector<cudaEvent_t> piece_ev;
     DevBuf hpl, hflag; // planar f64 staging + non-finite flag of the *_host_planar entry points
 };
 static std::mutex g_mu;
@@ -1936,13 +1940,66 @@ int32_t fgb_sdft_horizontal(const fgb_sdft_desc* d, int32_t u, const void* img, 
     return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, -1, img, j_out, s) : sdft_t<double>(d, u, -1, img, j_out, s);
 }
 
+// Host-buffer bank with the D2H pipelined behind the compute: the call is cut
+// into pieces (images of a batch, else frequencies of one image), each
+// piece's outputs leave on a copy stream as soon as its kernels finish, so
+// only the first piece's compute is exposed in front of the PCIe transfer.
+static int32_t bank_host_pipelined(const fgb_bank_desc* d, const void* in_h, void* out_h) {
+    Ctx& cx = ctx();
+    const fgb_image& im = d->img;
+    const int64_t entries = fgb_bank_entries(d);
+    const int64_t hw = (int64_t)im.height * im.width;
+    const size_t es = elem_size(im.dtype);
+    const size_t in_b = img_bytes(im);
+    const size_t out_b = (size_t)(entries * hw * im.batch) * 2 * es;
+    FGB_TRY(cx.hin.ensure(in_b));
+    FGB_TRY(cx.hout.ensure(out_b));
+    if (!cx.copy_stream) FGB_CUDA(cudaStreamCreateWithFlags(&cx.copy_stream, cudaStreamNonBlocking));
+    const bool by_image = im.batch > 1;
+    const bool by_freq = !by_image && d->n_freq > 1 && d->units == nullptr;
+    const int pieces = by_image ? im.batch : (by_freq ? d->n_freq : 1);
+    while ((int)cx.piece_ev.size() < pieces) {
+        cudaEvent_t e;
+        FGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cx.piece_ev.push_back(e);
+    }
+    cudaStream_t s = 0;
+    FGB_CUDA(cudaMemcpyAsync(cx.hin.p, in_h, in_b, cudaMemcpyHostToDevice, s));
+    const int64_t img_stride = im.batch > 1 ? im.batch_stride : (int64_t)im.height * im.pitch;
+    const int64_t per_freq = entries / std::max(1, d->n_freq);
+    for (int p = 0; p < pieces; ++p) {
+        fgb_bank_desc dp = *d;
+        const char* in_d = (const char*)cx.hin.p;
+        int64_t out_off = 0, out_n = entries * hw * im.batch;  // complex elements
+        if (by_image) {
+            dp.img.batch = 1;
+            in_d += (size_t)(p * img_stride) * es;
+            out_off = p * entries * hw;
+            out_n = entries * hw;
+        } else if (by_freq) {
+            const int f = d->n_freq - 1 - p;  // smallest sigma first: the copy engine starts earliest
+            dp.n_freq = 1;
+            dp.omegas = d->omegas + f;
+            dp.sigmas = d->sigmas + f;
+            out_off = f * per_freq * hw;
+            out_n = per_freq * hw;
+        }
+        char* out_d = (char*)cx.hout.p + (size_t)out_off * 2 * es;
+        FGB_TRY(im.dtype == FGB_F32 ? bank_t<float>(&dp, in_d, out_d, s) : bank_t<double>(&dp, in_d, out_d, s));
+        FGB_CUDA(cudaEventRecord(cx.piece_ev[p], s));
+        FGB_CUDA(cudaStreamWaitEvent(cx.copy_stream, cx.piece_ev[p], 0));
+        FGB_CUDA(cudaMemcpyAsync((char*)out_h + (size_t)out_off * 2 * es, out_d, (size_t)out_n * 2 * es,
+                                 cudaMemcpyDeviceToHost, cx.copy_stream));
+    }
+    FGB_CUDA(cudaStreamSynchronize(cx.copy_stream));
+    FGB_CUDA(cudaStreamSynchronize(s));
+    return FGB_OK;
+}
+
 int32_t fgb_bank_host(const fgb_bank_desc* d, const void* img_host, void* out_host) {
     FGB_TRY(validate_bank(d));
     std::lock_guard<std::mutex> lk(g_mu);
-    const int64_t n = fgb_bank_entries(d) * (int64_t)d->img.height * d->img.width * d->img.batch;
-    return host_call(d->img, n, img_host, out_host, [&](void* i, void* o, cudaStream_t s) {
-        return d->img.dtype == FGB_F32 ? bank_t<float>(d, i, o, s) : bank_t<double>(d, i, o, s);
-    });
+    return bank_host_pipelined(d, img_host, out_host);
 }
 
 int32_t fgb_filter_host(const fgb_filter_desc* d, const void* img_host, void* out_host) {

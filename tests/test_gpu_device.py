@@ -223,3 +223,26 @@ def test_fused_small_sigma_bank_f32(env, shape):
         ref = O.compute_bank(imgs[b].astype(np.float64), spec.frequencies, 8, spec.sigmas, ("fir", 3.0))
         for e, r in enumerate(ref):
             assert max_rel_err((out[b, e].real, out[b, e].imag), r[3:]) <= 1e-5, (shape, b, e)
+
+
+@pytest.mark.parametrize("batch,units", [(1, None), (3, None), (1, [0, 4, 7])])
+def test_host_buffer_bank_matches_device(env, batch, units):
+    """fgb_bank_host pipelines the D2H behind the compute (pieces = images of a
+    batch, else frequencies); its output must equal the device entry point's
+    bit for bit, including compact unit layouts."""
+    import ctypes as C
+
+    torch, fg, D, P = env
+    from paper_1704_05231_b200 import _native as N
+
+    h, w = 96, 80
+    imgs = np.random.default_rng(3).uniform(0.0, 1.0, size=(batch, h, w)).astype(np.float32)
+    spec = fg.BankSpec((math.pi / 2, math.pi / 4, math.pi / 8), 8, (2.0, 4.0, 8.0))
+    plan = D.BankPlan((batch, h, w), spec, fg.ExactFIR(3.0), "f32", units=units)
+    dev = plan(torch.from_numpy(imgs).cuda(), plan.new_output()).cpu().numpy()
+    host = np.empty_like(dev)
+    desc = plan.desc
+    desc.img.pitch = w
+    desc.img.batch_stride = h * w
+    N.check(N.lib.fgb_bank_host(C.byref(desc), C.c_void_p(imgs.ctypes.data), C.c_void_p(host.ctypes.data)))
+    assert np.array_equal(host, dev)
