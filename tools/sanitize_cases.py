@@ -1,13 +1,13 @@
-"""Small cases over every kernel family, for compute-sanitizer runs:
+"""Small cases over every kernel family (parity + NaN-poisoned, guard-banded outputs):
 
-    compute-sanitizer --tool memcheck  python tools/sanitize_cases.py
-    compute-sanitizer --tool racecheck python tools/sanitize_cases.py --quick
+    python tools/sanitize_cases.py [--quick]
 
-Covers the bank (FIR/IIR/box, f32/f64, even/odd/ragged widths, batched device
+compute-sanitizer is not available on the GPU pool, so out-of-bounds writes are
+caught with NaN guard bands around device outputs and unwritten elements with
+NaN-poisoned outputs.  Covers the bank (FIR/IIR/box, f32/f64, even/odd/ragged widths, batched device
 plans, no-reuse), single filters and stages, the SDFT (fused, generic, IIR,
 box, Mx != My), brute-force oracles on the GPU and the device GBNK writer.
-Each case is also compared with the CPU oracle so a sanitizer-clean run is a
-parity run too.
+Each case is also compared with the CPU oracle.
 """
 
 import argparse
