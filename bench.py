@@ -238,6 +238,22 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     # ---- shard the workload (config 2: every rank its own image -> weak) ----
     scaling = "weak"
+    bcast_ms = None
+
+    def timed_broadcast(t):
+        """The one input broadcast of the sharded configs, timed on the device
+        (max over ranks); it happens once per job, outside the timed steps."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        dist.broadcast(t, 0)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return ms.item()
+
     if cfg["kind"] == "bank":
         spec = fg.BankSpec(tuple(cfg["freqs"]), cfg["n"], tuple(cfg["sigmas"]))
         if args.config == 3:
@@ -256,7 +272,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             imgs = make_image(cfg, 0)[None]
             if world > 1:
                 t = torch.from_numpy(imgs).to(dev)
-                dist.broadcast(t, 0)  # one NCCL broadcast of the input over NVLink
+                bcast_ms = timed_broadcast(t)  # one NCCL broadcast of the input over NVLink
         else:
             imgs = make_image(cfg, rank)[None]
             units = None
@@ -272,7 +288,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         imgs = make_image(cfg, 0)[None]
         timg = torch.from_numpy(imgs).to(dev)
         if world > 1:
-            dist.broadcast(timg, 0)
+            bcast_ms = timed_broadcast(timg)
         plan = SdftPlan(tuple(timg.shape), spec, "f32", heads)
         units_step = timg.shape[1] * timg.shape[2] * plan.bins
     out = plan.new_output(dev)
@@ -427,6 +443,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE.json shapes)",
             "config": {"workload": cfg["workload"], "smoother": args.smoother, "l2": "256 MiB flush between timed steps",
+                       "input_broadcast_ms": bcast_ms,
                        "parallelism": f"{'image' if args.config in (2, 3) else 'unit'}-sharded x{world}"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "kernels": kernels, "fp32_peak_tflops_measured": fp32,
