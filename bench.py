@@ -177,7 +177,10 @@ def cpu_sample(cfg, rows, cores, pool=None):
     t0 = time.perf_counter()
     if cfg["kind"] == "bank":
         nh = cfg["n"] // 2
+        # (frequency, direct k) units -- the reference's own parallel grain (compute_bank
+        # threads=k) -- heaviest (largest sigma) first so the pool's tail is short
         jobs = [(img, w, k, cfg["n"], s) for w, s in zip(cfg["freqs"], cfg["sigmas"]) for k in range(nh + 1)]
+        jobs.sort(key=lambda j: -j[4])
         outs = sum(pool.map(_oracle_bank_unit, jobs, chunksize=1)) if pool else sum(map(_oracle_bank_unit, jobs))
         units = img.shape[0] * img.shape[1] * outs
     else:
