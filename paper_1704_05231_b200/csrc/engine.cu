@@ -1957,7 +1957,8 @@ static int32_t bank_host_pipelined(const fgb_bank_desc* d, const void* in_h, voi
     if (!cx.copy_stream) FGB_CUDA(cudaStreamCreateWithFlags(&cx.copy_stream, cudaStreamNonBlocking));
     const bool by_image = im.batch > 1;
     const bool by_freq = !by_image && d->n_freq > 1 && d->units == nullptr;
-    const int pieces = by_image ? im.batch : (by_freq ? d->n_freq : 1);
+    const bool by_units = !by_image && d->units != nullptr && d->n_units > 1;  // contiguous runs of the unit list
+    const int pieces = by_image ? im.batch : (by_freq ? d->n_freq : (by_units ? std::min(d->n_units, 8) : 1));
     while ((int)cx.piece_ev.size() < pieces) {
         cudaEvent_t e;
         FGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1967,6 +1968,10 @@ static int32_t bank_host_pipelined(const fgb_bank_desc* d, const void* in_h, voi
     FGB_CUDA(cudaMemcpyAsync(cx.hin.p, in_h, in_b, cudaMemcpyHostToDevice, s));
     const int64_t img_stride = im.batch > 1 ? im.batch_stride : (int64_t)im.height * im.pitch;
     const int64_t per_freq = entries / std::max(1, d->n_freq);
+    std::vector<int> order(std::max(1, d->n_freq));
+    for (int i = 0; i < (int)order.size(); ++i) order[i] = i;
+    if (by_freq)  // smallest sigma (cheapest) first: the copy engine starts earliest
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return d->sigmas[x] < d->sigmas[y]; });
     for (int p = 0; p < pieces; ++p) {
         fgb_bank_desc dp = *d;
         const char* in_d = (const char*)cx.hin.p;
@@ -1976,8 +1981,20 @@ static int32_t bank_host_pipelined(const fgb_bank_desc* d, const void* in_h, voi
             in_d += (size_t)(p * img_stride) * es;
             out_off = p * entries * hw;
             out_n = entries * hw;
+        } else if (by_units) {
+            // compact layout: entries of units [u0, u1) follow those of units [0, u0)
+            const int u0 = (int)((int64_t)d->n_units * p / pieces), u1 = (int)((int64_t)d->n_units * (p + 1) / pieces);
+            fgb_bank_desc head = *d;
+            head.n_units = u0;
+            const int64_t before = u0 > 0 ? fgb_bank_entries(&head) : 0;
+            dp.units = d->units + u0;
+            dp.n_units = u1 - u0;
+            const int64_t ne = fgb_bank_entries(&dp);
+            if (before < 0 || ne < 0) return fail(FGB_EINVAL, "invalid unit list");
+            out_off = before * hw;
+            out_n = ne * hw;
         } else if (by_freq) {
-            const int f = d->n_freq - 1 - p;  // smallest sigma first: the copy engine starts earliest
+            const int f = order[p];
             dp.n_freq = 1;
             dp.omegas = d->omegas + f;
             dp.sigmas = d->sigmas + f;
