@@ -9,7 +9,10 @@
 //   bank (Algorithm 1)   bank.py:90-129 / :132-157 -- per frequency: one fused
 //                        row launch for every directly computed orientation
 //                        k <= N/2, then one column launch emitting theta_k
-//                        and pi - theta_k from the same J (bank.py:109-116).
+//                        and pi - theta_k from the same J (bank.py:109-116);
+//                        small half-widths (h <= 6): one fused row+column
+//                        launch with J in shared memory.  Frequencies run on
+//                        up to 4 stream lanes, heaviest first.
 //   filter / stages      gabor.py:107-176, bank.py:68-74
 //   SDFT (Algorithm 2)   sdft.py:178-213 -- J_u for u <= Mx/2 once, every
 //                        (u, v<=My/2) column job writes bin(u,v), the mirror
