@@ -246,3 +246,29 @@ def test_host_buffer_bank_matches_device(env, batch, units):
     desc.img.batch_stride = h * w
     N.check(N.lib.fgb_bank_host(C.byref(desc), C.c_void_p(imgs.ctypes.data), C.c_void_p(host.ctypes.data)))
     assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("kn", ["fir", "iir"])
+def test_huge_image_int64_offsets(env, kn):
+    """16384^2 x 16 orientations (32 GB of outputs, element offsets past 2^31):
+    interior pixels of the full-image bank equal a crop's bank computed
+    separately (the crop carries the full filter support as margin)."""
+    torch, fg, D, P = env
+    n = 16384
+    g = torch.Generator(device="cuda").manual_seed(9)
+    img = torch.rand((1, n, n), device="cuda", generator=g)
+    kind = fg.ExactFIR(3.0) if kn == "fir" else fg.RecursiveIIR()
+    spec = fg.BankSpec((math.pi / 4,), 16, (3.0,))
+    plan = D.BankPlan((1, n, n), spec, kind, "f32")
+    out = plan(img, plan.new_output())
+    y0, x0, m, s = n - 300, n - 260, 200, 120  # crop with a margin wider than the support
+    crop = img[:, y0 - m:y0 + s + m, x0 - m:x0 + s + m].contiguous()
+    cplan = D.BankPlan(tuple(crop.shape), spec, kind, "f32")
+    cout = cplan(crop, cplan.new_output())
+    a = out[0, :, y0:y0 + s, x0:x0 + s]
+    b = cout[0, :, m:m + s, m:m + s]
+    scale = b.abs().max().item()
+    assert torch.isfinite(torch.view_as_real(out[0, -1])).all()
+    assert (a - b).abs().max().item() <= 1e-5 * scale
+    del out
+    torch.cuda.empty_cache()
