@@ -57,6 +57,14 @@ __device__ __forceinline__ void mat3_apply(const double* A, const double* s, dou
     o[2] = A[6] * s[0] + A[7] * s[1] + A[8] * s[2];
 }
 
+// Recursion step writing y[n] into the slot that held y[n-3]: with three
+// named registers whose roles rotate every sample, a 3x unrolled loop needs
+// no state moves (y[n] = B z - a1 y[n-1] - a2 y[n-2] - a3 y[n-3]).
+__device__ __forceinline__ void rec_into(double& oldest, double z, double ym1, double ym2, const IirCoef& c) {
+    const double t = fma(c.B, z, -(c.a2 * ym2 + c.a3 * oldest));
+    oldest = fma(-c.a1, ym1, t);
+}
+
 // one recursion step on a (y[n-1], y[n-2], y[n-3]) state; returns y[n]
 __device__ __forceinline__ double rec_step(double* p, double zin, const IirCoef& c) {
     const double t = fma(c.B, zin, -(c.a2 * p[1] + c.a3 * p[2]));
@@ -141,24 +149,46 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_fwd(const IirArgs<T> a
     } else {
         pa[0] = pa[1] = pa[2] = pb[0] = pb[1] = pb[2] = 0.0;
     }
-    // kIirU input samples are loaded before the dependent recursion consumes
-    // them (the scratch stores would otherwise keep the compiler from
-    // hoisting the next loads: one load in flight per thread)
-    for (int nb = n0; nb < n1; nb += kIirU) {
-        double2 v[kIirU];
-#pragma unroll
-        for (int u = 0; u < kIirU; ++u)
-            if (nb + u < n1) v[u] = ld_d2(src + (STAGE ? nb + u - P : clampi(nb + u - P, 0, len - 1) * ss));
-#pragma unroll
-        for (int u = 0; u < kIirU; ++u) {
-            const int n = nb + u;
-            if (n >= n1) break;
-            double za, zb;
-            modulate_pair(pair, v[u].x, v[u].y, tabm[n], za, zb);
-            T* o = sc + (int64_t)n * NL;
-            o[0] = (T)rec_step(pa, za, c);
-            o[plane] = (T)rec_step(pb, zb, c);
-        }
+    // Three samples per iteration: their inputs are loaded before the
+    // dependent recursion consumes them (the scratch stores would otherwise
+    // keep the compiler from hoisting loads), and the state registers rotate
+    // roles (r0, r1, r2) -> (r2, r0, r1) per sample, so no moves.
+    double a0 = pa[0], a1 = pa[1], a2 = pa[2], b0 = pb[0], b1 = pb[1], b2 = pb[2];
+    auto in_at = [&](int n) { return ld_d2(src + (STAGE ? n - P : clampi(n - P, 0, len - 1) * ss)); };
+    T* o = sc + (int64_t)n0 * NL;
+    const int64_t NL64 = NL;
+    int n = n0;
+    for (; n + 3 <= n1; n += 3) {
+        const double2 v0 = in_at(n), v1 = in_at(n + 1), v2 = in_at(n + 2);
+        double za, zb;
+        modulate_pair(pair, v0.x, v0.y, tabm[n], za, zb);
+        rec_into(a2, za, a0, a1, c);  // y[n] -> a2
+        rec_into(b2, zb, b0, b1, c);
+        o[0] = (T)a2;
+        o[plane] = (T)b2;
+        o += NL64;
+        modulate_pair(pair, v1.x, v1.y, tabm[n + 1], za, zb);
+        rec_into(a1, za, a2, a0, c);  // y[n+1] -> a1
+        rec_into(b1, zb, b2, b0, c);
+        o[0] = (T)a1;
+        o[plane] = (T)b1;
+        o += NL64;
+        modulate_pair(pair, v2.x, v2.y, tabm[n + 2], za, zb);
+        rec_into(a0, za, a1, a2, c);  // y[n+2] -> a0; roles back to (a0, a1, a2)
+        rec_into(b0, zb, b1, b2, c);
+        o[0] = (T)a0;
+        o[plane] = (T)b0;
+        o += NL64;
+    }
+    pa[0] = a0; pa[1] = a1; pa[2] = a2;
+    pb[0] = b0; pb[1] = b1; pb[2] = b2;
+    for (; n < n1; ++n) {  // 0-2 remaining samples
+        const double2 v = in_at(n);
+        double za, zb;
+        modulate_pair(pair, v.x, v.y, tabm[n], za, zb);
+        o[0] = (T)rec_step(pa, za, c);
+        o[plane] = (T)rec_step(pb, zb, c);
+        o += NL64;
     }
     // local end state (y[end], y[end-1], y[end-2]) per plane
     double* st = a.state + (((int64_t)blockIdx.z * a.nseg + seg) * 6) * NL + x;
@@ -205,28 +235,55 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_bwd(const IirArgs<T> a
     } else {
         ua[0] = ua[1] = ua[2] = ub[0] = ub[1] = ub[2] = 0.0;
     }
-    for (int nb = n1 - 1; nb >= n0; nb -= kIirUB) {
-        T ya[kIirUB], yb[kIirUB];
-#pragma unroll
-        for (int k = 0; k < kIirUB; ++k) {
-            const T* o = sc + (int64_t)(nb - k) * NL;
-            if (nb - k >= n0) { ya[k] = o[0]; yb[k] = o[plane]; }
+    // three samples per iteration, rotating state roles (see iir_fwd)
+    double a0 = ua[0], a1 = ua[1], a2 = ua[2], b0 = ub[0], b1 = ub[1], b2 = ub[2];
+    const double sa0 = sa[0], sa1 = sa[1], sa2 = sa[2], sb0 = sb[0], sb1 = sb[1], sb2 = sb[2];
+    const int64_t NL64 = NL;
+    T* o = sc + (int64_t)(n1 - 1) * NL;
+    const double* g = gt + 3 * (n1 - 1 - n0);  // correction row of the current sample
+    // forward value of this segment corrected by the carried-in state (segment 0: exact already)
+    auto corr2 = [&](T ya, T yb, const double* gg, double& va, double& vb) {
+        va = ya;
+        vb = yb;
+        if (!first) {
+            const double g0 = gg[0], g1 = gg[1], g2 = gg[2];
+            va += g0 * sa0 + g1 * sa1 + g2 * sa2;
+            vb += g0 * sb0 + g1 * sb1 + g2 * sb2;
         }
-#pragma unroll
-        for (int k = 0; k < kIirUB; ++k) {
-            const int n = nb - k;
-            if (n < n0) break;
-            T* o = sc + (int64_t)n * NL;
-            double va = ya[k], vb = yb[k];
-            if (!first) {
-                const double* g = gt + 3 * (n - n0);
-                const double g0 = g[0], g1 = g[1], g2 = g[2];
-                va += g0 * sa[0] + g1 * sa[1] + g2 * sa[2];
-                vb += g0 * sb[0] + g1 * sb[1] + g2 * sb[2];
-            }
-            o[0] = (T)rec_step(ua, va, c);
-            o[plane] = (T)rec_step(ub, vb, c);
-        }
+    };
+    int n = n1 - 1;
+    for (; n - 2 >= n0; n -= 3) {
+        const T y0a = o[0], y0b = o[plane];
+        const T y1a = o[-NL64], y1b = o[plane - NL64];
+        const T y2a = o[-2 * NL64], y2b = o[plane - 2 * NL64];
+        double va, vb;
+        corr2(y0a, y0b, g, va, vb);
+        rec_into(a2, va, a0, a1, c);
+        rec_into(b2, vb, b0, b1, c);
+        o[0] = (T)a2;
+        o[plane] = (T)b2;
+        corr2(y1a, y1b, g - 3, va, vb);
+        rec_into(a1, va, a2, a0, c);
+        rec_into(b1, vb, b2, b0, c);
+        o[-NL64] = (T)a1;
+        o[plane - NL64] = (T)b1;
+        corr2(y2a, y2b, g - 6, va, vb);
+        rec_into(a0, va, a1, a2, c);
+        rec_into(b0, vb, b1, b2, c);
+        o[-2 * NL64] = (T)a0;
+        o[plane - 2 * NL64] = (T)b0;
+        o -= 3 * NL64;
+        g -= 9;
+    }
+    ua[0] = a0; ua[1] = a1; ua[2] = a2;
+    ub[0] = b0; ub[1] = b1; ub[2] = b2;
+    for (; n >= n0; --n) {  // 0-2 remaining samples
+        double va, vb;
+        corr2(o[0], o[plane], g, va, vb);
+        o[0] = (T)rec_step(ua, va, c);
+        o[plane] = (T)rec_step(ub, vb, c);
+        o -= NL64;
+        g -= 3;
     }
     // local start state (u[start], u[start+1], u[start+2]) -> the backward half of the state buffer
     double* st = a.state + ((int64_t)a.njobs * a.batch * a.nseg * 6) * NL +
