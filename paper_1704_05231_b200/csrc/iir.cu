@@ -27,10 +27,11 @@
 // chain as s_out = s_loc_end + A^len s_in (a 3x3 scan over segments).  The
 // backward pass is the same recursion on reversed indices.  Five kernels:
 //   fwd    : modulate, local forward recursion -> y_loc (storage type), end states
-//   scan<0>: end states -> carry-ins (grouped affine scan over segments)
+//   scan<0>: end states -> carry-ins (sequential per line, batched loads)
 //   bwd    : correct y, local backward recursion -> u_loc, start states
 //   scan<1>: start states -> carry-ins from above
 //   out    : correct u, recombine -> outputs
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_bwd(const IirArgs<T> a
     T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
     const IirCoef c = a.c;
     const double* st_all = a.state + ((int64_t)blockIdx.z * a.nseg * 6) * NL + x;
-    // true state entering this segment (iir_scan<0> turned the local end states into carry-ins)
+    // true state entering this segment (iir_scan_seq<0> turned the local end states into carry-ins)
     double sa[3], sb[3];
     {
         const double* sj = st_all + (int64_t)seg * 6 * NL;
@@ -378,7 +379,7 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_out(const IirArgs<T> a
     const T* sc = a.scratch + (int64_t)blockIdx.z * 2 * plane + x;
     const double* st_all = a.state + ((int64_t)a.njobs * a.batch * a.nseg * 6) * NL +
                            ((int64_t)blockIdx.z * a.nseg * 6) * NL + x;
-    // true state entering this segment from above (iir_scan<1> turned the local start states into carry-ins)
+    // true state entering this segment from above (iir_scan_seq<1> turned the local start states into carry-ins)
     double ta[3], tb[3];
     {
         const double* sj = st_all + (int64_t)seg * 6 * NL;
@@ -438,108 +439,47 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_out(const IirArgs<T> a
 // DIR 0 (after iir_fwd): s_in[0] = 0, s_in[j+1] = Aseg s_in[j] + end_loc[j]
 // DIR 1 (after iir_bwd): t_in[n-1] = 0, t_in[j-1] = A_j t_in[j] + start_loc[j]
 //                        (A_j = Alast for the shorter last segment)
-// Block = 32 lines x kScanG segment groups.  Each group folds its run of
-// segments into one affine map (P_g, v_g), the groups are chained through
-// shared memory, then each group re-walks its run writing the carry-ins.
-constexpr int kScanG = 16;  // segment groups per CTA
-constexpr int kScanKC = 4;  // register-cached segments per group
-
-__device__ __forceinline__ void mat3_mul(const double* X, const double* Y, double* Z) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) Z[3 * i + j] = X[3 * i] * Y[j] + X[3 * i + 1] * Y[3 + j] + X[3 * i + 2] * Y[6 + j];
-}
-
+// One thread per (line, plane) walks its segments in scan order, loading
+// kSeqB segments' states per round trip (the loads do not depend on the
+// running state; the writes go to slots already read).
+constexpr int kSeqB = 16;
 template <int DIR>
-__global__ void __launch_bounds__(32 * kScanG) iir_scan(double* state, int64_t sec_off, int lines, int nseg,
-                                                       const __grid_constant__ IirScanMats m) {
-    __shared__ double sP[kScanG][9];
-    __shared__ double sv[kScanG][6][32];
-    const int lane = threadIdx.x, grp = threadIdx.y;
-    const int x = blockIdx.x * 32 + lane;
+__global__ void __launch_bounds__(128) iir_scan_seq(double* state, int64_t sec_off, int lines, int nseg,
+                                                   const __grid_constant__ IirScanMats m) {
+    const int x = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int q = threadIdx.x >> 6;  // plane
+    if (x >= lines) return;
     const int NL = lines, ns = nseg;
-    const int k = (ns + kScanG - 1) / kScanG;
-    const int r0 = grp * k, r1 = min(ns, r0 + k);
-    const bool live = x < lines;
-    double* st = state + sec_off + ((int64_t)blockIdx.z * ns * 6) * NL + (live ? x : 0);
-    auto seg_of = [&](int r) { return DIR == 0 ? r : ns - 1 - r; };
-    auto mat_of = [&](int j) -> const double* { return (DIR == 1 && j == ns - 1) ? m.Alast : m.Aseg; };
-    auto load = [&](int r, double* l) {
-        const double* sj = st + (int64_t)seg_of(r) * 6 * NL;
+    double* st = state + sec_off + ((int64_t)blockIdx.z * ns * 6) * NL + (int64_t)(q * 3) * NL + x;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int r0 = 0; r0 < ns; r0 += kSeqB) {
+        double l[kSeqB][3];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) l[q] = live ? sj[(int64_t)q * NL] : 0.0;
-    };
-    auto step = [&](int r, double* v, const double* l) {  // v = M_j v + l
-        const double* M = mat_of(seg_of(r));
-        double o[6];
-        mat3_apply(M, v, o);
-        mat3_apply(M, v + 3, o + 3);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) v[q] = o[q] + l[q];
-    };
-    // runs of up to kScanKC segments keep their states in registers: one load
-    // round trip per thread instead of one per segment and pass
-    const bool cached = r1 - r0 <= kScanKC;
-    double lc[kScanKC][6];
-    if (cached) {
-#pragma unroll
-        for (int i = 0; i < kScanKC; ++i)
-            if (r0 + i < r1) load(r0 + i, lc[i]);
-    }
-    // 1) fold the group's run: v = M_j v + l_j, P = M_j P
-    double v[6] = {0, 0, 0, 0, 0, 0};
-    double P[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-    auto fold_P = [&](int r) {
-        double Q[9];
-        mat3_mul(mat_of(seg_of(r)), P, Q);
-#pragma unroll
-        for (int q = 0; q < 9; ++q) P[q] = Q[q];
-    };
-    if (cached) {
-#pragma unroll
-        for (int i = 0; i < kScanKC; ++i)
-            if (r0 + i < r1) { step(r0 + i, v, lc[i]); fold_P(r0 + i); }
-    } else {
-        for (int r = r0; r < r1; ++r) {
-            double l[6];
-            load(r, l);
-            step(r, v, l);
-            fold_P(r);
+        for (int i = 0; i < kSeqB; ++i) {
+            const int r = r0 + i;
+            if (r < ns) {
+                const double* p = st + (int64_t)(DIR == 0 ? r : ns - 1 - r) * 6 * NL;
+                l[i][0] = p[0];
+                l[i][1] = p[NL];
+                l[i][2] = p[2 * (int64_t)NL];
+            }
         }
-    }
-    if (lane == 0)
 #pragma unroll
-        for (int q = 0; q < 9; ++q) sP[grp][q] = P[q];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) sv[grp][q][lane] = v[q];
-    __syncthreads();
-    // 2) incoming state of this group: X_0 = 0, X_{g+1} = P_g X_g + v_g
-    double X[6] = {0, 0, 0, 0, 0, 0};
-    for (int g = 0; g < grp; ++g) {
-        double o[6];
-        mat3_apply(sP[g], X, o);
-        mat3_apply(sP[g], X + 3, o + 3);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) X[q] = o[q] + sv[g][q][lane];
-    }
-    // 3) re-walk: write the carry-in of each segment, then step past it
-    if (!live) return;
-    auto store = [&](int r) {
-        double* sj = st + (int64_t)seg_of(r) * 6 * NL;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) sj[(int64_t)q * NL] = X[q];
-    };
-    if (cached) {
-#pragma unroll
-        for (int i = 0; i < kScanKC; ++i)
-            if (r0 + i < r1) { store(r0 + i); step(r0 + i, X, lc[i]); }
-    } else {
-        for (int r = r0; r < r1; ++r) {
-            double l[6];
-            load(r, l);  // read before this thread overwrites the slot
-            store(r);
-            step(r, X, l);
+        for (int i = 0; i < kSeqB; ++i) {
+            const int r = r0 + i;
+            if (r >= ns) break;
+            const int j = DIR == 0 ? r : ns - 1 - r;
+            double* p = st + (int64_t)j * 6 * NL;
+            p[0] = s0;
+            p[NL] = s1;
+            p[2 * (int64_t)NL] = s2;
+            const double* A = (DIR == 1 && j == ns - 1) ? m.Alast : m.Aseg;
+            const double n0 = A[0] * s0 + A[1] * s1 + A[2] * s2 + l[i][0];
+            const double n1 = A[3] * s0 + A[4] * s1 + A[5] * s2 + l[i][1];
+            const double n2 = A[6] * s0 + A[7] * s1 + A[8] * s2 + l[i][2];
+            s0 = n0;
+            s1 = n1;
+            s2 = n2;
         }
     }
 }
@@ -558,7 +498,6 @@ template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s
     IirScanMats m;
     std::memcpy(m.Aseg, a.Aseg, sizeof(m.Aseg));
     std::memcpy(m.Alast, a.Alast, sizeof(m.Alast));
-    const dim3 sgrid((a.lines + 31) / 32, 1, a.njobs * a.batch), sblock(32, kScanG);
     const int64_t bwd_sec = (int64_t)a.njobs * a.batch * a.nseg * 6 * a.lines;
     // horizontal stage (real rows in, one output per job): stage through shared memory
     const size_t sw = (size_t)(kIirSY * a.seglen) | 1;
@@ -567,9 +506,10 @@ template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s
     if (stage) iir_fwd<T, true, true><<<grid, block, in_smem, s>>>(a);
     else if (a.real_in) iir_fwd<T, true, false><<<grid, block, 0, s>>>(a);
     else iir_fwd<T, false, false><<<grid, block, 0, s>>>(a);
-    iir_scan<0><<<sgrid, sblock, 0, s>>>(a.state, 0, a.lines, a.nseg, m);
+    const dim3 qgrid((a.lines + 63) / 64, 1, a.njobs * a.batch);
+    iir_scan_seq<0><<<qgrid, 128, 0, s>>>(a.state, 0, a.lines, a.nseg, m);
     iir_bwd<T><<<grid, block, 0, s>>>(a);
-    iir_scan<1><<<sgrid, sblock, 0, s>>>(a.state, bwd_sec, a.lines, a.nseg, m);
+    iir_scan_seq<1><<<qgrid, 128, 0, s>>>(a.state, bwd_sec, a.lines, a.nseg, m);
     if (stage) iir_out<T, true><<<grid, block, out_smem, s>>>(a);
     else iir_out<T, false><<<grid, block, 0, s>>>(a);
     return cudaGetLastError();
