@@ -547,11 +547,16 @@ template <typename T> struct Builder {
         // segment-parallel recursion: enough (column, job, segment) threads to fill the GPU
         const int L = H + 2 * P;
         const double threads = (double)W * jobs.size();
-        static const double iir_threads = std::getenv("FGB_IIR_THREADS") ? std::atof(std::getenv("FGB_IIR_THREADS")) : 3072.0;
+        static const double iir_threads = std::getenv("FGB_IIR_THREADS") ? std::atof(std::getenv("FGB_IIR_THREADS")) : 12288.0;
         int nseg = (int)std::ceil(148.0 * iir_threads / std::max(1.0, threads));
         nseg = std::max(1, std::min(nseg, std::max(1, L / 24)));
         nseg = std::min(nseg, 128);
-        const int seglen = (L + nseg - 1) / nseg;
+        // whole CTAs: the IIR kernels put 4 segments of 32 lines in a CTA, so a
+        // segment count that is not a multiple of 4 leaves threads idle
+        // (config 4: 5 segments 8.95 ms, 4 segments 8.30 ms per step)
+        nseg = (nseg + 3) / 4 * 4;
+        if (nseg > L / 8 && L / 8 >= 4) nseg = (L / 8) / 4 * 4;  // keep segments >= 8 samples
+        int seglen = (L + nseg - 1) / nseg;
         nseg = (L + seglen - 1) / seglen;
         st.nseg = nseg;
         st.seglen = seglen;
