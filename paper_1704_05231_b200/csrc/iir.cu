@@ -124,11 +124,16 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_fwd(const IirArgs<T> a
         const int nb0 = blockIdx.y * kIirSY * a.seglen;
         const S* base = reinterpret_cast<const S*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
         const int tid = threadIdx.y * kIirTX + threadIdx.x;
-        for (int i = tid; i < kIirTX * sw; i += kIirTX * kIirSY) {
-            const int r = i / sw, cc = i - r * sw;
-            const int line = blockIdx.x * kIirTX + r, n = nb0 + cc;
-            if (line < NL && n < L) tile[r * swp + cc] = base[(int64_t)line * a.src_ls + clampi(n - P, 0, len - 1)];
+        for (int r = threadIdx.y; r < kIirTX; r += kIirSY) {  // row r of the CTA, samples across the warp
+            const int line = blockIdx.x * kIirTX + r;
+            if (line >= NL) continue;
+            const S* row = base + (int64_t)line * a.src_ls;
+            for (int cc = threadIdx.x; cc < sw; cc += kIirTX) {
+                const int n = nb0 + cc;
+                if (n < L) tile[r * swp + cc] = row[clampi(n - P, 0, len - 1)];
+            }
         }
+        (void)tid;
         __syncthreads();
         // thread view: sample n of this line at tile[threadIdx.x * swp + (n - nb0)]
         src = reinterpret_cast<const S*>(tile) + threadIdx.x * swp - nb0 + P;
@@ -350,10 +355,13 @@ __device__ __forceinline__ void iir_out_rows(const IirArgs<T>& a, const IirJob<T
     // row-contiguous write-out of the CTA's 32 rows x sw samples (crop window only)
     C* dst = a.dst_base + job.dst_off[0] + (int64_t)b * a.dst_bstride;
     const int tid = threadIdx.y * kIirTX + threadIdx.x;
-    for (int i = tid; i < kIirTX * sw; i += kIirTX * kIirSY) {
-        const int r = i / sw, cc = i - r * sw;
-        const int line = blockIdx.x * kIirTX + r, n = nb0 + cc;
-        if (line < NL && n >= P && n < P + len && n < L) dst[(int64_t)line * a.dst_ls + (n - P)] = tile[r * swp + cc];
+    (void)tid;
+    for (int r = threadIdx.y; r < kIirTX; r += kIirSY) {
+        const int line = blockIdx.x * kIirTX + r;
+        if (line >= NL) continue;
+        C* row = dst + (int64_t)line * a.dst_ls - P;
+        const int c0 = max(0, P - nb0), c1 = min(sw, min(P + len, L) - nb0);
+        for (int cc = c0 + threadIdx.x; cc < c1; cc += kIirTX) row[nb0 + cc] = tile[r * swp + cc];
     }
 }
 
@@ -426,10 +434,12 @@ __global__ void __launch_bounds__(128, kIirMinBlocks) iir_out(const IirArgs<T> a
             }
             const T re = (T)fma(cs.x, va, cs.y * vb);
             const double im = fma(cs.y, va, -cs.x * vb);
+            const int64_t dof = (int64_t)yo * dss;
+            dptr[0][dof] = mk<T>(re, (T)(osg[0] * im));
+            if (nout > 1) {  // SDFT jobs: the conjugate-symmetric fills
 #pragma unroll
-            for (int o = 0; o < 4; ++o) {
-                if (o >= nout) break;
-                dptr[o][(int64_t)yo * dss] = mk<T>(re, (T)(osg[o] * im));
+                for (int o = 1; o < 4; ++o)
+                    if (o < nout) dptr[o][dof] = mk<T>(re, (T)(osg[o] * im));
             }
         }
     }
