@@ -272,3 +272,26 @@ def test_huge_image_int64_offsets(env, kn):
     assert (a - b).abs().max().item() <= 1e-5 * scale
     del out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("kn", ["fir", "iir"])
+def test_workspace_chunking_equals_unchunked(env, kn, monkeypatch):
+    """A 1 MB workspace budget forces the engine to run a batch of 5 images one
+    chunk at a time (and the IIR scratch per chunk); results are bit-identical
+    to the default budget."""
+    torch, fg, D, P = env
+    imgs = torch.from_numpy(np.random.default_rng(21).uniform(0, 1, size=(5, 88, 104)).astype(np.float32)).cuda()
+    kind = fg.ExactFIR(3.0) if kn == "fir" else fg.RecursiveIIR()
+    spec = fg.BankSpec((math.pi / 2, math.pi / 8), 8, (2.0, 8.0))
+    ref = D.BankPlan((5, 88, 104), spec, kind, "f32")
+    want = ref(imgs, ref.new_output())
+    from paper_1704_05231_b200 import _native as N
+
+    torch.cuda.synchronize()
+    N.lib.fgb_release_caches()  # plans are cached per descriptor: rebuild under the small budget
+    monkeypatch.setenv("FGB_WS_BUDGET_MB", "1")
+    small = D.BankPlan((5, 88, 104), spec, kind, "f32")
+    got = small(imgs, small.new_output())
+    torch.cuda.synchronize()
+    N.lib.fgb_release_caches()  # later tests plan under the default budget again
+    assert torch.equal(got, want)
