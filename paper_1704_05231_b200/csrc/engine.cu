@@ -19,6 +19,12 @@
 //                        bin(Mx-u,v) from conj(J_u) (sdft.py:202-203) and the
 //                        conjugate-symmetric fills (sdft.py:209-212).
 #include <cuda_runtime.h>
+//
+// Sections: errors | host coefficient math (sampled Gaussian, IIR poles,
+// pad radius) | device memory | plans (Step, Plan) and builders | descriptor
+// validation | Gabor plans | SDFT plans | execution (lanes, chunks, live
+// profile) | plan cache keys | GPU brute-force oracles | C ABI (device,
+// host-buffer with pipelined D2H, planar host, GBNK, probes).
 
 #include <algorithm>
 #include <type_traits>
