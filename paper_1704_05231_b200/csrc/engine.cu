@@ -18,16 +18,15 @@
 //                        (u, v<=My/2) column job writes bin(u,v), the mirror
 //                        bin(Mx-u,v) from conj(J_u) (sdft.py:202-203) and the
 //                        conjugate-symmetric fills (sdft.py:209-212).
-#include <cuda_runtime.h>
 //
 // Sections: errors | host coefficient math (sampled Gaussian, IIR poles,
 // pad radius) | device memory | plans (Step, Plan) and builders | descriptor
 // validation | Gabor plans | SDFT plans | execution (lanes, chunks, live
 // profile) | plan cache keys | GPU brute-force oracles | C ABI (device,
 // host-buffer with pipelined D2H, planar host, GBNK, probes).
+#include <cuda_runtime.h>
 
 #include <algorithm>
-#include <type_traits>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -37,6 +36,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/fgb200.h"
