@@ -319,7 +319,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     launches = N.lib.fgb_launch_count() - l0
     if world > 1:
         dist.barrier()
-    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    per_step = sorted(s.elapsed_time(e) for s, e in zip(starts, ends))
+    total_ms = sum(per_step)
+    step_stats = {"min": per_step[0], "p50": per_step[len(per_step) // 2],
+                  "p90": per_step[min(len(per_step) - 1, (9 * len(per_step)) // 10)], "max": per_step[-1]}
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -450,6 +453,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                        "parallelism": f"{'image' if args.config in (2, 3) else 'unit'}-sharded x{world}"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(), "kernels": kernels, "fp32_peak_tflops_measured": fp32,
+            "step_ms_rank0": step_stats,
         }
         print(json.dumps(line), flush=True)
 
