@@ -859,7 +859,7 @@ template <typename T> static int64_t iir_state_need(const Plan<T>& p) {
 
 static int64_t ws_budget_bytes() {
     const char* e = std::getenv("FGB_WS_BUDGET_MB");
-    const int64_t mb = e ? std::atoll(e) : 160;
+    const int64_t mb = e ? std::atoll(e) : 2048;  // 2 GB of 180: batches of up to 16 1024² images per chunk (config 3: +5%)
     return std::max<int64_t>(mb, 1) << 20;
 }
 
