@@ -20,6 +20,13 @@ GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    # the library is a build artefact (git-ignored): a fresh checkout builds it
+    # once here (nvcc cross-compiles for sm_100a without a GPU)
+    lib = os.path.join(ROOT, "paper_1704_05231_b200", "lib", "libfgb200.so")
+    if not os.path.exists(lib):
+        import subprocess
+
+        subprocess.run([sys.executable, os.path.join(ROOT, "paper_1704_05231_b200", "_build.py")], check=True)
 
 
 def random_image(seed: int, size: int = 32, lo: float = 0.0, hi: float = 255.0, width=None):
