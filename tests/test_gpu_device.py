@@ -295,3 +295,33 @@ def test_workspace_chunking_equals_unchunked(env, kn, monkeypatch):
     torch.cuda.synchronize()
     N.lib.fgb_release_caches()  # later tests plan under the default budget again
     assert torch.equal(got, want)
+
+
+def test_randomized_sweep_f32(env):
+    """Seeded random f32 banks and SDFTs at sizes that take the fast paths (fused
+    small-sigma kernel, FFMA2 row / column kernels, fused SDFT, IIR) vs the
+    float64 oracle at 1e-5."""
+    torch, fg, D, P = env
+    rng = np.random.default_rng(77)
+    for case in range(10):
+        h, w = int(rng.integers(64, 260)), int(rng.integers(64, 260))
+        f = rng.uniform(0.0, 1.0, size=(h, w)).astype(np.float32)
+        f64 = f.astype(np.float64)
+        iir = case % 3 == 2
+        k, ok = (fg.RecursiveIIR(), ("iir",)) if iir else (fg.ExactFIR(3.0), ("fir", 3.0))
+        nf = int(rng.integers(1, 4))
+        freqs = tuple(float(x) for x in rng.uniform(0.2, 2.5, size=nf))
+        sig = tuple(float(x) for x in rng.uniform(0.8, 6.0, size=nf))
+        n = int(rng.integers(2, 10))
+        out = fg.compute_bank(fg.RealImage.from_array(f), fg.BankSpec(freqs, n, sig), k, fg.OpCounters(),
+                              precision="f32")
+        ref = O.compute_bank(f64, freqs, n, sig, ok)
+        for e, ((p, img), r) in enumerate(zip(out.entries, ref)):
+            assert max_rel_err(img, r[3:]) <= 1e-5, (case, h, w, n, e, freqs, sig)
+        m = int(rng.choice([4, 8, 16]))
+        spec = fg.SdftSpec(m, m, k, float(rng.uniform(1.0, 4.0)))
+        sd = fg.sdft_full(fg.RealImage.from_array(f), spec, fg.OpCounters(), precision="f32")
+        sref = O.sdft_full(f64, m, m, ok, spec.sigma)
+        for u in range(m):
+            for v in range(m):
+                assert max_rel_err(sd.bins[u][v], sref[u][v]) <= 1e-5, (case, h, w, m, u, v)
