@@ -175,3 +175,25 @@ def test_config2_full_iir_f32(fg):
                                        O.vertical_stage(jr, ji, om, 3 * math.pi / 8, s, ("iir",), conjugate=True)))
         worst = max(worst, max_rel_err(out.entries[i * 8 + 4][1], O.gabor_filter(f, om, math.pi / 2, s, ("iir",))))
     assert worst <= TOL32, worst
+
+
+def test_config2_full_f64_validation_build(fg):
+    """The fp64 validation build at config 2's full size: every frequency's
+    direct / mirror pair and theta = pi/2 vs the float64 oracle at 1e-10."""
+    import scipy.ndimage as ndi
+
+    f64 = np.random.default_rng(1).uniform(0.0, 1.0, size=(1024, 1024)).astype(np.float32).astype(np.float64)
+    f = ndi.uniform_filter(f64, size=5, mode="nearest").astype(np.float32).astype(np.float64)
+    freqs = (math.pi / 2, math.pi / 4, math.pi / 8, math.pi / 16)
+    sig = (2.0, 4.0, 8.0, 16.0)
+    out = fg.compute_bank(fg.RealImage.from_array(f), fg.BankSpec(freqs, 8, sig), fg.ExactFIR(3.0),
+                          fg.OpCounters(), precision="f64")
+    worst = 0.0
+    for i, (om, s) in enumerate(zip(freqs, sig)):
+        jr, ji = O.horizontal_stage(f, om, 3 * math.pi / 8, s, ("fir", 3.0))
+        worst = max(worst, max_rel_err(out.entries[i * 8 + 3][1], O.vertical_stage(jr, ji, om, 3 * math.pi / 8, s,
+                                                                                   ("fir", 3.0))))
+        worst = max(worst, max_rel_err(out.entries[i * 8 + 5][1], O.vertical_stage(jr, ji, om, 3 * math.pi / 8, s,
+                                                                                   ("fir", 3.0), conjugate=True)))
+        worst = max(worst, max_rel_err(out.entries[i * 8 + 4][1], O.gabor_filter(f, om, math.pi / 2, s, ("fir", 3.0))))
+    assert worst <= TOL64, worst
