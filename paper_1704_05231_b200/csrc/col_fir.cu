@@ -14,15 +14,22 @@
 //    bin(M-u,v) = P conj(X), and the conjugate-filled bins conj(P) conj(Y),
 //    conj(P) X are written from the same registers.
 //
-// Layout: CTA = 32 columns x G row-groups x one segment of S rows of one
-// job; each thread owns one column and R consecutive rows per TY = G*R row
-// chunk.  The segment's (S + nt - 1)-row tile (rows clamped = replicate pad,
+// Layout (both variants): a CTA owns a column tile x one segment of S rows of
+// one job.  The segment's (S + nt - 1)-row tile (rows clamped = replicate pad,
 // or zeroed for the box window) is requested up front with cp.async, one
-// commit group per chunk, so chunk i computes while chunks > i stream in and
-// the 2h halo is fetched once per segment.  Taps run in chunks of R with a
-// (2R-1)-deep register window: every J load feeds 4R FFMAs and each
-// (ka, kb) tap pair is one broadcast LDS.  REM = nt % R is a template
-// parameter so no taps are padded.
+// commit group per chunk of rows, so chunk i computes while chunks > i stream
+// in and the 2h halo is fetched once per segment.  Taps run in chunks of R
+// with a (2R-1)-deep register window; REM = nt % R is a template parameter so
+// no taps are padded.  Tap tables travel in the kernel parameters (constant
+// bank -> uniform-register operands) when they fit, else in shared memory.
+//  * col_kernel2 (fp32, even widths): two adjacent columns per thread (16-byte
+//    cp.async / LDS.128 / STG.128), 8 rows per thread, packed FFMA2
+//    accumulation (A and B of both columns: 4 FFMA2 per tap and row); CTA =
+//    16 or 32 columns (CP = 8 / 16 column pairs) x 4 warps.
+//  * col_kernel (fp64 validation build, odd widths): one column per thread,
+//    scalar FMAs, CTA = 32 columns x G row groups.
+//  * col_kernel_gmem: supports beyond shared memory (sigma 50 at radius 6).
+// launch_col picks the variant, tile width and S with a small cost model.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
