@@ -9,7 +9,10 @@
 // kernel needs no per-pixel trig and no large-phase fp32 products.  The
 // Gaussian is even, so taps t and -t share one add/sub of the input pair,
 // and every direct orientation of one frequency (up to kMaxND per launch)
-// shares those adds:  per tap pair 2 FADD + 2*ND FFMA instead of 4*ND FFMA.
+// shares those adds:  per tap pair 2 FADD + 2*ND FFMA instead of 4*ND FFMA
+// (fp32: one packed FFMA2 (Jr, Ji) += (kr, ki) * (f+ + f-, f+ - f-) per
+// orientation; the (kr, ki) pairs come from the kernel-parameter bank as
+// uniform-register operands).
 //
 // Layout: CTA = 64 x 4 threads, each thread R=4 consecutive outputs of one
 // row (256 px per CTA row).  The clamped row segment lives in shared memory
