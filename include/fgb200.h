@@ -126,6 +126,12 @@ int32_t fgb_iir_coeffs(double sigma, double out_b_a1_a2_a3[4]);
 int64_t fgb_bank_entries(const fgb_bank_desc* d);
 int64_t fgb_sdft_bins(const fgb_sdft_desc* d);
 
+/* Device workspace (bytes) the library allocates for such a call (J planes,
+ * IIR scratch, segment states for one chunk of images; grow-only, kept
+ * across calls).  Builds and caches the call's plan; needs a CUDA device. */
+int64_t fgb_bank_workspace_bytes(const fgb_bank_desc* d);
+int64_t fgb_sdft_workspace_bytes(const fgb_sdft_desc* d);
+
 /* ---- device-pointer entry points (stream ordered, async) --------------- */
 int32_t fgb_bank(const fgb_bank_desc* d, const void* img, void* out, void* stream);
 int32_t fgb_filter(const fgb_filter_desc* d, const void* img, void* out, void* stream);

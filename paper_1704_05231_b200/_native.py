@@ -102,6 +102,8 @@ _SIGS = {
     "fgb_iir_coeffs": (C.c_int32, [C.c_double, _P(C.c_double)]),
     "fgb_bank_entries": (C.c_int64, [_P(fgb_bank_desc)]),
     "fgb_sdft_bins": (C.c_int64, [_P(fgb_sdft_desc)]),
+    "fgb_bank_workspace_bytes": (C.c_int64, [_P(fgb_bank_desc)]),
+    "fgb_sdft_workspace_bytes": (C.c_int64, [_P(fgb_sdft_desc)]),
     "fgb_bank": (C.c_int32, [_P(fgb_bank_desc), _vp, _vp, _vp]),
     "fgb_filter": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp, _vp]),
     "fgb_horizontal_stage": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp, _vp]),

@@ -941,7 +941,7 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
         ++li;
     }
     p.nlanes = NL;
-    p.ws_img_c = std::max(need, NL * lane_stride);
+    p.ws_img_c = need;  // lanes whose frequency runs fused (no J planes) reserve nothing
     finish_chunking(p, d.img.batch);
     return p.upload();
 }
@@ -1360,6 +1360,16 @@ static Ctx& ctx() {
     return *c;
 }
 
+// Device workspace a call of this plan needs (J planes, IIR scratch and
+// segment states for one chunk of images); the library keeps it grow-only.
+template <typename T> static int64_t plan_ws_bytes(const Plan<T>& p, int batch) {
+    const int chunk = std::min(p.chunk, batch);
+    const int64_t ws_img_bytes = p.ws_img_c * (int64_t)sizeof(cx_t<T>);
+    const int64_t scr_bytes = p.scratch_img_t * (int64_t)sizeof(T);
+    const int64_t stt_bytes = (p.state_img_d * (int64_t)sizeof(double) + 255) / 256 * 256;
+    return (ws_img_bytes + scr_bytes + stt_bytes) * chunk + 512;
+}
+
 template <typename T>
 static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img, void* out, cudaStream_t s) {
     using C = cx_t<T>;
@@ -1367,8 +1377,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     const int chunk = std::min(p.chunk, batch);
     const int64_t ws_img_bytes = p.ws_img_c * (int64_t)sizeof(C);
     const int64_t scr_bytes = p.scratch_img_t * (int64_t)sizeof(T);
-    const int64_t stt_bytes = (p.state_img_d * (int64_t)sizeof(double) + 255) / 256 * 256;
-    FGB_TRY(cx.ws.ensure((size_t)(ws_img_bytes + scr_bytes + stt_bytes) * chunk + 512));
+    FGB_TRY(cx.ws.ensure((size_t)plan_ws_bytes(p, batch)));
     C* ws = (C*)cx.ws.p;
     T* scratch = (T*)((char*)cx.ws.p + ws_img_bytes * chunk);
     const int64_t scratch_lane = p.scratch_img_t / std::max(1, p.nlanes) * chunk;
@@ -1631,7 +1640,7 @@ static int32_t validate_bank(const fgb_bank_desc* d) {
     return FGB_OK;
 }
 
-template <typename T> static int32_t bank_t(const fgb_bank_desc* d, const void* img, void* out, cudaStream_t s) {
+template <typename T> static int32_t bank_plan(const fgb_bank_desc* d, Plan<T>** p) {
     std::ostringstream k;
     k.precision(17);
     k << "bank|";
@@ -1641,10 +1650,13 @@ template <typename T> static int32_t bank_t(const fgb_bank_desc* d, const void* 
     for (int i = 0; i < d->n_freq; ++i) k << d->omegas[i] << ',' << d->sigmas[i] << ';';
     if (d->units)
         for (int i = 0; i < d->n_units; ++i) k << 'u' << d->units[i];
-    Ctx& cx = ctx();
+    return get_plan<T>(ctx(), k.str(), [&](Plan<T>& pl) { return build_bank<T>(pl, *d); }, p);
+}
+
+template <typename T> static int32_t bank_t(const fgb_bank_desc* d, const void* img, void* out, cudaStream_t s) {
     Plan<T>* p;
-    FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_bank<T>(pl, *d); }, &p));
-    return execute<T>(*p, cx, d->img, img, out, s);
+    FGB_TRY(bank_plan<T>(d, &p));
+    return execute<T>(*p, ctx(), d->img, img, out, s);
 }
 
 static int32_t validate_filter(const fgb_filter_desc* d, bool complex_in) {
@@ -1677,8 +1689,7 @@ static int32_t validate_sdft(const fgb_sdft_desc* d) {
     return check_smoother(d->smoother, sdft_sigma(*d));
 }
 
-template <typename T>
-static int32_t sdft_t(const fgb_sdft_desc* d, int u, int v, const void* img, void* out, cudaStream_t s) {
+template <typename T> static int32_t sdft_plan(const fgb_sdft_desc* d, int u, int v, Plan<T>** pp) {
     std::ostringstream k;
     k.precision(17);
     k << "sdft|" << u << ',' << v << '|';
@@ -1688,13 +1699,15 @@ static int32_t sdft_t(const fgb_sdft_desc* d, int u, int v, const void* img, voi
     if (d->u_heads)
         for (int i = 0; i < d->n_heads; ++i) k << 'h' << d->u_heads[i];
     Ctx& cx = ctx();
+    if (u < 0) return get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_sdft<T>(pl, *d); }, pp);
+    return get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_sdft_single<T>(pl, *d, u, v); }, pp);
+}
+
+template <typename T>
+static int32_t sdft_t(const fgb_sdft_desc* d, int u, int v, const void* img, void* out, cudaStream_t s) {
     Plan<T>* p;
-    if (u < 0) {
-        FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_sdft<T>(pl, *d); }, &p));
-    } else {
-        FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_sdft_single<T>(pl, *d, u, v); }, &p));
-    }
-    return execute<T>(*p, cx, d->img, img, out, s);
+    FGB_TRY(sdft_plan<T>(d, u, v, &p));
+    return execute<T>(*p, ctx(), d->img, img, out, s);
 }
 
 // ===========================================================================
@@ -1899,6 +1912,32 @@ int64_t fgb_sdft_bins(const fgb_sdft_desc* d) {
     int32_t r = make_binmap(*d, &bm);
     if (r != FGB_OK) return r;
     return bm.nbins;
+}
+
+int64_t fgb_bank_workspace_bytes(const fgb_bank_desc* d) {
+    FGB_TRY(validate_bank(d));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (d->img.dtype == FGB_F32) {
+        Plan<float>* p;
+        FGB_TRY(bank_plan<float>(d, &p));
+        return plan_ws_bytes(*p, d->img.batch);
+    }
+    Plan<double>* p;
+    FGB_TRY(bank_plan<double>(d, &p));
+    return plan_ws_bytes(*p, d->img.batch);
+}
+
+int64_t fgb_sdft_workspace_bytes(const fgb_sdft_desc* d) {
+    FGB_TRY(validate_sdft(d));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (d->img.dtype == FGB_F32) {
+        Plan<float>* p;
+        FGB_TRY(sdft_plan<float>(d, -1, -1, &p));
+        return plan_ws_bytes(*p, d->img.batch);
+    }
+    Plan<double>* p;
+    FGB_TRY(sdft_plan<double>(d, -1, -1, &p));
+    return plan_ws_bytes(*p, d->img.batch);
 }
 
 int32_t fgb_bank(const fgb_bank_desc* d, const void* img, void* out, void* stream) {

@@ -57,6 +57,11 @@ class BankPlan:
         b, h, w = self.shape
         return torch.empty((b, self.entries, h, w), dtype=_cplx(self.prec), device=device)
 
+    @property
+    def workspace_bytes(self) -> int:
+        """Device workspace the library keeps for this call (J planes, IIR scratch)."""
+        return int(N.check(N.lib.fgb_bank_workspace_bytes(C.byref(self.desc))))
+
     def __call__(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         img = _check_img(img)
         if tuple(img.shape) != self.shape:
@@ -85,6 +90,11 @@ class SdftPlan:
     def new_output(self, device="cuda") -> torch.Tensor:
         b, h, w = self.shape
         return torch.empty((b, self.bins, h, w), dtype=_cplx(self.prec), device=device)
+
+    @property
+    def workspace_bytes(self) -> int:
+        """Device workspace the library keeps for this call (J planes, IIR scratch)."""
+        return int(N.check(N.lib.fgb_sdft_workspace_bytes(C.byref(self.desc))))
 
     def __call__(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         img = _check_img(img)

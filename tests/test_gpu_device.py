@@ -325,3 +325,24 @@ def test_randomized_sweep_f32(env):
         for u in range(m):
             for v in range(m):
                 assert max_rel_err(sd.bins[u][v], sref[u][v]) <= 1e-5, (case, h, w, m, u, v)
+
+
+def test_workspace_bytes_query(env):
+    """fgb_*_workspace_bytes: the fused small-sigma frequency needs no J planes,
+    the FIR bank of config 2 keeps one J plane set per lane, the fused SDFT
+    none, the IIR adds scratch; the numbers bound what the call allocates."""
+    torch, fg, D, P = env
+    hw = 1024 * 1024
+    fused = D.BankPlan((1, 1024, 1024), fg.BankSpec((math.pi / 2,), 8, (2.0,)), fg.ExactFIR(3.0), "f32")
+    assert fused.workspace_bytes < 4096
+    cfg2 = D.BankPlan((1, 1024, 1024), fg.BankSpec((math.pi / 2, math.pi / 4, math.pi / 8, math.pi / 16), 8,
+                                                  (2.0, 4.0, 8.0, 16.0)), fg.ExactFIR(3.0), "f32")
+    assert 3 * 5 * hw * 8 <= cfg2.workspace_bytes <= 4 * 5 * hw * 8 + 4096  # J of the 3 non-fused lanes
+    sd = D.SdftPlan((1, 512, 512), fg.SdftSpec(16, 16, fg.ExactFIR(3.0), 4.0), "f32")
+    assert sd.workspace_bytes < 4096
+    iir = D.BankPlan((1, 256, 256), fg.BankSpec((math.pi / 4,), 8, (4.0,)), fg.RecursiveIIR(), "f32")
+    assert iir.workspace_bytes > 5 * 256 * 256 * 8
+    before = torch.cuda.memory_allocated()
+    out = cfg2(torch.rand(1, 1024, 1024, device="cuda"), cfg2.new_output())
+    torch.cuda.synchronize()
+    assert out.shape[1] == 32 and torch.cuda.memory_allocated() >= before  # torch's pool is separate
