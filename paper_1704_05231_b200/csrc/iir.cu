@@ -52,11 +52,6 @@ struct IirScanMats {
 };
 
 
-__device__ __forceinline__ void mat3_apply(const double* A, const double* s, double* o) {
-    o[0] = A[0] * s[0] + A[1] * s[1] + A[2] * s[2];
-    o[1] = A[3] * s[0] + A[4] * s[1] + A[5] * s[2];
-    o[2] = A[6] * s[0] + A[7] * s[1] + A[8] * s[2];
-}
 
 // Recursion step writing y[n] into the slot that held y[n-3]: with three
 // named registers whose roles rotate every sample, a 3x unrolled loop needs
