@@ -1431,7 +1431,8 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                 *bs = img_bs;
                 return imgb + r.off;
             }
-            // SEL_WSR: real plane inside ws (dense)
+            // SEL_WSR: real plane inside ws (dense; the caller sets the row length)
+            *pitch = 0;
             *bs = 2 * p.ws_img_c;
             return (const T*)ws + r.off;
         };
@@ -1654,7 +1655,7 @@ template <typename T> static int32_t bank_plan(const fgb_bank_desc* d, Plan<T>**
 }
 
 template <typename T> static int32_t bank_t(const fgb_bank_desc* d, const void* img, void* out, cudaStream_t s) {
-    Plan<T>* p;
+    Plan<T>* p = nullptr;
     FGB_TRY(bank_plan<T>(d, &p));
     return execute<T>(*p, ctx(), d->img, img, out, s);
 }
@@ -1676,7 +1677,7 @@ static int32_t filter_t(const fgb_filter_desc* d, int mode, const void* img, voi
     key_sm(k, d->smoother);
     k << d->omega << ',' << d->theta << ',' << d->sigma << '|' << d->img.batch;
     Ctx& cx = ctx();
-    Plan<T>* p;
+    Plan<T>* p = nullptr;
     FGB_TRY(get_plan<T>(cx, k.str(), [&](Plan<T>& pl) { return build_filter<T>(pl, *d, mode); }, &p));
     return execute<T>(*p, cx, d->img, img, out, s);
 }
@@ -1705,7 +1706,7 @@ template <typename T> static int32_t sdft_plan(const fgb_sdft_desc* d, int u, in
 
 template <typename T>
 static int32_t sdft_t(const fgb_sdft_desc* d, int u, int v, const void* img, void* out, cudaStream_t s) {
-    Plan<T>* p;
+    Plan<T>* p = nullptr;
     FGB_TRY(sdft_plan<T>(d, u, v, &p));
     return execute<T>(*p, ctx(), d->img, img, out, s);
 }
@@ -1918,11 +1919,11 @@ int64_t fgb_bank_workspace_bytes(const fgb_bank_desc* d) {
     FGB_TRY(validate_bank(d));
     std::lock_guard<std::mutex> lk(g_mu);
     if (d->img.dtype == FGB_F32) {
-        Plan<float>* p;
+        Plan<float>* p = nullptr;
         FGB_TRY(bank_plan<float>(d, &p));
         return plan_ws_bytes(*p, d->img.batch);
     }
-    Plan<double>* p;
+    Plan<double>* p = nullptr;
     FGB_TRY(bank_plan<double>(d, &p));
     return plan_ws_bytes(*p, d->img.batch);
 }
@@ -1931,11 +1932,11 @@ int64_t fgb_sdft_workspace_bytes(const fgb_sdft_desc* d) {
     FGB_TRY(validate_sdft(d));
     std::lock_guard<std::mutex> lk(g_mu);
     if (d->img.dtype == FGB_F32) {
-        Plan<float>* p;
+        Plan<float>* p = nullptr;
         FGB_TRY(sdft_plan<float>(d, -1, -1, &p));
         return plan_ws_bytes(*p, d->img.batch);
     }
-    Plan<double>* p;
+    Plan<double>* p = nullptr;
     FGB_TRY(sdft_plan<double>(d, -1, -1, &p));
     return plan_ws_bytes(*p, d->img.batch);
 }

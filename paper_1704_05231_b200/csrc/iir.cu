@@ -44,7 +44,6 @@ namespace {
 constexpr int kIirTX = 32;  // lines per block (one warp)
 constexpr int kIirSY = 4;   // segments per block
 constexpr int kIirMinBlocks = 8;  // 64 registers: more resident warps for the latency-bound passes
-constexpr int kIirU = 3;    // samples per load batch (forward pass)
 constexpr int kIirUB = 3;   // scratch samples per load batch (backward / output passes)
 
 struct IirScanMats {
