@@ -114,7 +114,6 @@ def sharded_bank(img, spec, kind, group=None, compute=None, radius: float = 3.0)
     ``compute(img, spec, kind, units)`` defaults to the device path
     (paper_1704_05231_b200.device.compute_bank); tests inject a CPU stand-in.
     """
-    import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1

@@ -59,8 +59,6 @@ def test_sdft_fused_matches_separable_and_oracle(env, m, sigma, radius):
     fused = D.sdft_full(f, spec)[0].cpu().numpy()
     os.environ["FGB_SDFT_UNFUSED"] = "1"
     try:
-        import ctypes
-
         from paper_1704_05231_b200 import _native as N
 
         N.lib.fgb_release_caches()

@@ -1,4 +1,4 @@
-import time, math, sys
+import time, sys
 sys.path.insert(0, '.')
 import numpy as np
 import bench

@@ -1,4 +1,4 @@
-import time, math, sys, ctypes as C
+import time, sys, ctypes as C
 sys.path.insert(0, '.')
 import numpy as np
 import bench

@@ -1,4 +1,4 @@
-import torch, time
+import torch
 x = torch.empty(8 << 30, dtype=torch.uint8, device="cuda")
 for _ in range(3): x.zero_()
 torch.cuda.synchronize()
