@@ -18,6 +18,7 @@
 // row (256 px per CTA row).  The clamped row segment lives in shared memory
 // split into R residue sub-arrays (element i at (i%R)*S + i/R) so the
 // stride-R register windows load conflict-free with immediate offsets.
+#include <cstdint>
 #include <cstring>
 
 #include "common.cuh"
@@ -44,6 +45,13 @@ template <typename T> __host__ __device__ inline int row_sub_len(int need) {
     return s;
 }
 
+// fp32 row pitch: room for the 16-byte window reads past the segment end,
+// a multiple of 4 floats (16-byte aligned rows).
+__host__ __device__ inline int row_vec_pitch(int nseg) { return (nseg + 4 + 3) / 4 * 4; }
+// Vector windows for fp32 up to 6 orientations per launch (measured: config 2 / 3
+// +1-2%; at 8 orientations the extra live registers made config 5's rows 27% slower).
+template <typename T> __host__ __device__ constexpr bool row_vec(int nd) { return sizeof(T) == 4 && nd <= 6; }
+
 // CAP > 0: the group's tap table travels in the kernel parameters (constant
 // bank) so the FFMA multipliers are uniform-register operands; CAP == 0:
 // table staged in shared memory.
@@ -57,9 +65,14 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* wsm = reinterpret_cast<T*>(smem_raw);  // [(hp+1)][NDP][2]
     const int hp = a.hp;
+    // fp32: each CTA row is contiguous (pitch S4, 16-byte aligned) and the
+    // windows are read as 16-byte vectors; fp64: R residue sub-arrays of
+    // length S (element i at (i%R)*S + i/R) so scalar windows are conflict-free
+    constexpr bool VEC = row_vec<T>(ND);
     const int nseg = kRowSpan + 2 * hp;
     const int S = row_sub_len<T>((nseg + R - 1) / R);
-    T* rows = CAP > 0 ? wsm : wsm + (size_t)(hp + 1) * NDP * 2;  // [kRowTY][R][S]
+    const int S4 = row_vec_pitch(nseg);
+    T* rows = CAP > 0 ? wsm : wsm + (size_t)(hp + 1) * NDP * 2;  // [kRowTY][R][S] or [kRowTY][S4]
     auto W = [&](int i) -> T { if constexpr (CAP > 0) return pw.w[i]; else return wsm[i]; };
 
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -76,12 +89,23 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
         const int n = (hp + 1) * NDP * 2 / per16;
         for (int i = tid; i < n; i += kRowTX * kRowTY) cp_async16(wsm + i * per16, wg + i * per16);
     }
-    T* my = rows + (size_t)ty * R * S;
+    T* my = rows + (size_t)ty * (VEC ? S4 : R * S);
     if (y < a.H) {
         const T* src = a.img + (size_t)b * a.img_bstride + (size_t)y * a.pitch;
-        for (int i = tx; i < nseg; i += kRowTX) {
-            int x = clampi(x0 - hp + i, 0, a.W - 1);
-            cp_async<sizeof(T)>(my + (i % R) * S + i / R, src + x);
+        if constexpr (VEC) {
+            // interior rows with a 16-byte aligned source: 16-byte copies
+            const int xs = x0 - hp;
+            const bool inner = xs >= 0 && xs + nseg <= a.W && ((reinterpret_cast<uintptr_t>(src + xs) & 15) == 0);
+            if (inner) {
+                for (int i = 4 * tx; i < nseg; i += 4 * kRowTX) cp_async16(my + i, src + xs + i);
+            } else {
+                for (int i = tx; i < nseg; i += kRowTX) cp_async<sizeof(T)>(my + i, src + clampi(xs + i, 0, a.W - 1));
+            }
+        } else {
+            for (int i = tx; i < nseg; i += kRowTX) {
+                int x = clampi(x0 - hp + i, 0, a.W - 1);
+                cp_async<sizeof(T)>(my + (i % R) * S + i / R, src + x);
+            }
         }
     }
     cp_async_wait_all();
@@ -91,14 +115,20 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
     // accumulators (Jr, Ji) per orientation and output: one FFMA2 (fp32) per
     // orientation per tap pair: (Jr, Ji) += (kr, ki) * (f[x+t] + f[x-t], f[x+t] - f[x-t])
     C acc[ND][R];
-    // centre tap t = 0: sub-array r, index tx + hp/R
+    // centre tap t = 0: element R*tx + hp + r
     {
-        const int base = tx + hp / R;
+        T cv[R];
+        if constexpr (VEC) {
+            const float4 c4 = *reinterpret_cast<const float4*>(my + R * tx + hp);
+            cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) cv[r] = my[r * S + tx + hp / R];
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            T v = my[r * S + base];
 #pragma unroll
-            for (int k = 0; k < ND; ++k) acc[k][r] = mk<T>(W(k * 2) * v, T(0));
+            for (int k = 0; k < ND; ++k) acc[k][r] = mk<T>(W(k * 2) * cv[r], T(0));
         }
     }
     const int nch = hp / R;
@@ -106,13 +136,22 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
     for (int c = 0; c < nch; ++c) {
         // right window: f[x + r + t], t = 1 + cR + tt  ->  q = r + tt in [0, 2R-2]
         // left  window: f[x + r - t]                    ->  q' = r - tt + R - 1
+        // right window element R*tx + hp + R*c + 1 + q, left R*tx + hp - R*c - R + q
         T rv[2 * R - 1], lv[2 * R - 1];
-        const int rb = tx + hp / R + c;
-        const int lb = tx + hp / R - c - 1;
+        if constexpr (VEC) {
+            const float4* r4 = reinterpret_cast<const float4*>(my + R * tx + hp + R * c);
+            const float4* l4 = reinterpret_cast<const float4*>(my + R * tx + hp - R * c - R);
+            const float4 ra = r4[0], rb4 = r4[1], la = l4[0], lb4 = l4[1];
+            rv[0] = ra.y; rv[1] = ra.z; rv[2] = ra.w; rv[3] = rb4.x; rv[4] = rb4.y; rv[5] = rb4.z; rv[6] = rb4.w;
+            lv[0] = la.x; lv[1] = la.y; lv[2] = la.z; lv[3] = la.w; lv[4] = lb4.x; lv[5] = lb4.y; lv[6] = lb4.z;
+        } else {
+            const int rb = tx + hp / R + c;
+            const int lb = tx + hp / R - c - 1;
 #pragma unroll
-        for (int q = 0; q < 2 * R - 1; ++q) {
-            rv[q] = my[((1 + q) % R) * S + rb + (1 + q) / R];
-            lv[q] = my[(q % R) * S + lb + q / R];
+            for (int q = 0; q < 2 * R - 1; ++q) {
+                rv[q] = my[((1 + q) % R) * S + rb + (1 + q) / R];
+                lv[q] = my[(q % R) * S + lb + q / R];
+            }
         }
 #pragma unroll
         for (int tt = 0; tt < R; ++tt) {
@@ -188,7 +227,8 @@ template <typename T> size_t row_sym_smem(int hp, int nd, bool taps_in_smem) {
     const int ndp = (nd + 1) & ~1;
     const int nseg = kRowSpan + 2 * hp;
     const int S = row_sub_len<T>((nseg + kRowR - 1) / kRowR);
-    return sizeof(T) * ((taps_in_smem ? (size_t)(hp + 1) * ndp * 2 : 0) + (size_t)kRowTY * kRowR * S);
+    const size_t rows = row_vec<T>(nd) ? (size_t)kRowTY * row_vec_pitch(nseg) : (size_t)kRowTY * kRowR * S;
+    return sizeof(T) * ((taps_in_smem ? (size_t)(hp + 1) * ndp * 2 : 0) + rows);
 }
 
 template <typename T> int row_sym_pad(int h) { return (h + kRowR - 1) / kRowR * kRowR; }
