@@ -341,7 +341,7 @@ template <typename T> struct Plan : PlanBase {
     std::vector<int32_t> ints;
     std::vector<double> dbls;
     DevBuf blob;
-    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0, off_ints = 0, off_dbls = 0;
+    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0, off_tabs32 = 0, off_ints = 0, off_dbls = 0;
     // workspace per image (bytes), scratch (T elements per image-chunk) and chunking
     int64_t ws_img_c = 0;         // complex elements per image
     int64_t scratch_img_t = 0;    // T elements per image (IIR scratch)
@@ -359,6 +359,7 @@ template <typename T> struct Plan : PlanBase {
         off_cjobs = o; o = al(o + cjobs.size() * sizeof(ColJob<T>));
         off_ijobs = o; o = al(o + ijobs.size() * sizeof(IirJob<T>));
         off_tabs = o; o = al(o + tabs.size() * sizeof(double2));
+        off_tabs32 = o; o = al(o + tabs.size() * sizeof(float2));
         off_ints = o; o = al(o + ints.size() * sizeof(int32_t));
         off_dbls = o; o = al(o + dbls.size() * sizeof(double));
         FGB_TRY(blob.ensure(std::max<size_t>(o, 256)));
@@ -368,6 +369,10 @@ template <typename T> struct Plan : PlanBase {
         if (!cjobs.empty()) std::memcpy(h.data() + off_cjobs, cjobs.data(), cjobs.size() * sizeof(ColJob<T>));
         if (!ijobs.empty()) std::memcpy(h.data() + off_ijobs, ijobs.data(), ijobs.size() * sizeof(IirJob<T>));
         if (!tabs.empty()) std::memcpy(h.data() + off_tabs, tabs.data(), tabs.size() * sizeof(double2));
+        for (size_t i = 0; i < tabs.size(); ++i) {  // fp32 copy (each value rounded once from the fp64 table)
+            const float2 v = make_float2((float)tabs[i].x, (float)tabs[i].y);
+            std::memcpy(h.data() + off_tabs32 + i * sizeof(float2), &v, sizeof(v));
+        }
         if (!ints.empty()) std::memcpy(h.data() + off_ints, ints.data(), ints.size() * sizeof(int32_t));
         if (!dbls.empty()) std::memcpy(h.data() + off_dbls, dbls.data(), dbls.size() * sizeof(double));
         FGB_CUDA(cudaMemcpy(blob.p, h.data(), o, cudaMemcpyHostToDevice));
@@ -378,6 +383,7 @@ template <typename T> struct Plan : PlanBase {
     const ColJob<T>* d_cjobs() const { return (const ColJob<T>*)((char*)blob.p + off_cjobs); }
     const IirJob<T>* d_ijobs() const { return (const IirJob<T>*)((char*)blob.p + off_ijobs); }
     const double2* d_tabs() const { return (const double2*)((char*)blob.p + off_tabs); }
+    const float2* d_tabs32() const { return (const float2*)((char*)blob.p + off_tabs32); }
     const int32_t* d_ints() const { return (const int32_t*)((char*)blob.p + off_ints); }
     const double* d_dbls() const { return (const double*)((char*)blob.p + off_dbls); }
 };
@@ -564,6 +570,10 @@ template <typename T> struct Builder {
         if (nseg > L / 8 && L / 8 >= 4) nseg = (L / 8) / 4 * 4;  // keep segments >= 8 samples
         int seglen = (L + nseg - 1) / nseg;
         nseg = (L + seglen - 1) / seglen;
+        if (sizeof(T) == 4 && iir32_enabled()) {  // iir32.cu: fixed register-window segments
+            seglen = kIir32M;
+            nseg = (L + seglen - 1) / seglen;
+        }
         st.nseg = nseg;
         st.seglen = seglen;
         // companion matrix A, g_m = first row of A^(m+1), A^seglen, A^last
@@ -1448,7 +1458,8 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                 pr.e1 = pool_event();
                 cudaEventRecord(pr.e0, s);
             }
-            g_launches += st.kind == ST_IIR ? 5 : 1;  // kernels per step: IIR = fwd, scan, bwd, scan, out
+            // kernels per step: IIR = sum, carry, fin (fp32 parallel form) or fwd, scan, bwd, scan, out
+            g_launches += st.kind == ST_IIR ? ((sizeof(T) == 4 && iir32_enabled()) ? 3 : 5) : 1;
             switch (st.kind) {
                 case ST_ROW: {
                     RowArgs<T> a{};
@@ -1523,6 +1534,13 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     if ((int64_t)iir_scratch_elems<T>(st.H, st.W, st.P, st.njobs, nb) > scratch_lane)
                         return fail(FGB_EINVAL, "internal: IIR scratch too small");
                     a.g = p.d_dbls() + st.g_off;
+                    a.tab32 = p.d_tabs32();
+                    if constexpr (sizeof(T) == 4) {
+                        if (iir32_enabled()) {
+                            FGB_CUDA(launch_iir32(a, s));
+                            break;
+                        }
+                    }
                     FGB_CUDA(launch_iir<T>(a, s));
                     break;
                 }

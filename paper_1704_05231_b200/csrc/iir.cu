@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(128) iir_scan_seq(double* state, int64_t sec_o
 }  // namespace
 
 template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch) {
+    if (sizeof(T) == 4 && iir32_enabled()) return 0;  // iir32.cu keeps no sequences
     return (size_t)njobs * batch * 2 * (size_t)(len + 2 * P) * lines;
 }
 

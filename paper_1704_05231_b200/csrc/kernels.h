@@ -118,6 +118,8 @@ template <typename T> struct IirArgs {
     T* scratch;              // [njobs*batch][2][len+2P][lines] local forward / backward sequences
     double* state;           // [2][njobs*batch][nseg][2 planes][3][lines] segment boundary states
     const double* g;         // [seglen][3]: first row of A^(m+1)
+    const float2* tab32;     // fp32 copy of the tables (same offsets as tab_base; iir32.cu)
+    float* state32;          // iir32.cu: [njobs*batch][nseg][12][lines] segment states (aliases `state`)
     double Aseg[9];          // A^seglen
     double Alast[9];         // A^(length of the last segment)
     int64_t src_bstride, dst_bstride;  // per image, in source / complex elements
@@ -131,6 +133,11 @@ template <typename T> struct IirArgs {
     int one_out;             // every job has exactly one output
 };
 template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s);
+// fp32 build: parallel-form sections in fp32, two passes + carries, no scratch
+// planes (iir32.cu).  Segments of exactly kIir32M samples (nseg = ceil(L / kIir32M)).
+constexpr int kIir32M = 32;
+bool iir32_enabled();  // false when FGB_IIR64 is set (the fp64-state kernels of iir.cu for A/B runs)
+cudaError_t launch_iir32(const IirArgs<float>& a, cudaStream_t s);
 template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch);
 size_t iir_state_doubles(int lines, int nseg, int njobs, int batch);
 
