@@ -34,6 +34,9 @@
 //     recombination, outputs.
 // Lines are adjacent threads; the horizontal stage (lines = image rows)
 // stages its rows through shared memory both ways.
+#include <algorithm>
+#include <array>
+#include <map>
 #include <complex>
 #include <cstdlib>
 #include <cstring>
@@ -86,83 +89,111 @@ __device__ __forceinline__ void sec_steady(Sec& s, float2 z0, const Iir32Par& q)
     s.ci = make_float2(q.gci * z0.x, q.gci * z0.y);
 }
 
-// modulation pair (see kernels.h): pair 0: (jr c + ji s, jr s - ji c); pair 1: (jr c - ji s, jr s + ji c)
-__device__ __forceinline__ float2 modz(float sgn, float jr, float ji, float2 cs) {
-    const float sj = sgn * ji;
-    return make_float2(fmaf(jr, cs.x, sj * cs.y), fmaf(jr, cs.y, -sj * cs.x));
+// CTA tile: 32 lines x kSY segments (kSW samples from nb0) of one job.
+// Shared memory: the modulation table of the tile's samples, the
+// recombination table, then the input tile:
+//   ROWS (horizontal stage, real rows): [32 rows][kSW | 1] floats (odd pitch)
+//   COLS (lines contiguous in memory):  [kSW samples][32 lines] of S (float or float2)
+// The fin kernel of the ROWS layout reuses the input tile (after a barrier)
+// as its [32][kSW | 1] complex output tile.
+constexpr int kSW = kSY * kM;
+constexpr int kTabBytes = 2 * kSW * (int)sizeof(float2);
+
+template <bool ROWS, bool CPLX> struct Tile {
+    static constexpr size_t in_bytes = ROWS ? (size_t)kTX * (kSW | 1) * sizeof(float)
+                                            : (size_t)kSW * kTX * (CPLX ? sizeof(float2) : sizeof(float));
+    static constexpr size_t out_bytes = ROWS ? (size_t)kTX * (kSW | 1) * sizeof(float2) : 0;
+    static constexpr size_t smem = kTabBytes + (in_bytes > out_bytes ? in_bytes : out_bytes);
+};
+
+// cp.async the tile (clamped = replicate pad) and both tables; one wait.
+template <bool ROWS, bool CPLX>
+__device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<float>& a, const IirJob<float>& job, int b,
+                                           bool want_tabr) {
+    const int len = a.len, P = a.P, L = len + 2 * P;
+    const int nb0 = blockIdx.y * kSW;
+    const int tid = threadIdx.y * kTX + threadIdx.x;
+    float2* tabm = reinterpret_cast<float2*>(smem);
+    float2* tabr = tabm + kSW;
+    for (int i = tid; i < kSW; i += kTX * kSY) {
+        const int n = nb0 + i;
+        if (n < L) cp_async8(tabm + i, a.tab32 + job.tabm_off + n);
+        if (want_tabr && n >= P && n < P + len) cp_async8(tabr + i, a.tab32 + job.tabr_off + (n - P));
+    }
+    unsigned char* tile = smem + kTabBytes;
+    if constexpr (ROWS) {
+        constexpr int swp = kSW | 1;
+        const float* base = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
+        float* t = reinterpret_cast<float*>(tile);
+        for (int r = threadIdx.y; r < kTX; r += kSY) {
+            const int line = blockIdx.x * kTX + r;
+            if (line >= a.lines) continue;
+            const float* row = base + (int64_t)line * a.src_ls;
+            for (int cc = threadIdx.x; cc < kSW; cc += kTX) {
+                const int n = nb0 + cc;
+                if (n < L) cp_async4(t + r * swp + cc, row + clampi(n - P, 0, len - 1));
+            }
+        }
+    } else {
+        const int x = min(blockIdx.x * kTX + threadIdx.x, a.lines - 1);
+        if constexpr (CPLX) {
+            const float2* src = reinterpret_cast<const float2*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + x;
+            float2* t = reinterpret_cast<float2*>(tile);
+            for (int cc = threadIdx.y; cc < kSW; cc += kSY) {
+                const int n = nb0 + cc;
+                if (n < L) cp_async8(t + cc * kTX + threadIdx.x, src + (int64_t)clampi(n - P, 0, len - 1) * a.src_ss);
+            }
+        } else {
+            const float* src = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + x;
+            float* t = reinterpret_cast<float*>(tile);
+            for (int cc = threadIdx.y; cc < kSW; cc += kSY) {
+                const int n = nb0 + cc;
+                if (n < L) cp_async4(t + cc * kTX + threadIdx.x, src + (int64_t)clampi(n - P, 0, len - 1) * a.src_ss);
+            }
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
 }
 
-// Source access of one line.  STAGE: the CTA's rows sit in shared memory
-// (samples nb0 .. nb0 + kSY kM - 1 of each row, already clamped).
-template <bool REAL, bool STAGE> struct Src {
-    const void* p;
-    int64_t ss;
-    int P, len, nb0;
-    const float2* tab;
-    float sgn;
-    __device__ __forceinline__ float2 z(int n) const {
-        const float2 cs = tab[n];
-        if constexpr (STAGE) {
-            const float f = reinterpret_cast<const float*>(p)[n - nb0];
+// modulated input (za, zb) of tile sample i (relative to nb0) for this thread's line
+template <bool ROWS, bool CPLX> struct In {
+    const unsigned char* tile;
+    const float2* tabm;
+    float sgn;  // +1: pair 0, -1: pair 1 (see kernels.h)
+    __device__ __forceinline__ float2 z(int i) const {
+        const float2 cs = tabm[i];
+        if constexpr (ROWS) {
+            const float f = reinterpret_cast<const float*>(tile)[threadIdx.x * (kSW | 1) + i];
             return make_float2(f * cs.x, f * cs.y);
-        } else if constexpr (REAL) {
-            const float f = reinterpret_cast<const float*>(p)[(int64_t)clampi(n - P, 0, len - 1) * ss];
-            return make_float2(f * cs.x, f * cs.y);
+        } else if constexpr (CPLX) {
+            const float2 v = reinterpret_cast<const float2*>(tile)[i * kTX + threadIdx.x];
+            const float sj = sgn * v.y;
+            return make_float2(fmaf(v.x, cs.x, sj * cs.y), fmaf(v.x, cs.y, -sj * cs.x));
         } else {
-            const float2 v = reinterpret_cast<const float2*>(p)[(int64_t)clampi(n - P, 0, len - 1) * ss];
-            return modz(sgn, v.x, v.y, cs);
+            const float f = reinterpret_cast<const float*>(tile)[i * kTX + threadIdx.x];
+            return make_float2(f * cs.x, f * cs.y);
         }
     }
 };
 
-// Row staging of the horizontal stage: the CTA's 32 rows x (kSY kM) samples,
-// row-contiguous loads, odd pitch for conflict-free per-thread reads.
-__device__ __forceinline__ void stage_rows(float* tile, const IirArgs<float>& a, const IirJob<float>& job, int b) {
-    constexpr int sw = kSY * kM, swp = sw | 1;
-    const int len = a.len, P = a.P, L = len + 2 * P;
-    const int nb0 = blockIdx.y * sw;
-    const float* base = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
-    for (int r = threadIdx.y; r < kTX; r += kSY) {
-        const int line = blockIdx.x * kTX + r;
-        if (line >= a.lines) continue;
-        const float* row = base + (int64_t)line * a.src_ls;
-        for (int cc = threadIdx.x; cc < sw; cc += kTX) {
-            const int n = nb0 + cc;
-            if (n < L) tile[r * swp + cc] = row[clampi(n - P, 0, len - 1)];
-        }
-    }
-}
-
-template <bool REAL, bool STAGE>
-__device__ __forceinline__ Src<REAL, STAGE> make_src(const IirArgs<float>& a, const IirJob<float>& job, int x, int b,
-                                                     const float* tile) {
-    Src<REAL, STAGE> s;
-    s.P = a.P;
-    s.len = a.len;
-    s.nb0 = blockIdx.y * kSY * kM;
-    s.tab = a.tab32 + job.tabm_off;
-    s.sgn = (job.need >> 1) ? -1.f : 1.f;
-    if constexpr (STAGE) {
-        s.p = tile + threadIdx.x * ((kSY * kM) | 1);
-        s.ss = 1;
-    } else if constexpr (REAL) {
-        s.p = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + (int64_t)x * a.src_ls;
-        s.ss = a.src_ss;
-    } else {
-        s.p = reinterpret_cast<const float2*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + (int64_t)x * a.src_ls;
-        s.ss = a.src_ss;
-    }
-    return s;
+template <bool ROWS, bool CPLX>
+__device__ __forceinline__ In<ROWS, CPLX> make_in(const unsigned char* smem, const IirJob<float>& job) {
+    In<ROWS, CPLX> in;
+    in.tabm = reinterpret_cast<const float2*>(smem);
+    in.tile = smem + kTabBytes;
+    in.sgn = (job.need >> 1) ? -1.f : 1.f;
+    return in;
 }
 
 // ---- pass 1: local forward sections -> end state e, backward-start sums b ----
-template <bool REAL, bool STAGE, bool FULL>
-__device__ __forceinline__ void sum_body(const Src<REAL, STAGE>& src, int n0, int m, Sec& s, float2& br, float2& bcr,
+template <bool ROWS, bool CPLX, bool FULL>
+__device__ __forceinline__ void sum_body(const In<ROWS, CPLX>& in, int i0, int m, Sec& s, float2& br, float2& bcr,
                                          float2& bci, const Iir32Par& q) {
 #pragma unroll
     for (int i = 0; i < kM; ++i) {
         if (FULL || i < m) {
-            const float2 y = sec_step(s, src.z(n0 + i), q);
+            const float2 y = sec_step(s, in.z(i0 + i), q);
             br = __ffma2_rn(dup(q.wr[i]), y, br);
             bcr = __ffma2_rn(dup(q.wcr[i]), y, bcr);
             bci = __ffma2_rn(dup(q.wci[i]), y, bci);
@@ -170,121 +201,162 @@ __device__ __forceinline__ void sum_body(const Src<REAL, STAGE>& src, int n0, in
     }
 }
 
-template <bool REAL, bool STAGE>
-__global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const __grid_constant__ Iir32Par q) {
-    const int x = blockIdx.x * kTX + threadIdx.x;
-    const int seg = blockIdx.y * kSY + threadIdx.y;
-    const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
-    const IirJob<float>& job = a.jobs[jb];
-    const int L = a.len + 2 * a.P, NL = a.lines;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* tile = reinterpret_cast<float*>(smem_raw);
-    if constexpr (STAGE) {
-        stage_rows(tile, a, job, b);
-        __syncthreads();
+// ---- carries ----
+// The last CTA of a 32-line block to finish pass 1 (an arrival counter per
+// block) scans that block's states, so the scans overlap the rest of pass 1
+// instead of running as a separate latency-bound launch.  States are staged
+// through the CTA's shared memory in chunks of kCS segments
+// ([kCS][12 slots][32 lines], 128-byte line runs); warp 0 scans plane a,
+// warp 1 plane b (lane = line); all four warps move the data.
+constexpr int kCL = kTX;
+__device__ __forceinline__ void carry_io(float* sm, float* g, int64_t NL, int j0, int nj, int nl, int k0, int k1, bool load) {
+    const int tid = threadIdx.y * kTX + threadIdx.x;
+    if (nl == kCL && (NL & 3) == 0) {  // 16-byte runs: thread = 4 lines of one (segment, slot)
+        const int l4 = (tid & 7) * 4, r0 = tid >> 3;  // 16 row groups
+        const int nk = k1 - k0;
+        for (int r = r0; r < nj * nk; r += 16) {
+            const int jj = r / nk, k = k0 + r - jj * nk;
+            float* gp = g + ((int64_t)(j0 + jj) * 12 + k) * NL + l4;
+            float* sp = sm + (jj * 12 + k) * kCL + l4;
+            if (load) cp_async16(sp, gp);
+            else *reinterpret_cast<float4*>(gp) = *reinterpret_cast<const float4*>(sp);
+        }
+    } else {
+        const int l = tid & 31, grp = tid >> 5;
+        if (l < nl)
+            for (int jj = 0; jj < nj; ++jj) {
+                float* gp = g + (int64_t)(j0 + jj) * 12 * NL + l;
+                float* sp = sm + jj * 12 * kCL + l;
+                for (int k = k0 + grp; k < k1; k += 4) {
+                    if (load) cp_async4(sp + k * kCL, gp + (int64_t)k * NL);
+                    else gp[(int64_t)k * NL] = sp[k * kCL];
+                }
+            }
     }
-    const int n0 = seg * kM;
-    if (x >= NL || n0 >= L) return;
-    const int m = min(kM, L - n0);
-    const Src<REAL, STAGE> src = make_src<REAL, STAGE>(a, job, x, b, tile);
-    Sec s;
-    if (seg == 0) sec_steady(s, src.z(0), q);
-    else s.r = s.cr = s.ci = dup(0.f);
-    float2 br = dup(0.f), bcr = dup(0.f), bci = dup(0.f);
-    if (m == kM) sum_body<REAL, STAGE, true>(src, n0, m, s, br, bcr, bci, q);
-    else sum_body<REAL, STAGE, false>(src, n0, m, s, br, bcr, bci, q);
-    float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
-    const float v[12] = {s.r.x, s.cr.x, s.ci.x, s.r.y, s.cr.y, s.ci.y, br.x, bcr.x, bci.x, br.y, bcr.y, bci.y};
-#pragma unroll
-    for (int k = 0; k < 12; ++k) st[(int64_t)k * NL] = v[k];
+    if (load) cp_async_wait_all();
+    __syncthreads();
 }
 
-// ---- carries: one thread per (line, plane), segments in order, loads batched ----
-constexpr int kCB = 8;
-__global__ void __launch_bounds__(128) iir32_carry(float* state, int lines, int nseg, const __grid_constant__ Iir32Par q) {
-    const int x = blockIdx.x * 64 + (threadIdx.x & 63);
-    const int pl = threadIdx.x >> 6;
-    if (x >= lines) return;
-    const int64_t NL = lines, SS = 12 * NL;  // slot / segment strides
-    float* base = state + (int64_t)blockIdx.z * nseg * SS + x;
-    float* e0 = base + 3 * pl * NL;        // e (then s_in) of this plane
-    float* b0 = base + (6 + 3 * pl) * NL;  // b (then t_in) of this plane
+// g: the block's states ([nseg][12][NL] from line x0); sm: kCS segments of staging
+__device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, int nseg, const Iir32Par& q) {
+    const int l = threadIdx.x, pl = threadIdx.y;  // scanning threads: pl < 2
+    const bool scan = pl < 2 && l < nl;
+    const int es = 3 * pl, bs = 6 + 3 * pl;  // slots of e (then s_in) and b (then t_in) of this plane
+    const bool one = nseg <= kCS;
+    // forward: s_in[j] = carry-in, s_{j+1} = q^m s_j + e_j
     float sr = 0.f, scr = 0.f, sci = 0.f;
-    for (int j0 = 0; j0 < nseg; j0 += kCB) {
-        float e[kCB][3];
-#pragma unroll
-        for (int i = 0; i < kCB; ++i)
-            if (j0 + i < nseg) {
-                const float* p = e0 + (j0 + i) * SS;
-                e[i][0] = p[0];
-                e[i][1] = p[NL];
-                e[i][2] = p[2 * NL];
+    const float Q0r = q.Q[0][0], Q0c = q.Q[0][1], Q0s = q.Q[0][2];
+    for (int j0 = 0; j0 < nseg; j0 += kCS) {
+        const int nj = min(kCS, nseg - j0);
+        carry_io(sm, g, NL, j0, nj, nl, 0, one ? 12 : 6, true);
+        if (scan) {
+            float* p = sm + l;
+#pragma unroll 4
+            for (int jj = 0; jj < nj; ++jj, p += 12 * kCL) {
+                const float e0 = p[es * kCL], e1 = p[(es + 1) * kCL], e2 = p[(es + 2) * kCL];
+                p[es * kCL] = sr;
+                p[(es + 1) * kCL] = scr;
+                p[(es + 2) * kCL] = sci;
+                const bool lt = j0 + jj == nseg - 1;
+                const float Qr = lt ? q.Q[1][0] : Q0r, Qc = lt ? q.Q[1][1] : Q0c, Qs = lt ? q.Q[1][2] : Q0s;
+                const float nr = fmaf(Qr, sr, e0);
+                const float ncr = fmaf(Qc, scr, fmaf(-Qs, sci, e1));
+                const float nci = fmaf(Qc, sci, fmaf(Qs, scr, e2));
+                sr = nr;
+                scr = ncr;
+                sci = nci;
             }
-#pragma unroll
-        for (int i = 0; i < kCB; ++i) {
-            const int j = j0 + i;
-            if (j >= nseg) break;
-            float* p = e0 + j * SS;
-            p[0] = sr;
-            p[NL] = scr;
-            p[2 * NL] = sci;
-            const float* Q = q.Q[j == nseg - 1];
-            const float nr = fmaf(Q[0], sr, e[i][0]);
-            const float ncr = fmaf(Q[1], scr, fmaf(-Q[2], sci, e[i][1]));
-            const float nci = fmaf(Q[1], sci, fmaf(Q[2], scr, e[i][2]));
-            sr = nr;
-            scr = ncr;
-            sci = nci;
         }
+        __syncthreads();
+        if (!one) carry_io(sm, g, NL, j0, nj, nl, 0, 6, false);
     }
     // true y[L-1] -> the backward sections' steady-state init
     const float yL = fmaf(2.f, scr, sr);
     float tr = q.gr * yL, tcr = q.gcr * yL, tci = q.gci * yL;
-    for (int j0 = nseg - 1; j0 >= 0; j0 -= kCB) {
-        float bb[kCB][3], si[kCB][3];
+    float M0[9];
 #pragma unroll
-        for (int i = 0; i < kCB; ++i)
-            if (j0 - i >= 0) {
-                const float* p = b0 + (j0 - i) * SS;
-                const float* r = e0 + (j0 - i) * SS;
-                bb[i][0] = p[0];
-                bb[i][1] = p[NL];
-                bb[i][2] = p[2 * NL];
-                si[i][0] = r[0];
-                si[i][1] = r[NL];
-                si[i][2] = r[2 * NL];
+    for (int k = 0; k < 9; ++k) M0[k] = q.Mb[0][k];
+    for (int j0 = (nseg - 1) / kCS * kCS; j0 >= 0; j0 -= kCS) {
+        const int nj = min(kCS, nseg - j0);
+        if (!one) carry_io(sm, g, NL, j0, nj, nl, 0, 12, true);
+        if (scan) {
+            float* p = sm + (nj - 1) * 12 * kCL + l;
+#pragma unroll 4
+            for (int jj = nj - 1; jj >= 0; --jj, p -= 12 * kCL) {
+                const float b0 = p[bs * kCL], b1 = p[(bs + 1) * kCL], b2 = p[(bs + 2) * kCL];
+                const float i0 = p[es * kCL], i1 = p[(es + 1) * kCL], i2 = p[(es + 2) * kCL];  // s_in of this plane
+                p[bs * kCL] = tr;
+                p[(bs + 1) * kCL] = tcr;
+                p[(bs + 2) * kCL] = tci;
+                const bool lt = j0 + jj == nseg - 1;
+                float M[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) M[k] = lt ? q.Mb[1][k] : M0[k];
+                const float Qr = lt ? q.Q[1][0] : Q0r, Qc = lt ? q.Q[1][1] : Q0c, Qs = lt ? q.Q[1][2] : Q0s;
+                const float c0 = fmaf(M[0], i0, fmaf(M[1], i1, fmaf(M[2], i2, b0)));
+                const float c1 = fmaf(M[3], i0, fmaf(M[4], i1, fmaf(M[5], i2, b1)));
+                const float c2 = fmaf(M[6], i0, fmaf(M[7], i1, fmaf(M[8], i2, b2)));
+                const float nr = fmaf(Qr, tr, c0);
+                const float ncr = fmaf(Qc, tcr, fmaf(-Qs, tci, c1));
+                const float nci = fmaf(Qc, tci, fmaf(Qs, tcr, c2));
+                tr = nr;
+                tcr = ncr;
+                tci = nci;
             }
-#pragma unroll
-        for (int i = 0; i < kCB; ++i) {
-            const int j = j0 - i;
-            if (j < 0) break;
-            float* p = b0 + j * SS;
-            p[0] = tr;
-            p[NL] = tcr;
-            p[2 * NL] = tci;
-            const int lt = j == nseg - 1;
-            const float* Q = q.Q[lt];
-            const float* M = q.Mb[lt];
-            const float c0 = fmaf(M[0], si[i][0], fmaf(M[1], si[i][1], fmaf(M[2], si[i][2], bb[i][0])));
-            const float c1 = fmaf(M[3], si[i][0], fmaf(M[4], si[i][1], fmaf(M[5], si[i][2], bb[i][1])));
-            const float c2 = fmaf(M[6], si[i][0], fmaf(M[7], si[i][1], fmaf(M[8], si[i][2], bb[i][2])));
-            const float nr = fmaf(Q[0], tr, c0);
-            const float ncr = fmaf(Q[1], tcr, fmaf(-Q[2], tci, c1));
-            const float nci = fmaf(Q[1], tci, fmaf(Q[2], tcr, c2));
-            tr = nr;
-            tcr = ncr;
-            tci = nci;
         }
+        __syncthreads();
+        carry_io(sm, g, NL, j0, nj, nl, one ? 0 : 6, 12, false);
     }
 }
 
+template <bool ROWS, bool CPLX>
+__global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const __grid_constant__ Iir32Par q, int* counters) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
+    const IirJob<float>& job = a.jobs[jb];
+    stage_tile<ROWS, CPLX>(smem, a, job, b, false);
+    const int x = blockIdx.x * kTX + threadIdx.x;
+    const int seg = blockIdx.y * kSY + threadIdx.y;
+    const int L = a.len + 2 * a.P, NL = a.lines;
+    const int n0 = seg * kM;
+    if (x < NL && n0 < L) {
+        const int m = min(kM, L - n0);
+        const In<ROWS, CPLX> in = make_in<ROWS, CPLX>(smem, job);
+        const int i0 = threadIdx.y * kM;
+        Sec s;
+        if (seg == 0) sec_steady(s, in.z(0), q);
+        else s.r = s.cr = s.ci = dup(0.f);
+        float2 br = dup(0.f), bcr = dup(0.f), bci = dup(0.f);
+        if (m == kM) sum_body<ROWS, CPLX, true>(in, i0, m, s, br, bcr, bci, q);
+        else sum_body<ROWS, CPLX, false>(in, i0, m, s, br, bcr, bci, q);
+        float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
+        const float v[12] = {s.r.x, s.cr.x, s.ci.x, s.r.y, s.cr.y, s.ci.y, br.x, bcr.x, bci.x, br.y, bcr.y, bci.y};
+#pragma unroll
+        for (int k = 0; k < 12; ++k) st[(int64_t)k * NL] = v[k];
+    }
+    // arrival: the last CTA of this line block runs its carries
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    int* cnt = counters + (int64_t)blockIdx.z * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0 && threadIdx.y == 0) last = atomicAdd(cnt, 1) == (int)gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int x0 = blockIdx.x * kTX;
+    const int kCS = (int)(Tile<ROWS, CPLX>::smem / (12 * kCL * sizeof(float)));
+    carry_block(reinterpret_cast<float*>(smem), kCS, a.state32 + (int64_t)blockIdx.z * a.nseg * 12 * NL + x0, NL,
+                min(kTX, NL - x0), a.nseg, q);
+    if (threadIdx.x == 0 && threadIdx.y == 0) *cnt = 0;  // ready for the next launch
+}
+
 // ---- pass 2: exact forward (registers), exact backward, recombination ----
-template <bool REAL, bool STAGE, bool FULL>
-__device__ __forceinline__ void fin_fwd(const Src<REAL, STAGE>& src, int n0, int m, Sec& s, float2 (&y)[kM],
+template <bool ROWS, bool CPLX, bool FULL>
+__device__ __forceinline__ void fin_fwd(const In<ROWS, CPLX>& in, int i0, int m, Sec& s, float2 (&y)[kM],
                                         const Iir32Par& q) {
 #pragma unroll
     for (int i = 0; i < kM; ++i)
-        if (FULL || i < m) y[i] = sec_step(s, src.z(n0 + i), q);
+        if (FULL || i < m) y[i] = sec_step(s, in.z(i0 + i), q);
 }
 
 template <bool FULL, typename EMIT>
@@ -294,57 +366,54 @@ __device__ __forceinline__ void fin_bwd(int m, Sec& t, const float2 (&y)[kM], co
         if (FULL || i < m) emit(i, sec_step(t, y[i], q));
 }
 
-template <bool REAL, bool STAGE>
+template <bool ROWS, bool CPLX>
 __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const __grid_constant__ Iir32Par q) {
-    const int x = blockIdx.x * kTX + threadIdx.x;
-    const int seg = blockIdx.y * kSY + threadIdx.y;
+    extern __shared__ __align__(16) unsigned char smem[];
     const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
     const IirJob<float>& job = a.jobs[jb];
+    stage_tile<ROWS, CPLX>(smem, a, job, b, true);
+    const int x = blockIdx.x * kTX + threadIdx.x;
+    const int seg = blockIdx.y * kSY + threadIdx.y;
     const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* tile = reinterpret_cast<float*>(smem_raw);
-    if constexpr (STAGE) {
-        stage_rows(tile, a, job, b);
-        __syncthreads();
-    }
     const int n0 = seg * kM;
     const int m = min(kM, L - n0);
+    const int i0 = threadIdx.y * kM;
     // segments that leave nothing inside the crop [P, P + len) only fed the carries
     const bool live = x < NL && n0 < L && n0 + m > P && n0 < P + len;
     const float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
+    const float2* tabr = reinterpret_cast<const float2*>(smem) + kSW;  // [i] = tabr[nb0 + i - P]
+    const float isg = job.sdft ? -1.f : 1.f;  // Gabor im = s Sa - c Sb; SDFT im = c Sb - s Sa
     float2 y[kM];
+    Sec t;
     if (live) {
-        const Src<REAL, STAGE> src = make_src<REAL, STAGE>(a, job, x, b, tile);
+        const In<ROWS, CPLX> in = make_in<ROWS, CPLX>(smem, job);
         Sec s;
         if (seg == 0) {
-            sec_steady(s, src.z(0), q);
+            sec_steady(s, in.z(0), q);
         } else {
             s.r = make_float2(st[0], st[3 * (int64_t)NL]);
             s.cr = make_float2(st[(int64_t)NL], st[4 * (int64_t)NL]);
             s.ci = make_float2(st[2 * (int64_t)NL], st[5 * (int64_t)NL]);
         }
-        if (m == kM) fin_fwd<REAL, STAGE, true>(src, n0, m, s, y, q);
-        else fin_fwd<REAL, STAGE, false>(src, n0, m, s, y, q);
+        t.r = make_float2(st[6 * (int64_t)NL], st[9 * (int64_t)NL]);
+        t.cr = make_float2(st[7 * (int64_t)NL], st[10 * (int64_t)NL]);
+        t.ci = make_float2(st[8 * (int64_t)NL], st[11 * (int64_t)NL]);
+        if (m == kM) fin_fwd<ROWS, CPLX, true>(in, i0, m, s, y, q);
+        else fin_fwd<ROWS, CPLX, false>(in, i0, m, s, y, q);
     }
-    const float2* tabr = a.tab32 + job.tabr_off;
-    const float isg = job.sdft ? -1.f : 1.f;  // Gabor im = s Sa - c Sb; SDFT im = c Sb - s Sa
-    if constexpr (STAGE) {
-        __syncthreads();  // every input sample consumed: the tile becomes the output tile
-        float2* otile = reinterpret_cast<float2*>(smem_raw);
-        constexpr int sw = kSY * kM, swp = sw | 1;
-        const int nb0 = blockIdx.y * sw;
+    if constexpr (ROWS) {
+        constexpr int swp = kSW | 1;
+        const int nb0 = blockIdx.y * kSW;
+        __syncthreads();  // every input sample consumed: the input tile becomes the output tile
+        float2* otile = reinterpret_cast<float2*>(smem + kTabBytes);
         if (live) {
-            Sec t;
-            t.r = make_float2(st[6 * (int64_t)NL], st[9 * (int64_t)NL]);
-            t.cr = make_float2(st[7 * (int64_t)NL], st[10 * (int64_t)NL]);
-            t.ci = make_float2(st[8 * (int64_t)NL], st[11 * (int64_t)NL]);
             const float osg = isg * (job.conj[0] ? -1.f : 1.f);
-            float2* trow = otile + threadIdx.x * swp - nb0;
+            float2* trow = otile + threadIdx.x * swp + i0;
             auto emit = [&](int i, float2 u) {
                 const int n = n0 + i;
                 if (n >= P && n < P + len) {
-                    const float2 cs = tabr[n - P];
-                    trow[n] = make_float2(fmaf(cs.x, u.x, cs.y * u.y), osg * fmaf(cs.y, u.x, -cs.x * u.y));
+                    const float2 cs = tabr[i0 + i];
+                    trow[i] = make_float2(fmaf(cs.x, u.x, cs.y * u.y), osg * fmaf(cs.y, u.x, -cs.x * u.y));
                 }
             };
             if (m == kM) fin_bwd<true>(m, t, y, q, emit);
@@ -356,16 +425,11 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
             const int line = blockIdx.x * kTX + r;
             if (line >= NL) continue;
             float2* row = dst + (int64_t)line * a.dst_ls - P;
-            const int c0 = max(0, P - nb0), c1 = min(sw, min(P + len, L) - nb0);
-            for (int cc = c0 + threadIdx.x; cc < c1; cc += kTX) row[nb0 + cc] = otile[r * swp + cc];
+            const int c0 = max(0, P - nb0), c1 = min(kSW, min(P + len, L) - nb0);
+            for (int cc = c0 + threadIdx.x; cc < c1; cc += kTX) __stcs(row + nb0 + cc, otile[r * swp + cc]);
         }
-        return;
     } else {
         if (!live) return;
-        Sec t;
-        t.r = make_float2(st[6 * (int64_t)NL], st[9 * (int64_t)NL]);
-        t.cr = make_float2(st[7 * (int64_t)NL], st[10 * (int64_t)NL]);
-        t.ci = make_float2(st[8 * (int64_t)NL], st[11 * (int64_t)NL]);
         const int nout = job.nout;
         float2* dptr[4];
         float osg[4];
@@ -378,11 +442,10 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
         auto emit = [&](int i, float2 u) {
             const int n = n0 + i;
             if (n >= P && n < P + len) {
-                const int yo = n - P;
-                const float2 cs = tabr[yo];
+                const float2 cs = tabr[i0 + i];
                 const float re = fmaf(cs.x, u.x, cs.y * u.y);
                 const float im = fmaf(cs.y, u.x, -cs.x * u.y);
-                const int64_t dof = (int64_t)yo * dss;
+                const int64_t dof = (int64_t)(n - P) * dss;
                 __stcs(dptr[0] + dof, make_float2(re, osg[0] * im));
                 if (nout > 1) {
 #pragma unroll
@@ -476,16 +539,22 @@ void iir32_params(const IirCoef& c, int mlast, Iir32Par* out) {
     }
 }
 
-template <bool REAL, bool STAGE>
-cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, dim3 grid, dim3 block, size_t smem, cudaStream_t s) {
-    if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(iir32_sum<REAL, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(iir32_fin<REAL, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <bool ROWS, bool CPLX>
+cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream_t s) {
+    constexpr size_t smem = Tile<ROWS, CPLX>::smem;
+    static bool attr = false;  // launches are serialised by the engine lock
+    if (!attr) {
+        cudaFuncSetAttribute(iir32_sum<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(iir32_fin<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
     }
-    iir32_sum<REAL, STAGE><<<grid, block, STAGE ? smem / 2 : 0, s>>>(a, q);
-    const dim3 cgrid((a.lines + 63) / 64, 1, a.njobs * a.batch);
-    iir32_carry<<<cgrid, 128, 0, s>>>(a.state32, a.lines, a.nseg, q);
-    iir32_fin<REAL, STAGE><<<grid, block, STAGE ? smem : 0, s>>>(a, q);
+    const dim3 block(kTX, kSY);
+    const dim3 grid((a.lines + kTX - 1) / kTX, (a.nseg + kSY - 1) / kSY, a.njobs * a.batch);
+    // arrival counters (one int per 32-line block and job) after the states; zeroed once per launch
+    int* counters = reinterpret_cast<int*>(a.state32 + (int64_t)a.njobs * a.batch * a.nseg * 12 * a.lines);
+    cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)grid.x * grid.z, s);
+    iir32_sum<ROWS, CPLX><<<grid, block, smem, s>>>(a, q, counters);
+    iir32_fin<ROWS, CPLX><<<grid, block, smem, s>>>(a, q);
     return cudaGetLastError();
 }
 
@@ -501,15 +570,20 @@ cudaError_t launch_iir32(const IirArgs<float>& a_in, cudaStream_t s) {
     const int L = a.len + 2 * a.P;
     if (a.seglen != kM || a.nseg != (L + kM - 1) / kM) return cudaErrorInvalidValue;
     a.state32 = reinterpret_cast<float*>(a.state);
-    Iir32Par q;
-    iir32_params(a.c, L - (a.nseg - 1) * kM, &q);
-    const dim3 block(kTX, kSY);
-    const dim3 grid((a.lines + kTX - 1) / kTX, (a.nseg + kSY - 1) / kSY, a.njobs * a.batch);
-    const size_t out_smem = (size_t)kTX * ((kSY * kM) | 1) * sizeof(float2);
-    const bool stage = a.real_in && a.src_ss == 1 && a.dst_ss == 1 && a.one_out;
-    if (stage) return launch_passes<true, true>(a, q, grid, block, out_smem, s);
-    if (a.real_in) return launch_passes<true, false>(a, q, grid, block, 0, s);
-    return launch_passes<false, false>(a, q, grid, block, 0, s);
+    // parameters per (coefficients, last segment length), computed once (launches are serialised by the engine lock)
+    static std::map<std::array<double, 5>, Iir32Par> cache;
+    const std::array<double, 5> key = {a.c.B, a.c.a1, a.c.a2, a.c.a3, (double)(L - (a.nseg - 1) * kM)};
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        Iir32Par p;
+        iir32_params(a.c, L - (a.nseg - 1) * kM, &p);
+        it = cache.emplace(key, p).first;
+    }
+    const Iir32Par& q = it->second;
+    if (a.src_ls == 1) return a.real_in ? launch_passes<false, false>(a, q, s) : launch_passes<false, true>(a, q, s);
+    // horizontal stage: real rows in, one output per job, rows written in place
+    if (a.real_in && a.src_ss == 1 && a.dst_ss == 1 && a.one_out) return launch_passes<true, false>(a, q, s);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace fgb
