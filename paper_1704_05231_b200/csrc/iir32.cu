@@ -97,7 +97,17 @@ __device__ __forceinline__ void sec_steady(Sec& s, float2 z0, const Iir32Par& q)
 // The fin kernel of the ROWS layout reuses the input tile (after a barrier)
 // as its [32][kSW | 1] complex output tile.
 constexpr int kSW = kSY * kM;
-constexpr int kTabBytes = 2 * kSW * (int)sizeof(float2);
+
+// Grid: x = segment blocks (fastest, so the CTAs of one line block run
+// back to back and its carry scan starts early), y = 32-line blocks, z = jobs.
+__device__ __forceinline__ int sblk() { return blockIdx.x; }
+__device__ __forceinline__ int lblk() { return blockIdx.y; }
+// tables (float4 per sample, so modulation and recombination are one
+// FMUL2 + one FFMA2 each):  tabm[i] = (c, s, sgn s, -sgn c) of sample nb0 + i,
+// (za, zb) = jr (c, s) + ji (sgn s, -sgn c);  tabr[i] = (c, o s, s, -o c) of
+// output sample nb0 + i - P, (re, im) = Sa (c, o s) + Sb (s, -o c), o = the
+// sign of output 0's imaginary part.
+constexpr int kTabBytes = 2 * kSW * (int)sizeof(float4);
 
 template <bool ROWS, bool CPLX> struct Tile {
     static constexpr size_t in_bytes = ROWS ? (size_t)kTX * (kSW | 1) * sizeof(float)
@@ -111,14 +121,22 @@ template <bool ROWS, bool CPLX>
 __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<float>& a, const IirJob<float>& job, int b,
                                            bool want_tabr) {
     const int len = a.len, P = a.P, L = len + 2 * P;
-    const int nb0 = blockIdx.y * kSW;
+    const int nb0 = sblk() * kSW;
     const int tid = threadIdx.y * kTX + threadIdx.x;
-    float2* tabm = reinterpret_cast<float2*>(smem);
-    float2* tabr = tabm + kSW;
+    float4* tabm = reinterpret_cast<float4*>(smem);
+    float4* tabr = tabm + kSW;
+    const float sgn = (job.need >> 1) ? -1.f : 1.f;
+    const float osg = (job.sdft ? -1.f : 1.f) * (job.conj[0] ? -1.f : 1.f);
     for (int i = tid; i < kSW; i += kTX * kSY) {
         const int n = nb0 + i;
-        if (n < L) cp_async8(tabm + i, a.tab32 + job.tabm_off + n);
-        if (want_tabr && n >= P && n < P + len) cp_async8(tabr + i, a.tab32 + job.tabr_off + (n - P));
+        if (n < L) {
+            const float2 cs = a.tab32[job.tabm_off + n];
+            tabm[i] = make_float4(cs.x, cs.y, sgn * cs.y, -sgn * cs.x);
+        }
+        if (want_tabr && n >= P && n < P + len) {
+            const float2 cs = a.tab32[job.tabr_off + (n - P)];
+            tabr[i] = make_float4(cs.x, osg * cs.y, cs.y, -osg * cs.x);
+        }
     }
     unsigned char* tile = smem + kTabBytes;
     if constexpr (ROWS) {
@@ -126,7 +144,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
         const float* base = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
         float* t = reinterpret_cast<float*>(tile);
         for (int r = threadIdx.y; r < kTX; r += kSY) {
-            const int line = blockIdx.x * kTX + r;
+            const int line = lblk() * kTX + r;
             if (line >= a.lines) continue;
             const float* row = base + (int64_t)line * a.src_ls;
             for (int cc = threadIdx.x; cc < kSW; cc += kTX) {
@@ -135,7 +153,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
             }
         }
     } else {
-        const int x = min(blockIdx.x * kTX + threadIdx.x, a.lines - 1);
+        const int x = min(lblk() * kTX + threadIdx.x, a.lines - 1);
         if constexpr (CPLX) {
             const float2* src = reinterpret_cast<const float2*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + x;
             float2* t = reinterpret_cast<float2*>(tile);
@@ -159,30 +177,32 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
 // modulated input (za, zb) of tile sample i (relative to nb0) for this thread's line
 template <bool ROWS, bool CPLX> struct In {
     const unsigned char* tile;
-    const float2* tabm;
-    float sgn;  // +1: pair 0, -1: pair 1 (see kernels.h)
+    const float4* tabm;
     __device__ __forceinline__ float2 z(int i) const {
-        const float2 cs = tabm[i];
+        const float4 t = tabm[i];
         if constexpr (ROWS) {
             const float f = reinterpret_cast<const float*>(tile)[threadIdx.x * (kSW | 1) + i];
-            return make_float2(f * cs.x, f * cs.y);
+            return __fmul2_rn(make_float2(t.x, t.y), dup(f));
         } else if constexpr (CPLX) {
             const float2 v = reinterpret_cast<const float2*>(tile)[i * kTX + threadIdx.x];
-            const float sj = sgn * v.y;
-            return make_float2(fmaf(v.x, cs.x, sj * cs.y), fmaf(v.x, cs.y, -sj * cs.x));
+            return __ffma2_rn(make_float2(t.x, t.y), dup(v.x), __fmul2_rn(make_float2(t.z, t.w), dup(v.y)));
         } else {
             const float f = reinterpret_cast<const float*>(tile)[i * kTX + threadIdx.x];
-            return make_float2(f * cs.x, f * cs.y);
+            return __fmul2_rn(make_float2(t.x, t.y), dup(f));
         }
     }
 };
 
+// (re, im) of output 0 from the smoothed pair u = (Sa, Sb)
+__device__ __forceinline__ float2 recombine(const float4 t, float2 u) {
+    return __ffma2_rn(make_float2(t.x, t.y), dup(u.x), __fmul2_rn(make_float2(t.z, t.w), dup(u.y)));
+}
+
 template <bool ROWS, bool CPLX>
 __device__ __forceinline__ In<ROWS, CPLX> make_in(const unsigned char* smem, const IirJob<float>& job) {
     In<ROWS, CPLX> in;
-    in.tabm = reinterpret_cast<const float2*>(smem);
+    in.tabm = reinterpret_cast<const float4*>(smem);
     in.tile = smem + kTabBytes;
-    in.sgn = (job.need >> 1) ? -1.f : 1.f;
     return in;
 }
 
@@ -315,8 +335,8 @@ __global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const _
     const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
     const IirJob<float>& job = a.jobs[jb];
     stage_tile<ROWS, CPLX>(smem, a, job, b, false);
-    const int x = blockIdx.x * kTX + threadIdx.x;
-    const int seg = blockIdx.y * kSY + threadIdx.y;
+    const int x = lblk() * kTX + threadIdx.x;
+    const int seg = sblk() * kSY + threadIdx.y;
     const int L = a.len + 2 * a.P, NL = a.lines;
     const int n0 = seg * kM;
     if (x < NL && n0 < L) {
@@ -335,16 +355,23 @@ __global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const _
         for (int k = 0; k < 12; ++k) st[(int64_t)k * NL] = v[k];
     }
     // arrival: the last CTA of this line block runs its carries
+    // (the barrier orders the CTA's state writes before thread 0's cumulative
+    // gpu-scope fence; only one thread pays the membar)
     __shared__ int last;
-    __threadfence();
+    if (!counters) return;  // timing experiment only (FGB_IIR32_NOCARRY): no carries
     __syncthreads();
-    int* cnt = counters + (int64_t)blockIdx.z * gridDim.x + blockIdx.x;
-    if (threadIdx.x == 0 && threadIdx.y == 0) last = atomicAdd(cnt, 1) == (int)gridDim.y - 1;
+    int* cnt = counters + (int64_t)blockIdx.z * gridDim.y + lblk();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        __threadfence();
+        last = atomicAdd(cnt, 1) == (int)gridDim.x - 1;
+    }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    const int x0 = blockIdx.x * kTX;
-    const int kCS = (int)(Tile<ROWS, CPLX>::smem / (12 * kCL * sizeof(float)));
+    const int x0 = lblk() * kTX;
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const int kCS = (int)(dyn / (12 * kCL * sizeof(float)));
     carry_block(reinterpret_cast<float*>(smem), kCS, a.state32 + (int64_t)blockIdx.z * a.nseg * 12 * NL + x0, NL,
                 min(kTX, NL - x0), a.nseg, q);
     if (threadIdx.x == 0 && threadIdx.y == 0) *cnt = 0;  // ready for the next launch
@@ -372,17 +399,18 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
     const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
     const IirJob<float>& job = a.jobs[jb];
     stage_tile<ROWS, CPLX>(smem, a, job, b, true);
-    const int x = blockIdx.x * kTX + threadIdx.x;
-    const int seg = blockIdx.y * kSY + threadIdx.y;
+    const int x = lblk() * kTX + threadIdx.x;
+    const int seg = sblk() * kSY + threadIdx.y;
     const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
     const int n0 = seg * kM;
     const int m = min(kM, L - n0);
     const int i0 = threadIdx.y * kM;
     // segments that leave nothing inside the crop [P, P + len) only fed the carries
     const bool live = x < NL && n0 < L && n0 + m > P && n0 < P + len;
+    // interior: a whole segment inside the crop (no per-sample checks)
+    const bool interior = m == kM && n0 >= P && n0 + kM <= P + len;
     const float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
-    const float2* tabr = reinterpret_cast<const float2*>(smem) + kSW;  // [i] = tabr[nb0 + i - P]
-    const float isg = job.sdft ? -1.f : 1.f;  // Gabor im = s Sa - c Sb; SDFT im = c Sb - s Sa
+    const float4* tabr = reinterpret_cast<const float4*>(smem) + kSW;  // [i]: output sample nb0 + i - P
     float2 y[kM];
     Sec t;
     if (live) {
@@ -403,26 +431,26 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
     }
     if constexpr (ROWS) {
         constexpr int swp = kSW | 1;
-        const int nb0 = blockIdx.y * kSW;
+        const int nb0 = sblk() * kSW;
         __syncthreads();  // every input sample consumed: the input tile becomes the output tile
         float2* otile = reinterpret_cast<float2*>(smem + kTabBytes);
         if (live) {
-            const float osg = isg * (job.conj[0] ? -1.f : 1.f);
             float2* trow = otile + threadIdx.x * swp + i0;
-            auto emit = [&](int i, float2 u) {
-                const int n = n0 + i;
-                if (n >= P && n < P + len) {
-                    const float2 cs = tabr[i0 + i];
-                    trow[i] = make_float2(fmaf(cs.x, u.x, cs.y * u.y), osg * fmaf(cs.y, u.x, -cs.x * u.y));
-                }
-            };
-            if (m == kM) fin_bwd<true>(m, t, y, q, emit);
-            else fin_bwd<false>(m, t, y, q, emit);
+            if (interior) {
+                fin_bwd<true>(m, t, y, q, [&](int i, float2 u) { trow[i] = recombine(tabr[i0 + i], u); });
+            } else {
+                auto emit = [&](int i, float2 u) {
+                    const int n = n0 + i;
+                    if (n >= P && n < P + len) trow[i] = recombine(tabr[i0 + i], u);
+                };
+                if (m == kM) fin_bwd<true>(m, t, y, q, emit);
+                else fin_bwd<false>(m, t, y, q, emit);
+            }
         }
         __syncthreads();
         float2* dst = a.dst_base + job.dst_off[0] + (int64_t)b * a.dst_bstride;
         for (int r = threadIdx.y; r < kTX; r += kSY) {
-            const int line = blockIdx.x * kTX + r;
+            const int line = lblk() * kTX + r;
             if (line >= NL) continue;
             float2* row = dst + (int64_t)line * a.dst_ls - P;
             const int c0 = max(0, P - nb0), c1 = min(kSW, min(P + len, L) - nb0);
@@ -430,32 +458,39 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
         }
     } else {
         if (!live) return;
+        // outputs 1..3 (SDFT conjugate fills) = output 0 with im scaled by rel[o] = +-1
         const int nout = job.nout;
-        float2* dptr[4];
-        float osg[4];
+        float2* d0 = a.dst_base + job.dst_off[0] + (int64_t)b * a.dst_bstride + (int64_t)x * a.dst_ls;
+        int64_t dlt[4];
+        float rel[4];
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
-            dptr[o] = a.dst_base + (o < nout ? job.dst_off[o] : 0) + (int64_t)b * a.dst_bstride + (int64_t)x * a.dst_ls;
-            osg[o] = (o < nout && job.conj[o]) ? -isg : isg;
+            dlt[o] = o < nout ? job.dst_off[o] - job.dst_off[0] : 0;
+            rel[o] = (o < nout && job.conj[o] != job.conj[0]) ? -1.f : 1.f;
         }
         const int64_t dss = a.dst_ss;
-        auto emit = [&](int i, float2 u) {
-            const int n = n0 + i;
-            if (n >= P && n < P + len) {
-                const float2 cs = tabr[i0 + i];
-                const float re = fmaf(cs.x, u.x, cs.y * u.y);
-                const float im = fmaf(cs.y, u.x, -cs.x * u.y);
-                const int64_t dof = (int64_t)(n - P) * dss;
-                __stcs(dptr[0] + dof, make_float2(re, osg[0] * im));
-                if (nout > 1) {
+        auto put = [&](float2* p, float2 v) {
+            __stcs(p, v);
+            if (nout > 1) {
 #pragma unroll
-                    for (int o = 1; o < 4; ++o)
-                        if (o < nout) __stcs(dptr[o] + dof, make_float2(re, osg[o] * im));
-                }
+                for (int o = 1; o < 4; ++o)
+                    if (o < nout) __stcs(p + dlt[o], make_float2(v.x, rel[o] * v.y));
             }
         };
-        if (m == kM) fin_bwd<true>(m, t, y, q, emit);
-        else fin_bwd<false>(m, t, y, q, emit);
+        if (interior) {
+            float2* p = d0 + (int64_t)(n0 + kM - 1 - P) * dss;  // walks up with the backward pass
+            fin_bwd<true>(m, t, y, q, [&](int i, float2 u) {
+                put(p, recombine(tabr[i0 + i], u));
+                p -= dss;
+            });
+        } else {
+            auto emit = [&](int i, float2 u) {
+                const int n = n0 + i;
+                if (n >= P && n < P + len) put(d0 + (int64_t)(n - P) * dss, recombine(tabr[i0 + i], u));
+            };
+            if (m == kM) fin_bwd<true>(m, t, y, q, emit);
+            else fin_bwd<false>(m, t, y, q, emit);
+        }
     }
 }
 
@@ -542,18 +577,25 @@ void iir32_params(const IirCoef& c, int mlast, Iir32Par* out) {
 template <bool ROWS, bool CPLX>
 cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream_t s) {
     constexpr size_t smem = Tile<ROWS, CPLX>::smem;
+    // pass 1 also stages the carry scan of its line block: room for every
+    // segment when that is <= kCarrySegs (one load / store round trip),
+    // else chunks of what the tile leaves
+    static const int carry_segs = std::getenv("FGB_IIR32_CARRY_SEGS") ? std::atoi(std::getenv("FGB_IIR32_CARRY_SEGS")) : 0;
+    const size_t csmem = (size_t)std::min(a.nseg, carry_segs) * 12 * kCL * sizeof(float);
+    const size_t ssmem = std::max(smem, csmem);
     static bool attr = false;  // launches are serialised by the engine lock
     if (!attr) {
-        cudaFuncSetAttribute(iir32_sum<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(iir32_sum<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         cudaFuncSetAttribute(iir32_fin<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const dim3 block(kTX, kSY);
-    const dim3 grid((a.lines + kTX - 1) / kTX, (a.nseg + kSY - 1) / kSY, a.njobs * a.batch);
+    const dim3 grid((a.nseg + kSY - 1) / kSY, (a.lines + kTX - 1) / kTX, a.njobs * a.batch);
     // arrival counters (one int per 32-line block and job) after the states; zeroed once per launch
     int* counters = reinterpret_cast<int*>(a.state32 + (int64_t)a.njobs * a.batch * a.nseg * 12 * a.lines);
-    cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)grid.x * grid.z, s);
-    iir32_sum<ROWS, CPLX><<<grid, block, smem, s>>>(a, q, counters);
+    cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)grid.y * grid.z, s);
+    static const bool nocarry = std::getenv("FGB_IIR32_NOCARRY") != nullptr;
+    iir32_sum<ROWS, CPLX><<<grid, block, ssmem, s>>>(a, q, nocarry ? nullptr : counters);
     iir32_fin<ROWS, CPLX><<<grid, block, smem, s>>>(a, q);
     return cudaGetLastError();
 }
