@@ -109,12 +109,15 @@ __device__ __forceinline__ int lblk() { return blockIdx.y; }
 // sign of output 0's imaginary part.
 constexpr int kTabBytes = 2 * kSW * (int)sizeof(float4);
 
+// Every tile slot is a float2 (real inputs fill .x): pass 2 overwrites a
+// thread's own slots in place with y, and (ROWS) with the outputs.
 template <bool ROWS, bool CPLX> struct Tile {
-    static constexpr size_t in_bytes = ROWS ? (size_t)kTX * (kSW | 1) * sizeof(float)
-                                            : (size_t)kSW * kTX * (CPLX ? sizeof(float2) : sizeof(float));
-    static constexpr size_t out_bytes = ROWS ? (size_t)kTX * (kSW | 1) * sizeof(float2) : 0;
-    static constexpr size_t smem = kTabBytes + (in_bytes > out_bytes ? in_bytes : out_bytes);
+    static constexpr size_t smem = kTabBytes + (ROWS ? (size_t)kTX * (kSW | 1) : (size_t)kSW * kTX) * sizeof(float2);
 };
+// slot of sample i (relative to the tile start) of this thread's line
+template <bool ROWS> __device__ __forceinline__ int slot(int i) {
+    return ROWS ? threadIdx.x * (kSW | 1) + i : i * kTX + threadIdx.x;
+}
 
 // cp.async the tile (clamped = replicate pad) and both tables; one wait.
 template <bool ROWS, bool CPLX>
@@ -142,7 +145,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
     if constexpr (ROWS) {
         constexpr int swp = kSW | 1;
         const float* base = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
-        float* t = reinterpret_cast<float*>(tile);
+        float2* t = reinterpret_cast<float2*>(tile);
         for (int r = threadIdx.y; r < kTX; r += kSY) {
             const int line = lblk() * kTX + r;
             if (line >= a.lines) continue;
@@ -163,7 +166,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
             }
         } else {
             const float* src = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + x;
-            float* t = reinterpret_cast<float*>(tile);
+            float2* t = reinterpret_cast<float2*>(tile);
             for (int cc = threadIdx.y; cc < kSW; cc += kSY) {
                 const int n = nb0 + cc;
                 if (n < L) cp_async4(t + cc * kTX + threadIdx.x, src + (int64_t)clampi(n - P, 0, len - 1) * a.src_ss);
@@ -176,20 +179,13 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
 
 // modulated input (za, zb) of tile sample i (relative to nb0) for this thread's line
 template <bool ROWS, bool CPLX> struct In {
-    const unsigned char* tile;
+    float2* tile;
     const float4* tabm;
     __device__ __forceinline__ float2 z(int i) const {
         const float4 t = tabm[i];
-        if constexpr (ROWS) {
-            const float f = reinterpret_cast<const float*>(tile)[threadIdx.x * (kSW | 1) + i];
-            return __fmul2_rn(make_float2(t.x, t.y), dup(f));
-        } else if constexpr (CPLX) {
-            const float2 v = reinterpret_cast<const float2*>(tile)[i * kTX + threadIdx.x];
-            return __ffma2_rn(make_float2(t.x, t.y), dup(v.x), __fmul2_rn(make_float2(t.z, t.w), dup(v.y)));
-        } else {
-            const float f = reinterpret_cast<const float*>(tile)[i * kTX + threadIdx.x];
-            return __fmul2_rn(make_float2(t.x, t.y), dup(f));
-        }
+        const float2 v = tile[slot<ROWS>(i)];
+        if constexpr (CPLX) return __ffma2_rn(make_float2(t.x, t.y), dup(v.x), __fmul2_rn(make_float2(t.z, t.w), dup(v.y)));
+        else return __fmul2_rn(make_float2(t.x, t.y), dup(v.x));
     }
 };
 
@@ -199,10 +195,10 @@ __device__ __forceinline__ float2 recombine(const float4 t, float2 u) {
 }
 
 template <bool ROWS, bool CPLX>
-__device__ __forceinline__ In<ROWS, CPLX> make_in(const unsigned char* smem, const IirJob<float>& job) {
+__device__ __forceinline__ In<ROWS, CPLX> make_in(unsigned char* smem, const IirJob<float>& job) {
     In<ROWS, CPLX> in;
     in.tabm = reinterpret_cast<const float4*>(smem);
-    in.tile = smem + kTabBytes;
+    in.tile = reinterpret_cast<float2*>(smem + kTabBytes);
     return in;
 }
 
@@ -210,9 +206,10 @@ __device__ __forceinline__ In<ROWS, CPLX> make_in(const unsigned char* smem, con
 template <bool ROWS, bool CPLX, bool FULL>
 __device__ __forceinline__ void sum_body(const In<ROWS, CPLX>& in, int i0, int m, Sec& s, float2& br, float2& bcr,
                                          float2& bci, const Iir32Par& q) {
-#pragma unroll
-    for (int i = 0; i < kM; ++i) {
-        if (FULL || i < m) {
+    // the short last segment of a line runs rolled (keeps the kernel's code small)
+#pragma unroll(FULL ? kM : 1)
+    for (int i = 0; i < (FULL ? kM : m); ++i) {
+        {
             const float2 y = sec_step(s, in.z(i0 + i), q);
             br = __ffma2_rn(dup(q.wr[i]), y, br);
             bcr = __ffma2_rn(dup(q.wcr[i]), y, bcr);
@@ -377,20 +374,22 @@ __global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const _
     if (threadIdx.x == 0 && threadIdx.y == 0) *cnt = 0;  // ready for the next launch
 }
 
-// ---- pass 2: exact forward (registers), exact backward, recombination ----
+// ---- pass 2: exact forward (y into the thread's own tile slots), exact backward, recombination ----
+// FULL (interior segments): unrolled; otherwise (segments at the pad
+// boundaries, the short last one) rolled, so the kernel's code stays small
 template <bool ROWS, bool CPLX, bool FULL>
-__device__ __forceinline__ void fin_fwd(const In<ROWS, CPLX>& in, int i0, int m, Sec& s, float2 (&y)[kM],
-                                        const Iir32Par& q) {
-#pragma unroll
-    for (int i = 0; i < kM; ++i)
-        if (FULL || i < m) y[i] = sec_step(s, in.z(i0 + i), q);
+__device__ __forceinline__ void fin_fwd(const In<ROWS, CPLX>& in, int i0, int m, Sec& s, const Iir32Par& q) {
+#pragma unroll(FULL ? kM : 1)
+    for (int i = 0; i < (FULL ? kM : m); ++i) {
+        const float2 z = in.z(i0 + i);
+        in.tile[slot<ROWS>(i0 + i)] = sec_step(s, z, q);
+    }
 }
 
-template <bool FULL, typename EMIT>
-__device__ __forceinline__ void fin_bwd(int m, Sec& t, const float2 (&y)[kM], const Iir32Par& q, EMIT emit) {
-#pragma unroll
-    for (int i = kM - 1; i >= 0; --i)
-        if (FULL || i < m) emit(i, sec_step(t, y[i], q));
+template <bool ROWS, bool FULL, typename EMIT>
+__device__ __forceinline__ void fin_bwd(const float2* tile, int i0, int m, Sec& t, const Iir32Par& q, EMIT emit) {
+#pragma unroll(FULL ? kM : 1)
+    for (int i = (FULL ? kM : m) - 1; i >= 0; --i) emit(i, sec_step(t, tile[slot<ROWS>(i0 + i)], q));
 }
 
 template <bool ROWS, bool CPLX>
@@ -411,7 +410,7 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
     const bool interior = m == kM && n0 >= P && n0 + kM <= P + len;
     const float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
     const float4* tabr = reinterpret_cast<const float4*>(smem) + kSW;  // [i]: output sample nb0 + i - P
-    float2 y[kM];
+    float2* tile = reinterpret_cast<float2*>(smem + kTabBytes);
     Sec t;
     if (live) {
         const In<ROWS, CPLX> in = make_in<ROWS, CPLX>(smem, job);
@@ -426,25 +425,23 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
         t.r = make_float2(st[6 * (int64_t)NL], st[9 * (int64_t)NL]);
         t.cr = make_float2(st[7 * (int64_t)NL], st[10 * (int64_t)NL]);
         t.ci = make_float2(st[8 * (int64_t)NL], st[11 * (int64_t)NL]);
-        if (m == kM) fin_fwd<ROWS, CPLX, true>(in, i0, m, s, y, q);
-        else fin_fwd<ROWS, CPLX, false>(in, i0, m, s, y, q);
+        if (interior) fin_fwd<ROWS, CPLX, true>(in, i0, m, s, q);
+        else fin_fwd<ROWS, CPLX, false>(in, i0, m, s, q);
     }
     if constexpr (ROWS) {
         constexpr int swp = kSW | 1;
         const int nb0 = sblk() * kSW;
-        __syncthreads();  // every input sample consumed: the input tile becomes the output tile
-        float2* otile = reinterpret_cast<float2*>(smem + kTabBytes);
+        float2* otile = tile;  // outputs replace y in the same slots
         if (live) {
             float2* trow = otile + threadIdx.x * swp + i0;
             if (interior) {
-                fin_bwd<true>(m, t, y, q, [&](int i, float2 u) { trow[i] = recombine(tabr[i0 + i], u); });
+                fin_bwd<ROWS, true>(tile, i0, m, t, q, [&](int i, float2 u) { trow[i] = recombine(tabr[i0 + i], u); });
             } else {
                 auto emit = [&](int i, float2 u) {
                     const int n = n0 + i;
                     if (n >= P && n < P + len) trow[i] = recombine(tabr[i0 + i], u);
                 };
-                if (m == kM) fin_bwd<true>(m, t, y, q, emit);
-                else fin_bwd<false>(m, t, y, q, emit);
+                fin_bwd<ROWS, false>(tile, i0, m, t, q, emit);
             }
         }
         __syncthreads();
@@ -479,7 +476,7 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
         };
         if (interior) {
             float2* p = d0 + (int64_t)(n0 + kM - 1 - P) * dss;  // walks up with the backward pass
-            fin_bwd<true>(m, t, y, q, [&](int i, float2 u) {
+            fin_bwd<ROWS, true>(tile, i0, m, t, q, [&](int i, float2 u) {
                 put(p, recombine(tabr[i0 + i], u));
                 p -= dss;
             });
@@ -488,8 +485,7 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
                 const int n = n0 + i;
                 if (n >= P && n < P + len) put(d0 + (int64_t)(n - P) * dss, recombine(tabr[i0 + i], u));
             };
-            if (m == kM) fin_bwd<true>(m, t, y, q, emit);
-            else fin_bwd<false>(m, t, y, q, emit);
+            fin_bwd<ROWS, false>(tile, i0, m, t, q, emit);
         }
     }
 }
