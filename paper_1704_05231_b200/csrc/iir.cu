@@ -495,7 +495,11 @@ template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int nj
     return (size_t)njobs * batch * 2 * (size_t)(len + 2 * P) * lines;
 }
 
-size_t iir_state_doubles(int lines, int nseg, int njobs, int batch) { return 2 * (size_t)njobs * batch * nseg * 6 * lines; }
+// (iir32.cu keeps [z][nseg + ceil(nseg / 4)][12][lines] floats plus one arrival counter per 32-line block and z
+// in the same region: the extra z * lines doubles cover the counters when nseg is tiny)
+size_t iir_state_doubles(int lines, int nseg, int njobs, int batch) {
+    return 2 * (size_t)njobs * batch * nseg * 6 * lines + (size_t)njobs * batch * lines;
+}
 
 template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s) {
     dim3 block(kIirTX, kIirSY);

@@ -60,6 +60,14 @@ struct Iir32Par {
     float wr[kM], wcr[kM], wci[kM];  // backward-start weights c q^i
     float Q[2][3];           // q^kM, q^mlast: (real, complex re, complex im)
     float Mb[2][9];          // b contribution of a forward carry-in (s_r, s_cr, s_ci) -> (b_r, b_cr, b_ci)
+    float QS[2][3];          // the same for super-segments (the kSY segments of a CTA): q^(kSY kM), q^mlastS
+    float MbS[2][9];
+    // expansion of the super-segment carries (s_S, t_S) to sub-segment k of a
+    // [regular, last] super-segment:  s_in_k = QF[k] s_S + s_loc_k,
+    // t_in_k = QB[.][k] t_S + T_loc_k + G[.][k] s_S   (3-vectors (r, c re, c im))
+    float QF[kSY][3];
+    float QB[2][kSY][3];
+    float G[2][kSY][9];
 };
 
 __device__ __forceinline__ float2 dup(float v) { return make_float2(v, v); }
@@ -255,14 +263,15 @@ __device__ __forceinline__ void carry_io(float* sm, float* g, int64_t NL, int j0
 }
 
 // g: the block's states ([nseg][12][NL] from line x0); sm: kCS segments of staging
-__device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, int nseg, const Iir32Par& q) {
+__device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, int nseg, const Iir32Par& q,
+                            const float (*QT)[3], const float (*MT)[9]) {
     const int l = threadIdx.x, pl = threadIdx.y;  // scanning threads: pl < 2
     const bool scan = pl < 2 && l < nl;
     const int es = 3 * pl, bs = 6 + 3 * pl;  // slots of e (then s_in) and b (then t_in) of this plane
     const bool one = nseg <= kCS;
     // forward: s_in[j] = carry-in, s_{j+1} = q^m s_j + e_j
     float sr = 0.f, scr = 0.f, sci = 0.f;
-    const float Q0r = q.Q[0][0], Q0c = q.Q[0][1], Q0s = q.Q[0][2];
+    const float Q0r = QT[0][0], Q0c = QT[0][1], Q0s = QT[0][2];
     for (int j0 = 0; j0 < nseg; j0 += kCS) {
         const int nj = min(kCS, nseg - j0);
         carry_io(sm, g, NL, j0, nj, nl, 0, one ? 12 : 6, true);
@@ -275,7 +284,7 @@ __device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, in
                 p[(es + 1) * kCL] = scr;
                 p[(es + 2) * kCL] = sci;
                 const bool lt = j0 + jj == nseg - 1;
-                const float Qr = lt ? q.Q[1][0] : Q0r, Qc = lt ? q.Q[1][1] : Q0c, Qs = lt ? q.Q[1][2] : Q0s;
+                const float Qr = lt ? QT[1][0] : Q0r, Qc = lt ? QT[1][1] : Q0c, Qs = lt ? QT[1][2] : Q0s;
                 const float nr = fmaf(Qr, sr, e0);
                 const float ncr = fmaf(Qc, scr, fmaf(-Qs, sci, e1));
                 const float nci = fmaf(Qc, sci, fmaf(Qs, scr, e2));
@@ -292,7 +301,7 @@ __device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, in
     float tr = q.gr * yL, tcr = q.gcr * yL, tci = q.gci * yL;
     float M0[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) M0[k] = q.Mb[0][k];
+    for (int k = 0; k < 9; ++k) M0[k] = MT[0][k];
     for (int j0 = (nseg - 1) / kCS * kCS; j0 >= 0; j0 -= kCS) {
         const int nj = min(kCS, nseg - j0);
         if (!one) carry_io(sm, g, NL, j0, nj, nl, 0, 12, true);
@@ -308,8 +317,8 @@ __device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, in
                 const bool lt = j0 + jj == nseg - 1;
                 float M[9];
 #pragma unroll
-                for (int k = 0; k < 9; ++k) M[k] = lt ? q.Mb[1][k] : M0[k];
-                const float Qr = lt ? q.Q[1][0] : Q0r, Qc = lt ? q.Q[1][1] : Q0c, Qs = lt ? q.Q[1][2] : Q0s;
+                for (int k = 0; k < 9; ++k) M[k] = lt ? MT[1][k] : M0[k];
+                const float Qr = lt ? QT[1][0] : Q0r, Qc = lt ? QT[1][1] : Q0c, Qs = lt ? QT[1][2] : Q0s;
                 const float c0 = fmaf(M[0], i0, fmaf(M[1], i1, fmaf(M[2], i2, b0)));
                 const float c1 = fmaf(M[3], i0, fmaf(M[4], i1, fmaf(M[5], i2, b1)));
                 const float c2 = fmaf(M[6], i0, fmaf(M[7], i1, fmaf(M[8], i2, b2)));
@@ -336,6 +345,9 @@ __global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const _
     const int seg = sblk() * kSY + threadIdx.y;
     const int L = a.len + 2 * a.P, NL = a.lines;
     const int n0 = seg * kM;
+    float sub[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) sub[k] = 0.f;
     if (x < NL && n0 < L) {
         const int m = min(kM, L - n0);
         const In<ROWS, CPLX> in = make_in<ROWS, CPLX>(smem, job);
@@ -346,10 +358,66 @@ __global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const _
         float2 br = dup(0.f), bcr = dup(0.f), bci = dup(0.f);
         if (m == kM) sum_body<ROWS, CPLX, true>(in, i0, m, s, br, bcr, bci, q);
         else sum_body<ROWS, CPLX, false>(in, i0, m, s, br, bcr, bci, q);
-        float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
         const float v[12] = {s.r.x, s.cr.x, s.ci.x, s.r.y, s.cr.y, s.ci.y, br.x, bcr.x, bci.x, br.y, bcr.y, bci.y};
 #pragma unroll
-        for (int k = 0; k < 12; ++k) st[(int64_t)k * NL] = v[k];
+        for (int k = 0; k < 12; ++k) sub[k] = v[k];
+    }
+    // super-segment summary (this CTA's kSY segments as one segment): the
+    // carries then scan kSY times fewer steps; pass 2 expands them again
+    __syncthreads();  // the tile is dead: it holds the sub-segment summaries now
+    float* sm = reinterpret_cast<float*>(smem);  // [kSY][12][kTX]
+#pragma unroll
+    for (int k = 0; k < 12; ++k) sm[(threadIdx.y * 12 + k) * kTX + threadIdx.x] = sub[k];
+    __syncthreads();
+    const int nS = gridDim.x, K = min(kSY, a.nseg - sblk() * kSY);
+    if (threadIdx.y < 2 && x < NL) {
+        // local chains with zero super carries: s_loc_k (forward, entering sub k) and
+        // T_loc_k (backward, entering sub k from above); e_S / b_S close them
+        const int pl = threadIdx.y;
+        float sl[kSY][3];
+        float r0 = 0.f, r1 = 0.f, r2 = 0.f;
+#pragma unroll
+        for (int k = 0; k < kSY; ++k) {
+            if (k >= K) break;
+            const float* p = sm + (k * 12 + 3 * pl) * kTX + threadIdx.x;
+            sl[k][0] = r0; sl[k][1] = r1; sl[k][2] = r2;
+            const float* Q = q.Q[sblk() * kSY + k == a.nseg - 1];
+            const float n0_ = fmaf(Q[0], r0, p[0]);
+            const float n1_ = fmaf(Q[1], r1, fmaf(-Q[2], r2, p[kTX]));
+            const float n2_ = fmaf(Q[1], r2, fmaf(Q[2], r1, p[2 * kTX]));
+            r0 = n0_; r1 = n1_; r2 = n2_;
+        }
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+        float* sb = a.state32 + ((int64_t)blockIdx.z * a.nseg + sblk() * kSY) * 12 * NL + x;  // sub 0 of this CTA
+#pragma unroll
+        for (int k = kSY - 1; k >= 0; --k) {
+            if (k >= K) continue;
+            float* d = sb + (int64_t)k * 12 * NL;
+            d[(int64_t)(3 * pl) * NL] = sl[k][0];
+            d[(int64_t)(3 * pl + 1) * NL] = sl[k][1];
+            d[(int64_t)(3 * pl + 2) * NL] = sl[k][2];
+            d[(int64_t)(6 + 3 * pl) * NL] = t0;
+            d[(int64_t)(7 + 3 * pl) * NL] = t1;
+            d[(int64_t)(8 + 3 * pl) * NL] = t2;
+            const float* p = sm + (k * 12 + 6 + 3 * pl) * kTX + threadIdx.x;
+            const int lt = sblk() * kSY + k == a.nseg - 1;
+            const float* Q = q.Q[lt];
+            const float* M = q.Mb[lt];
+            const float c0 = fmaf(M[0], sl[k][0], fmaf(M[1], sl[k][1], fmaf(M[2], sl[k][2], p[0])));
+            const float c1 = fmaf(M[3], sl[k][0], fmaf(M[4], sl[k][1], fmaf(M[5], sl[k][2], p[kTX])));
+            const float c2 = fmaf(M[6], sl[k][0], fmaf(M[7], sl[k][1], fmaf(M[8], sl[k][2], p[2 * kTX])));
+            const float n0_ = fmaf(Q[0], t0, c0);
+            const float n1_ = fmaf(Q[1], t1, fmaf(-Q[2], t2, c1));
+            const float n2_ = fmaf(Q[1], t2, fmaf(Q[2], t1, c2));
+            t0 = n0_; t1 = n1_; t2 = n2_;
+        }
+        float* su = a.state32 + ((int64_t)gridDim.z * a.nseg + (int64_t)blockIdx.z * nS + sblk()) * 12 * NL + x;
+        su[(int64_t)(3 * pl) * NL] = r0;
+        su[(int64_t)(3 * pl + 1) * NL] = r1;
+        su[(int64_t)(3 * pl + 2) * NL] = r2;
+        su[(int64_t)(6 + 3 * pl) * NL] = t0;
+        su[(int64_t)(7 + 3 * pl) * NL] = t1;
+        su[(int64_t)(8 + 3 * pl) * NL] = t2;
     }
     // arrival: the last CTA of this line block runs its carries
     // (the barrier orders the CTA's state writes before thread 0's cumulative
@@ -369,8 +437,9 @@ __global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const _
     unsigned dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     const int kCS = (int)(dyn / (12 * kCL * sizeof(float)));
-    carry_block(reinterpret_cast<float*>(smem), kCS, a.state32 + (int64_t)blockIdx.z * a.nseg * 12 * NL + x0, NL,
-                min(kTX, NL - x0), a.nseg, q);
+    carry_block(reinterpret_cast<float*>(smem), kCS,
+                a.state32 + ((int64_t)gridDim.z * a.nseg + (int64_t)blockIdx.z * nS) * 12 * NL + x0, NL, min(kTX, NL - x0),
+                nS, q, q.QS, q.MbS);
     if (threadIdx.x == 0 && threadIdx.y == 0) *cnt = 0;  // ready for the next launch
 }
 
@@ -397,10 +466,22 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
     extern __shared__ __align__(16) unsigned char smem[];
     const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
     const IirJob<float>& job = a.jobs[jb];
-    stage_tile<ROWS, CPLX>(smem, a, job, b, true);
     const int x = lblk() * kTX + threadIdx.x;
     const int seg = sblk() * kSY + threadIdx.y;
     const int len = a.len, P = a.P, L = len + 2 * P, NL = a.lines;
+    // carries of this segment: its local chains (s_loc, T_loc) and the super-segment carries (s_S, t_S)
+    float lc[12], sc[12];
+    {
+        const bool ok = x < NL && seg < a.nseg;
+        const float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
+        const float* su = a.state32 + ((int64_t)gridDim.z * a.nseg + (int64_t)blockIdx.z * gridDim.x + sblk()) * 12 * NL + x;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            lc[k] = ok ? st[(int64_t)k * NL] : 0.f;
+            sc[k] = ok ? su[(int64_t)k * NL] : 0.f;
+        }
+    }
+    stage_tile<ROWS, CPLX>(smem, a, job, b, true);
     const int n0 = seg * kM;
     const int m = min(kM, L - n0);
     const int i0 = threadIdx.y * kM;
@@ -408,23 +489,42 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
     const bool live = x < NL && n0 < L && n0 + m > P && n0 < P + len;
     // interior: a whole segment inside the crop (no per-sample checks)
     const bool interior = m == kM && n0 >= P && n0 + kM <= P + len;
-    const float* st = a.state32 + ((int64_t)blockIdx.z * a.nseg + seg) * 12 * NL + x;
     const float4* tabr = reinterpret_cast<const float4*>(smem) + kSW;  // [i]: output sample nb0 + i - P
     float2* tile = reinterpret_cast<float2*>(smem + kTabBytes);
     Sec t;
     if (live) {
         const In<ROWS, CPLX> in = make_in<ROWS, CPLX>(smem, job);
+        // true carries: s_in = QF s_S + s_loc,  t_in = QB t_S + T_loc + G s_S
+        const int kk = threadIdx.y, lt = sblk() == (int)gridDim.x - 1;
+        const float* QF = q.QF[kk];
+        const float* QB = q.QB[lt][kk];
+        const float* G = q.G[lt][kk];
+        float si[2][3], ti[2][3];
+#pragma unroll
+        for (int pl = 0; pl < 2; ++pl) {
+            const float* S = sc + 3 * pl;  // s_S of this plane
+            const float* T = sc + 6 + 3 * pl;
+            si[pl][0] = fmaf(QF[0], S[0], lc[3 * pl]);
+            si[pl][1] = fmaf(QF[1], S[1], fmaf(-QF[2], S[2], lc[3 * pl + 1]));
+            si[pl][2] = fmaf(QF[1], S[2], fmaf(QF[2], S[1], lc[3 * pl + 2]));
+            const float g0 = fmaf(G[0], S[0], fmaf(G[1], S[1], fmaf(G[2], S[2], lc[6 + 3 * pl])));
+            const float g1 = fmaf(G[3], S[0], fmaf(G[4], S[1], fmaf(G[5], S[2], lc[7 + 3 * pl])));
+            const float g2 = fmaf(G[6], S[0], fmaf(G[7], S[1], fmaf(G[8], S[2], lc[8 + 3 * pl])));
+            ti[pl][0] = fmaf(QB[0], T[0], g0);
+            ti[pl][1] = fmaf(QB[1], T[1], fmaf(-QB[2], T[2], g1));
+            ti[pl][2] = fmaf(QB[1], T[2], fmaf(QB[2], T[1], g2));
+        }
         Sec s;
         if (seg == 0) {
             sec_steady(s, in.z(0), q);
         } else {
-            s.r = make_float2(st[0], st[3 * (int64_t)NL]);
-            s.cr = make_float2(st[(int64_t)NL], st[4 * (int64_t)NL]);
-            s.ci = make_float2(st[2 * (int64_t)NL], st[5 * (int64_t)NL]);
+            s.r = make_float2(si[0][0], si[1][0]);
+            s.cr = make_float2(si[0][1], si[1][1]);
+            s.ci = make_float2(si[0][2], si[1][2]);
         }
-        t.r = make_float2(st[6 * (int64_t)NL], st[9 * (int64_t)NL]);
-        t.cr = make_float2(st[7 * (int64_t)NL], st[10 * (int64_t)NL]);
-        t.ci = make_float2(st[8 * (int64_t)NL], st[11 * (int64_t)NL]);
+        t.r = make_float2(ti[0][0], ti[1][0]);
+        t.cr = make_float2(ti[0][1], ti[1][1]);
+        t.ci = make_float2(ti[0][2], ti[1][2]);
         if (interior) fin_fwd<ROWS, CPLX, true>(in, i0, m, s, q);
         else fin_fwd<ROWS, CPLX, false>(in, i0, m, s, q);
     }
@@ -493,7 +593,10 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
 // ---- host: parallel-form parameters from the direct-form coefficients ----
 using cd = std::complex<double>;
 
-void iir32_params(const IirCoef& c, int mlast, Iir32Par* out) {
+// L = padded samples per line
+void iir32_params(const IirCoef& c, int L, Iir32Par* out) {
+    const int nseg = (L + kM - 1) / kM, mlast = L - (nseg - 1) * kM;
+    const int nS = (nseg + kSY - 1) / kSY, mlastS = L - (nS - 1) * kSW, Klast = nseg - (nS - 1) * kSY;
     // roots of z^3 + a1 z^2 + a2 z + a3 (Durand-Kerner, then Newton polish)
     auto poly = [&](cd z) { return ((z + c.a1) * z + c.a2) * z + c.a3; };
     cd r[3] = {cd(0.4, 0.9), cd(0.4, 0.9) * cd(0.4, 0.9), cd(0.4, 0.9) * cd(0.4, 0.9) * cd(0.4, 0.9)};
@@ -543,13 +646,12 @@ void iir32_params(const IirCoef& c, int mlast, Iir32Par* out) {
         p.wcr[i] = (float)wc.real();
         p.wci[i] = (float)wc.imag();
     }
-    const int ms[2] = {kM, mlast};
-    for (int t = 0; t < 2; ++t) {
-        const int m = ms[t];
+    // transfer q^m and Mb of a run of m samples: segments (kM, mlast) and super-segments (kSW, mlastS)
+    auto run = [&](int m, float* Q, float* Mb) {
         const cd Qr = std::pow(qr, m), Qc = std::pow(qc, m);
-        p.Q[t][0] = (float)Qr.real();
-        p.Q[t][1] = (float)Qc.real();
-        p.Q[t][2] = (float)Qc.imag();
+        Q[0] = (float)Qr.real();
+        Q[1] = (float)Qc.real();
+        Q[2] = (float)Qc.imag();
         // corr_i(s) = s_r qr^(i+1) + 2 (s_cr Re qc^(i+1) - s_ci Im qc^(i+1))
         double Mr[3] = {0, 0, 0};
         cd Mc[3] = {0.0, 0.0, 0.0};
@@ -563,9 +665,52 @@ void iir32_params(const IirCoef& c, int mlast, Iir32Par* out) {
             }
         }
         for (int k = 0; k < 3; ++k) {
-            p.Mb[t][k] = (float)Mr[k];
-            p.Mb[t][3 + k] = (float)Mc[k].real();
-            p.Mb[t][6 + k] = (float)Mc[k].imag();
+            Mb[k] = (float)Mr[k];
+            Mb[3 + k] = (float)Mc[k].real();
+            Mb[6 + k] = (float)Mc[k].imag();
+        }
+    };
+    run(kM, p.Q[0], p.Mb[0]);
+    run(mlast, p.Q[1], p.Mb[1]);
+    run(kSW, p.QS[0], p.MbS[0]);
+    run(mlastS, p.QS[1], p.MbS[1]);
+    // super-segment -> sub-segment expansion (3x3 operators on (r, c re, c im), in double)
+    using M3 = std::array<double, 9>;
+    auto mat = [](cd a, cd b) { return M3{a.real(), 0, 0, 0, b.real(), -b.imag(), 0, b.imag(), b.real()}; };
+    auto mul = [](const M3& A, const M3& B) {
+        M3 C{};
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+        return C;
+    };
+    M3 Mbd[2];
+    for (int t = 0; t < 2; ++t)
+        for (int k = 0; k < 9; ++k) Mbd[t][k] = p.Mb[t][k];
+    // (Mb recomputed in double would be marginally more exact; the fp32 copies are what pass 1 used)
+    for (int k = 0; k < kSY; ++k) {
+        const cd a = std::pow(qr, kM * k), b = std::pow(qc, kM * k);
+        p.QF[k][0] = (float)a.real();
+        p.QF[k][1] = (float)b.real();
+        p.QF[k][2] = (float)b.imag();
+    }
+    for (int t = 0; t < 2; ++t) {
+        const int K = t ? Klast : kSY;
+        for (int k = 0; k < kSY; ++k) {
+            cd ar(1.0, 0.0), bc(1.0, 0.0);  // prod_{j=k+1}^{K-1} q^{m_j}
+            M3 P = mat(1.0, 1.0), G{};       // running prod_{j=k+1}^{i-1} Q_j, accumulated G
+            for (int i = k + 1; i < K; ++i) {
+                const bool last = t && i == K - 1;
+                const int m = last ? mlast : kM;
+                const M3 term = mul(mul(P, Mbd[last ? 1 : 0]), mat(std::pow(qr, kM * i), std::pow(qc, kM * i)));
+                for (int e = 0; e < 9; ++e) G[e] += term[e];
+                P = mul(P, mat(std::pow(qr, m), std::pow(qc, m)));
+                ar *= std::pow(qr, m);
+                bc *= std::pow(qc, m);
+            }
+            p.QB[t][k][0] = (float)ar.real();
+            p.QB[t][k][1] = (float)bc.real();
+            p.QB[t][k][2] = (float)bc.imag();
+            for (int e = 0; e < 9; ++e) p.G[t][k][e] = (float)G[e];
         }
     }
 }
@@ -588,7 +733,8 @@ cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream
     const dim3 block(kTX, kSY);
     const dim3 grid((a.nseg + kSY - 1) / kSY, (a.lines + kTX - 1) / kTX, a.njobs * a.batch);
     // arrival counters (one int per 32-line block and job) after the states; zeroed once per launch
-    int* counters = reinterpret_cast<int*>(a.state32 + (int64_t)a.njobs * a.batch * a.nseg * 12 * a.lines);
+    const int64_t nS = grid.x;  // super-segments per line
+    int* counters = reinterpret_cast<int*>(a.state32 + (int64_t)a.njobs * a.batch * (a.nseg + nS) * 12 * a.lines);
     cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)grid.y * grid.z, s);
     static const bool nocarry = std::getenv("FGB_IIR32_NOCARRY") != nullptr;
     iir32_sum<ROWS, CPLX><<<grid, block, ssmem, s>>>(a, q, nocarry ? nullptr : counters);
@@ -610,11 +756,11 @@ cudaError_t launch_iir32(const IirArgs<float>& a_in, cudaStream_t s) {
     a.state32 = reinterpret_cast<float*>(a.state);
     // parameters per (coefficients, last segment length), computed once (launches are serialised by the engine lock)
     static std::map<std::array<double, 5>, Iir32Par> cache;
-    const std::array<double, 5> key = {a.c.B, a.c.a1, a.c.a2, a.c.a3, (double)(L - (a.nseg - 1) * kM)};
+    const std::array<double, 5> key = {a.c.B, a.c.a1, a.c.a2, a.c.a3, (double)L};
     auto it = cache.find(key);
     if (it == cache.end()) {
         Iir32Par p;
-        iir32_params(a.c, L - (a.nseg - 1) * kM, &p);
+        iir32_params(a.c, L, &p);
         it = cache.emplace(key, p).first;
     }
     const Iir32Par& q = it->second;
