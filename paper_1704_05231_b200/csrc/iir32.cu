@@ -20,18 +20,26 @@
 // slots on B200: tools/probes/f64_probe.cu).  Measured emulation error vs
 // the fp64 reference: <= 2e-6 (sigma = 32), see DESIGN.md §4.
 //
-// Segment parallelism is exact.  A line is cut into segments of kM samples.
+// Segment parallelism is exact.  A line is cut into segments of kM = 32
+// samples; a CTA owns 32 lines x kSY = 4 consecutive segments (a
+// "super-segment") of one job, with the input tile and the trig tables
+// staged in shared memory (cp.async).
 //   pass 1 (iir32_sum): per segment, modulate and run the forward sections
-//     from a zero state (segment 0: the true init); keep the end state e and
-//     the backward-start sums b = sum_i c q^i y_loc[n0 + i] (the start state
-//     the backward sections would reach over this segment's local output).
-//   carry (iir32_carry): per line, forward s_in[j+1] = q^m s_in[j] + e[j];
-//     the backward init from the true y[L-1]; then backward
-//     t_in[j-1] = q^m t_in[j] + b[j] + Mb s_in[j]   (Mb: the backward-start
-//     response to a forward carry-in, host-computed).
-//   pass 2 (iir32_fin): per segment, forward sections from the true s_in
-//     (exact y, kept in registers), backward sections from the true t_in,
-//     recombination, outputs.
+//     from a zero state (segment 0: the true init); the end state e and the
+//     backward-start sums b = sum_i c q^i y_loc[n0 + i] (the start state the
+//     backward sections would reach over this segment's local output).  The
+//     CTA folds its 4 segments into super-segment summaries (e_S, b_S) and
+//     keeps each segment's local chains (s_loc, T_loc).
+//   carries: the last CTA of a 32-line block to finish (arrival counter)
+//     scans the block's super-segments: s_in[j+1] = q^m s_in[j] + e[j]; the
+//     backward init from the true y[L-1]; t_in[j-1] = q^m t_in[j] + b[j] +
+//     Mb s_in[j]  (Mb: the backward-start response to a forward carry-in,
+//     host-computed).  The scans overlap the rest of pass 1.
+//   pass 2 (iir32_fin): per segment, its true carries from the super ones
+//     (s_in = QF s_S + s_loc, t_in = QB t_S + T_loc + G s_S, host-computed
+//     operators), forward sections from s_in (exact y, written over the
+//     thread's own tile slots), backward sections from t_in, recombination,
+//     outputs.
 // Lines are adjacent threads; the horizontal stage (lines = image rows)
 // stages its rows through shared memory both ways.
 #include <algorithm>
