@@ -271,6 +271,52 @@ __device__ __forceinline__ void col_accumulate2(const float4* tb, WF wts, int nt
     }
 }
 
+// Real-J variant (ColJob::realj): A and B of the two columns from Re J only,
+// (A0, A1) += ka (J0r, J1r), (B0, B1) += kb (J0r, J1r) -- two FFMA2 per tap
+// and row instead of four.
+template <int R, int REM, int RS, typename WF>
+__device__ __forceinline__ void col_accumulate2_real(const float4* tb, WF wts, int nt, float2 (&A)[R], float2 (&Bv)[R]) {
+    const int nfull = (nt - REM) / R;
+#pragma unroll 1
+    for (int c = 0; c < nfull; ++c) {
+        float2 v[2 * R - 1];
+#pragma unroll
+        for (int m = 0; m < 2 * R - 1; ++m) {
+            const float4 q = tb[(c * R + m) * RS];
+            v[m] = make_float2(q.x, q.z);
+        }
+#pragma unroll
+        for (int tt = 0; tt < R; ++tt) {
+            const float2 w = wts(c * R + tt);
+            const float2 wa = make_float2(w.x, w.x), wb = make_float2(w.y, w.y);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                A[r] = __ffma2_rn(wa, v[r + tt], A[r]);
+                Bv[r] = __ffma2_rn(wb, v[r + tt], Bv[r]);
+            }
+        }
+    }
+    if constexpr (REM > 0) {
+        const int c = nfull;
+        float2 v[R + REM - 1];
+#pragma unroll
+        for (int m = 0; m < R + REM - 1; ++m) {
+            const float4 q = tb[(c * R + m) * RS];
+            v[m] = make_float2(q.x, q.z);
+        }
+#pragma unroll
+        for (int tt = 0; tt < REM; ++tt) {
+            const float2 w = wts(c * R + tt);
+            const float2 wa = make_float2(w.x, w.x), wb = make_float2(w.y, w.y);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                A[r] = __ffma2_rn(wa, v[r + tt], A[r]);
+                Bv[r] = __ffma2_rn(wb, v[r + tt], Bv[r]);
+            }
+        }
+    }
+}
+
 // CP = column pairs per CTA (16 -> 32 columns, 8 -> 16 columns for long
 // kernels whose (S + nt - 1)-row tile would otherwise limit occupancy).
 template <int REM, int CAP, int CP>
@@ -351,6 +397,33 @@ __global__ void __launch_bounds__(128) col_kernel2(const __grid_constant__ ColAr
     }
 
     float2* dst = a.dst_base + (size_t)b * a.dst_bstride + x;
+    if (jb->realj) {  // theta = pi/2 (mode 1, has_b): X = A - iB from Re J
+        for (int ch = 0; ch < nch; ++ch) {
+            cp_async_wait_pending(min(nch - 1 - ch, 7));
+            __syncthreads();
+            float2 A2[R], B2[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) { A2[r] = make_float2(0.f, 0.f); B2[r] = make_float2(0.f, 0.f); }
+            const float4* tb = tile + (ch * TY + rg * R) * CP + cx;
+            if constexpr (CAP > 0) {
+                const int pbase = job * nt;
+                col_accumulate2_real<R, REM, CP>(tb, [&](int i) { return pw.w[pbase + i]; }, nt, A2, B2);
+            } else {
+                col_accumulate2_real<R, REM, CP>(tb, [&](int i) { return wts[i]; }, nt, A2, B2);
+            }
+            if (x < W) {
+                float2* d0 = dst + doff[0];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int yl = ch * TY + rg * R + r;
+                    if (yl >= rows_out) break;
+                    __stcs(reinterpret_cast<float4*>(d0 + (size_t)(ys + yl) * W),
+                           make_float4(A2[r].x, -B2[r].x, A2[r].y, -B2[r].y));
+                }
+            }
+        }
+        return;
+    }
     for (int ch = 0; ch < nch; ++ch) {
         cp_async_wait_pending(min(nch - 1 - ch, 7));
         __syncthreads();

@@ -59,6 +59,9 @@ template <typename T> struct ColJob {
     int8_t conj[4];
     int32_t has_b;           // kb != 0 (0 for the theta = 0 / v = 0 jobs: A only)
     int32_t mode;            // epilogue: 0 generic, 1 Gabor X only, 2 Gabor X + conj(Y) (no phase)
+    int32_t realj;           // fp32 kernel, mode 1: J is real to ~1e-12 (theta = pi/2: the row phase step
+                             // omega cos(theta) ~ 1e-17), so A and B read only Re J (half the FMAs)
+    int32_t pad_;
 };
 
 // Row job group: up to kMaxND jobs sharing one input row and one symmetric

@@ -785,6 +785,11 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 if (jobs[j].out_direct >= 0) outs.push_back({jobs[j].out_direct, 0, 0, cd(1, 0)});
                 if (jobs[j].out_mirror >= 0) outs.push_back({jobs[j].out_mirror, 1, 1, cd(1, 0)});
                 ColJob<T> job = b.col_job(col_only ? 0 : ws_j0 + (int64_t)j * HW, wo, outs, jobs[j].ws != 0.0);
+                // theta = pi/2: the row stage's phase step omega cos(theta) ~ 1e-17 leaves Im J at
+                // ~1e-12 of |J| or less, so the fp32 column kernel reads Re J only (half the FMAs)
+                if (sizeof(T) == 4 && !col_only && !box && job.mode == 1 && job.has_b &&
+                    std::fabs(jobs[j].wc) * (W + 2.0 * (h + 1)) < 1e-12 && !std::getenv("FGB_NO_REALJ"))
+                    job.realj = 1;
                 // theta = 0 (ws = 0) jobs need A only (half the work): they share the
                 // launch (per-CTA branch) and go last so heavy CTAs start first
                 if (jobs[j].ws == 0.0) cj_nob.push_back(job);
