@@ -158,6 +158,8 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
         }
     }
     unsigned char* tile = smem + kTabBytes;
+    // tile samples [nb0, nb0 + kSW) need no clamping when they map into [0, len)
+    const bool inner = nb0 >= P && nb0 + kSW <= P + len;
     if constexpr (ROWS) {
         constexpr int swp = kSW | 1;
         const float* base = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
@@ -166,19 +168,47 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
             const int line = lblk() * kTX + r;
             if (line >= a.lines) continue;
             const float* row = base + (int64_t)line * a.src_ls;
-            for (int cc = threadIdx.x; cc < kSW; cc += kTX) {
-                const int n = nb0 + cc;
-                if (n < L) cp_async4(t + r * swp + cc, row + clampi(n - P, 0, len - 1));
+            if (inner) {
+                const float* rp = row + (nb0 - P) + threadIdx.x;
+#pragma unroll
+                for (int k = 0; k < kSW / kTX; ++k) cp_async4(t + r * swp + threadIdx.x + k * kTX, rp + k * kTX);
+            } else {
+                for (int cc = threadIdx.x; cc < kSW; cc += kTX) {
+                    const int n = nb0 + cc;
+                    if (n < L) cp_async4(t + r * swp + cc, row + clampi(n - P, 0, len - 1));
+                }
             }
         }
     } else {
         const int x = min(lblk() * kTX + threadIdx.x, a.lines - 1);
         if constexpr (CPLX) {
-            const float2* src = reinterpret_cast<const float2*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + x;
+            const float2* blk = reinterpret_cast<const float2*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride +
+                                lblk() * kTX;
             float2* t = reinterpret_cast<float2*>(tile);
+            // a whole 32-line block: each sample row is one contiguous 256-byte run -> one bulk copy per row
+            const bool bulk = lblk() * kTX + kTX <= a.lines && (a.src_ss & 1) == 0 &&
+                              ((reinterpret_cast<uintptr_t>(blk) & 15) == 0);
+            if (bulk) {
+                __shared__ alignas(8) uint64_t bar;
+                const int nrows = min(kSW, L - nb0);
+                if (tid == 0) {
+                    mbar_init(&bar, 1);
+                    mbar_arrive_expect_tx(&bar, (unsigned)(nrows * kTX * sizeof(float2)));
+                }
+                __syncthreads();
+                if (tid < nrows)
+                    bulk_g2s(t + tid * kTX, blk + (int64_t)clampi(nb0 + tid - P, 0, len - 1) * a.src_ss,
+                             kTX * sizeof(float2), &bar);
+                mbar_wait(&bar, 0);
+                __syncthreads();  // (tables)
+                return;
+            }
+            const float2* src = blk + threadIdx.x;
+            (void)x;
             for (int cc = threadIdx.y; cc < kSW; cc += kSY) {
                 const int n = nb0 + cc;
-                if (n < L) cp_async8(t + cc * kTX + threadIdx.x, src + (int64_t)clampi(n - P, 0, len - 1) * a.src_ss);
+                if (n < L && lblk() * kTX + threadIdx.x < a.lines)
+                    cp_async8(t + cc * kTX + threadIdx.x, src + (int64_t)clampi(n - P, 0, len - 1) * a.src_ss);
             }
         } else {
             const float* src = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride + x;
