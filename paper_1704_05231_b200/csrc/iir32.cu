@@ -461,7 +461,6 @@ __global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const _
     // (the barrier orders the CTA's state writes before thread 0's cumulative
     // gpu-scope fence; only one thread pays the membar)
     __shared__ int last;
-    if (!counters) return;  // timing experiment only (FGB_IIR32_NOCARRY): no carries
     __syncthreads();
     int* cnt = counters + (int64_t)blockIdx.z * gridDim.y + lblk();
     if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -755,16 +754,12 @@ void iir32_params(const IirCoef& c, int L, Iir32Par* out) {
 
 template <bool ROWS, bool CPLX>
 cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream_t s) {
+    // (pass 1's carry scans stage their states in chunks of what the tile
+    // leaves: reserving room for a single chunk cost more in occupancy)
     constexpr size_t smem = Tile<ROWS, CPLX>::smem;
-    // pass 1 also stages the carry scan of its line block: room for every
-    // segment when that is <= kCarrySegs (one load / store round trip),
-    // else chunks of what the tile leaves
-    static const int carry_segs = std::getenv("FGB_IIR32_CARRY_SEGS") ? std::atoi(std::getenv("FGB_IIR32_CARRY_SEGS")) : 0;
-    const size_t csmem = (size_t)std::min(a.nseg, carry_segs) * 12 * kCL * sizeof(float);
-    const size_t ssmem = std::max(smem, csmem);
     static bool attr = false;  // launches are serialised by the engine lock
     if (!attr) {
-        cudaFuncSetAttribute(iir32_sum<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(iir32_sum<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(iir32_fin<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
@@ -774,8 +769,7 @@ cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream
     const int64_t nS = grid.x;  // super-segments per line
     int* counters = reinterpret_cast<int*>(a.state32 + (int64_t)a.njobs * a.batch * (a.nseg + nS) * 12 * a.lines);
     cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)grid.y * grid.z, s);
-    static const bool nocarry = std::getenv("FGB_IIR32_NOCARRY") != nullptr;
-    iir32_sum<ROWS, CPLX><<<grid, block, ssmem, s>>>(a, q, nocarry ? nullptr : counters);
+    iir32_sum<ROWS, CPLX><<<grid, block, smem, s>>>(a, q, counters);
     iir32_fin<ROWS, CPLX><<<grid, block, smem, s>>>(a, q);
     return cudaGetLastError();
 }
