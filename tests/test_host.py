@@ -197,6 +197,9 @@ def test_images_and_conjugate(fg):
         fg.RealImage.from_array(np.array([[np.nan]]))
     with pytest.raises(ValueError):
         fg.RealImage.from_array(np.zeros(3))
+    for empty in (np.zeros((0, 5)), np.zeros((5, 0))):  # image_io.py:33,59
+        with pytest.raises(ValueError, match="at least 1x1"):
+            fg.RealImage.from_array(empty)
 
 
 def test_complex_image_from_planar(fg):
