@@ -60,9 +60,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// (the suspend-time hint parks the waiting warps instead of spinning on issue slots)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
     asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n @!p bra WAIT_%=;\n}\n" ::"r"(
             smem_u32(bar)),
         "r"(phase)
         : "memory");

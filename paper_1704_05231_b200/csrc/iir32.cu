@@ -164,18 +164,21 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
         constexpr int swp = kSW | 1;
         const float* base = reinterpret_cast<const float*>(a.src_base) + job.src_off + (int64_t)b * a.src_bstride;
         float2* t = reinterpret_cast<float2*>(tile);
-        for (int r = threadIdx.y; r < kTX; r += kSY) {
-            const int line = lblk() * kTX + r;
-            if (line >= a.lines) continue;
-            const float* row = base + (int64_t)line * a.src_ls;
+        // lanes along the row (coalesced), warps over rows; pointers step by 4 rows
+        const int line0 = lblk() * kTX + threadIdx.y;
+        const float* row = base + (int64_t)line0 * a.src_ls;
+        float2* d = t + threadIdx.y * swp + threadIdx.x;
+        const int64_t rstep = (int64_t)kSY * a.src_ls;
+        for (int r = threadIdx.y; r < kTX && lblk() * kTX + r < a.lines; r += kSY, row += rstep, d += kSY * swp) {
             if (inner) {
                 const float* rp = row + (nb0 - P) + threadIdx.x;
 #pragma unroll
-                for (int k = 0; k < kSW / kTX; ++k) cp_async4(t + r * swp + threadIdx.x + k * kTX, rp + k * kTX);
+                for (int k = 0; k < kSW / kTX; ++k) cp_async4(d + k * kTX, rp + k * kTX);
             } else {
-                for (int cc = threadIdx.x; cc < kSW; cc += kTX) {
-                    const int n = nb0 + cc;
-                    if (n < L) cp_async4(t + r * swp + cc, row + clampi(n - P, 0, len - 1));
+#pragma unroll
+                for (int k = 0; k < kSW / kTX; ++k) {
+                    const int n = nb0 + threadIdx.x + k * kTX;
+                    if (n < L) cp_async4(d + k * kTX, row + clampi(n - P, 0, len - 1));
                 }
             }
         }
