@@ -585,13 +585,20 @@ __global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const _
             }
         }
         __syncthreads();
-        float2* dst = a.dst_base + job.dst_off[0] + (int64_t)b * a.dst_bstride;
-        for (int r = threadIdx.y; r < kTX; r += kSY) {
-            const int line = lblk() * kTX + r;
-            if (line >= NL) continue;
-            float2* row = dst + (int64_t)line * a.dst_ls - P;
-            const int c0 = max(0, P - nb0), c1 = min(kSW, min(P + len, L) - nb0);
-            for (int cc = c0 + threadIdx.x; cc < c1; cc += kTX) __stcs(row + nb0 + cc, otile[r * swp + cc]);
+        // row-contiguous write-out (lanes along the row), pointers stepped per row
+        const int c0 = max(0, P - nb0), c1 = min(kSW, min(P + len, L) - nb0);
+        float2* row = a.dst_base + job.dst_off[0] + (int64_t)b * a.dst_bstride +
+                      (int64_t)(lblk() * kTX + threadIdx.y) * a.dst_ls - P + nb0;
+        const float2* orow = otile + threadIdx.y * swp;
+        const int64_t rstep = (int64_t)kSY * a.dst_ls;
+        if (c0 == 0 && c1 == kSW) {
+            for (int r = threadIdx.y; r < kTX && lblk() * kTX + r < NL; r += kSY, row += rstep, orow += kSY * swp) {
+#pragma unroll
+                for (int k = 0; k < kSW / kTX; ++k) __stcs(row + threadIdx.x + k * kTX, orow[threadIdx.x + k * kTX]);
+            }
+        } else {
+            for (int r = threadIdx.y; r < kTX && lblk() * kTX + r < NL; r += kSY, row += rstep, orow += kSY * swp)
+                for (int cc = c0 + threadIdx.x; cc < c1; cc += kTX) __stcs(row + cc, orow[cc]);
         }
     } else {
         if (!live) return;
