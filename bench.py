@@ -384,6 +384,11 @@ def run_ours(args, cfg, rank, world, local_rank):
                     "frac": ach / fp32 if fp32 > 0 else None, "traffic": traffic,
                     "algorithmic_flops_per_launch": top["flops"] / top["launches"],
                     "peak_source": "live FFMA probe (fgb_probe_fp32_tflops); flops = reference OpCounters M+A"}
+            if top["name"] == "iir":
+                roof["note"] = ("RecursiveIIR stage (iir32_sum + iir32_fin): the reference counts ~12 flops per "
+                                "output and plane, the exact segment-parallel fp32 recursion issues ~36 FMA per "
+                                "sample and plane in two passes; its ncu FMA-pipe utilisation (32-44%) is in "
+                                "profiles/r01/ncu_full_summary.txt")
     # whole-step roofline: algorithmic work of one step (sum over every launch, from the
     # profile pass) / measured step time of the timed region
     step_roof = None
