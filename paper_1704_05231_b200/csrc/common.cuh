@@ -98,7 +98,8 @@ template <typename T> struct RowGroup {
     int32_t wofs;            // offset (in T units) of the [(hp+1)][NDP][2] table
     int32_t nd;
     int32_t has_phase;
-    int32_t pad_;
+    int32_t last_real;       // fp32: the last job's J is real to <= 1e-12 |J| (theta = pi/2, row phase step
+                             // omega cos(theta) ~ 1e-17): its taps accumulate Re J only (scalar FFMA)
 };
 
 }  // namespace fgb

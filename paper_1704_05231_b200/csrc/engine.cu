@@ -422,6 +422,10 @@ template <typename T> struct Builder {
         st.rg.wofs = (int32_t)p.wrow.size();
         st.rg.nd = nd;
         st.rg.has_phase = 0;
+        // theta = pi/2 (last direct of a Gabor group): the phase step omega cos(theta) ~ 1e-17 leaves
+        // Im J <= 1e-12 |J|, so the fp32 kernel accumulates Re J only (the column pass reads Re J, realj)
+        st.rg.last_real = sizeof(T) == 4 && std::fabs(freq[nd - 1]) * (W + 2.0 * (h + 1)) < 1e-12 &&
+                          phase[nd - 1] == cd(1.0, 0.0) && !std::getenv("FGB_NO_REALJ");
         for (int k = 0; k < nd; ++k) {
             st.rg.dst_off[k] = dst_off[k];
             st.rg.phase_re[k] = (T)phase[k].real();

@@ -55,7 +55,7 @@ template <typename T> __host__ __device__ constexpr bool row_vec(int nd) { retur
 // CAP > 0: the group's tap table travels in the kernel parameters (constant
 // bank) so the FFMA multipliers are uniform-register operands; CAP == 0:
 // table staged in shared memory.
-template <typename T, int ND, int CAP>
+template <typename T, int ND, int CAP, bool LR>
 __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_constant__ RowArgs<T> a,
                                                                   const __grid_constant__ RowGroup<T> g,
                                                                   const __grid_constant__ RowWParam<T, CAP> pw) {
@@ -179,7 +179,9 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
                 const C sd = mk<T>(p + m, p - m);
 #pragma unroll
                 for (int k = 0; k < ND; ++k) {
-                    if constexpr (sizeof(T) == 4) {
+                    if (LR && k == ND - 1) {  // real J (RowGroup::last_real): Im stays 0
+                        acc[k][r].x = fma(wr[k], sd.x, acc[k][r].x);
+                    } else if constexpr (sizeof(T) == 4) {
                         acc[k][r] = __ffma2_rn(make_float2(wr[k], wi[k]), sd, acc[k][r]);
                     } else {
                         acc[k][r].x = fma(wr[k], sd.x, acc[k][r].x);
@@ -233,10 +235,10 @@ template <typename T> size_t row_sym_smem(int hp, int nd, bool taps_in_smem) {
 
 template <typename T> int row_sym_pad(int h) { return (h + kRowR - 1) / kRowR * kRowR; }
 
-template <typename T, int ND, int CAP>
+template <typename T, int ND, int CAP, bool LR = false>
 static cudaError_t launch_cap(const RowArgs<T>& a, const RowGroup<T>& g, const T* pw_host, cudaStream_t s) {
     const size_t smem = row_sym_smem<T>(a.hp, ND, CAP == 0);
-    auto kern = row_sym_kernel<T, ND, CAP>;
+    auto kern = row_sym_kernel<T, ND, CAP, LR>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -254,6 +256,12 @@ template <typename T, int ND>
 static cudaError_t launch_nd(const RowArgs<T>& a, const RowGroup<T>& g, const T* pw_host, cudaStream_t s) {
     constexpr int NDP = (ND + 1) & ~1;
     const size_t need = (size_t)(a.hp + 1) * NDP * 2;
+    if constexpr (sizeof(T) == 4) {
+        if (g.last_real && pw_host && need <= (size_t)RowWCap<T>::kSmall)
+            return launch_cap<T, ND, RowWCap<T>::kSmall, true>(a, g, pw_host, s);
+        if (g.last_real && pw_host && need <= (size_t)RowWCap<T>::kLarge)
+            return launch_cap<T, ND, RowWCap<T>::kLarge, true>(a, g, pw_host, s);
+    }
     if (pw_host && need <= (size_t)RowWCap<T>::kSmall) return launch_cap<T, ND, RowWCap<T>::kSmall>(a, g, pw_host, s);
     if (pw_host && need <= (size_t)RowWCap<T>::kLarge) return launch_cap<T, ND, RowWCap<T>::kLarge>(a, g, pw_host, s);
     return launch_cap<T, ND, 0>(a, g, nullptr, s);
