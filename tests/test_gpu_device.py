@@ -1,5 +1,6 @@
 """GPU: device-tensor API, sharded (compact) layouts, fused-vs-separable SDFT,
-large-sigma IIR in fp32 (fp64 recursion state), batch handling."""
+large-sigma IIR in fp32 (parallel-form sections; the fp64-state direct form
+kept behind FGB_IIR64), batch handling."""
 
 import math
 import os
@@ -77,7 +78,8 @@ def test_sdft_fused_matches_separable_and_oracle(env, m, sigma, radius):
 
 
 def test_iir_large_sigma_f32(env):
-    """fp32 storage with fp64 recursion state meets 1e-5 at sigma = 16, 32."""
+    """The fp32 build's parallel-form sections (iir32.cu) meet 1e-5 at sigma = 16, 32, where a
+    direct-form fp32 recursion misses it by up to 125x."""
     torch, fg, D, P = env
     fimg = random_image(6, 200, 0.0, 1.0, width=120)
     for sigma in (16.0, 32.0):
@@ -85,6 +87,31 @@ def test_iir_large_sigma_f32(env):
         out = fg.gabor_filter(fg.RealImage.from_array(fimg), p, fg.RecursiveIIR(), fg.OpCounters(), precision="f32")
         ref = O.gabor_filter(fimg, p.omega, p.theta, sigma, ("iir",))
         assert max_rel_err(out, ref) <= 1e-5
+
+
+def test_iir_fp64_state_alternative_f32():
+    """FGB_IIR64=1 switches the fp32 build to the direct-form kernels with fp64 state (iir.cu);
+    read once per process, so the check runs in a subprocess: a bank and an SDFT vs the oracle."""
+    import subprocess
+    import sys
+
+    code = (
+        "import math, numpy as np, sys; sys.path.insert(0, '.');"
+        "import paper_1704_05231_b200 as fg; from oracle import fastgabor_oracle as O;"
+        "f = np.random.default_rng(4).uniform(0, 1, size=(90, 130));"
+        "spec = fg.BankSpec((math.pi / 4, math.pi / 16), 8, (4.0, 16.0));"
+        "out = fg.compute_bank(fg.RealImage.from_array(f), spec, fg.RecursiveIIR(), fg.OpCounters(), precision='f32');"
+        "ref = O.compute_bank(f, spec.frequencies, 8, spec.sigmas, ('iir',));"
+        "w = max(O.max_rel_err((e.re, e.im), r[3:]) for (_, e), r in zip(out.entries, ref));"
+        "sd = fg.sdft_full(fg.RealImage.from_array(f), fg.SdftSpec(8, 8, fg.RecursiveIIR(), 2.0), fg.OpCounters(), precision='f32');"
+        "bins = O.sdft_full(f, 8, 8, ('iir',), 2.0);"
+        "w2 = max(O.max_rel_err((sd.bins[u][v].re, sd.bins[u][v].im), bins[u][v]) for u in range(8) for v in range(8));"
+        "print(w, w2); assert w <= 1e-5 and w2 <= 1e-5"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, FGB_IIR64="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 def test_batched_bank_equals_per_image(env):

@@ -155,7 +155,7 @@ def test_config2_full_f32(fg):
 
 def test_config2_full_iir_f32(fg):
     """Config 2's image and bank with RecursiveIIR (the reference CLI's default
-    smoother) at full size, fp32 build (fp64 recursion state) vs the oracle's
+    smoother) at full size, fp32 build (parallel-form sections) vs the oracle's
     float64 lfilter restatement: every frequency, a direct / mirror pair and the
     theta = pi/2 entry (the near-DC row pass, SURVEY App. B's worst case)."""
     import scipy.ndimage as ndi
