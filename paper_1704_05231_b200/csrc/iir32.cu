@@ -294,7 +294,7 @@ __device__ __forceinline__ void carry_io(float* sm, float* g, int64_t NL, int j0
                 float* gp = g + (int64_t)(j0 + jj) * 12 * NL + l;
                 float* sp = sm + jj * 12 * kCL + l;
                 for (int k = k0 + grp; k < k1; k += 4) {
-                    if (load) cp_async4(sp + k * kCL, gp + (int64_t)k * NL);
+                    if (load) sp[k * kCL] = __ldcg(gp + (int64_t)k * NL);  // L2 (other CTAs' states)
                     else gp[(int64_t)k * NL] = sp[k * kCL];
                 }
             }
