@@ -1467,8 +1467,9 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                 pr.e1 = pool_event();
                 cudaEventRecord(pr.e0, s);
             }
-            // kernels per step: IIR = sum, carry, fin (fp32 parallel form) or fwd, scan, bwd, scan, out
-            g_launches += st.kind == ST_IIR ? ((sizeof(T) == 4 && iir32_enabled()) ? 3 : 5) : 1;
+            // kernels per step: IIR = sum (with the carry scans), fin (fp32 parallel form; plus a
+            // driver memset of the arrival counters, not counted) or fwd, scan, bwd, scan, out
+            g_launches += st.kind == ST_IIR ? ((sizeof(T) == 4 && iir32_enabled()) ? 2 : 5) : 1;
             switch (st.kind) {
                 case ST_ROW: {
                     RowArgs<T> a{};
