@@ -278,9 +278,10 @@ constexpr int kCL = kTX;
 __device__ __forceinline__ void carry_io(float* sm, float* g, int64_t NL, int j0, int nj, int nl, int k0, int k1, bool load) {
     const int tid = threadIdx.y * kTX + threadIdx.x;
     if (nl == kCL && (NL & 3) == 0) {  // 16-byte runs: thread = 4 lines of one (segment, slot)
-        const int l4 = (tid & 7) * 4, r0 = tid >> 3;  // 16 row groups
+        constexpr int kGroups = kTX * kSY / 8;  // row groups of 8 threads
+        const int l4 = (tid & 7) * 4, r0 = tid >> 3;
         const int nk = k1 - k0;
-        for (int r = r0; r < nj * nk; r += 16) {
+        for (int r = r0; r < nj * nk; r += kGroups) {
             const int jj = r / nk, k = k0 + r - jj * nk;
             float* gp = g + ((int64_t)(j0 + jj) * 12 + k) * NL + l4;
             float* sp = sm + (jj * 12 + k) * kCL + l4;
@@ -293,7 +294,7 @@ __device__ __forceinline__ void carry_io(float* sm, float* g, int64_t NL, int j0
             for (int jj = 0; jj < nj; ++jj) {
                 float* gp = g + (int64_t)(j0 + jj) * 12 * NL + l;
                 float* sp = sm + jj * 12 * kCL + l;
-                for (int k = k0 + grp; k < k1; k += 4) {
+                for (int k = k0 + grp; k < k1; k += kSY) {
                     if (load) sp[k * kCL] = __ldcg(gp + (int64_t)k * NL);  // L2 (other CTAs' states)
                     else gp[(int64_t)k * NL] = sp[k * kCL];
                 }
@@ -377,7 +378,7 @@ __device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, in
 }
 
 template <bool ROWS, bool CPLX>
-__global__ void __launch_bounds__(128) iir32_sum(const IirArgs<float> a, const __grid_constant__ Iir32Par q, int* counters) {
+__global__ void __launch_bounds__(kTX * kSY) iir32_sum(const IirArgs<float> a, const __grid_constant__ Iir32Par q, int* counters) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
     const IirJob<float>& job = a.jobs[jb];
@@ -502,7 +503,7 @@ __device__ __forceinline__ void fin_bwd(const float2* tile, int i0, int m, Sec& 
 }
 
 template <bool ROWS, bool CPLX>
-__global__ void __launch_bounds__(128) iir32_fin(const IirArgs<float> a, const __grid_constant__ Iir32Par q) {
+__global__ void __launch_bounds__(kTX * kSY) iir32_fin(const IirArgs<float> a, const __grid_constant__ Iir32Par q) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
     const IirJob<float>& job = a.jobs[jb];
