@@ -18,7 +18,7 @@
 // the recursion runs in fp32 FFMA2 (planes a and b of a modulation pair
 // packed), with no fp32 <-> fp64 conversions (each costs ~4 DFMA issue
 // slots on B200: tools/probes/f64_probe.cu).  Measured emulation error vs
-// the fp64 reference: <= 2e-6 (sigma = 32), see DESIGN.md §4.
+// the fp64 reference: <= 2e-6 (sigma = 32, tests/test_iir_parallel_form.py).
 //
 // Segment parallelism is exact.  A line is cut into segments of kM = 32
 // samples; a CTA owns 32 lines x kSY = 4 consecutive segments (a
