@@ -199,8 +199,8 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
                     mbar_arrive_expect_tx(&bar, (unsigned)(nrows * kTX * sizeof(float2)));
                 }
                 __syncthreads();
-                if (tid < nrows)
-                    bulk_g2s(t + tid * kTX, blk + (int64_t)clampi(nb0 + tid - P, 0, len - 1) * a.src_ss,
+                for (int r = tid; r < nrows; r += kTX * kSY)
+                    bulk_g2s(t + r * kTX, blk + (int64_t)clampi(nb0 + r - P, 0, len - 1) * a.src_ss,
                              kTX * sizeof(float2), &bar);
                 mbar_wait(&bar, 0);
                 __syncthreads();  // (tables)
