@@ -177,6 +177,19 @@ def test_config2_full_iir_f32(fg):
     assert worst <= TOL32, worst
 
 
+def test_iir_sigma32_full_size_f32(fg):
+    """RecursiveIIR at sigma = 32 (config 3 / 5's widest filter) on a 1024^2 image, fp32 build:
+    the parallel-form sections keep ~2.7x margin to 1e-5 (worst: theta = pi/2, the near-DC
+    row stage; measured 1.6e-6 / 2.5e-6 / 3.7e-6 at theta = 0 / 3pi/8 / pi/2)."""
+    f = np.random.default_rng(100).uniform(0.0, 1.0, size=(1024, 1024)).astype(np.float32).astype(np.float64)
+    worst = 0.0
+    for th in (0.0, 3 * math.pi / 8, math.pi / 2):
+        p = fg.GaborParams(math.pi / 32, th, 32.0)
+        out = fg.gabor_filter(fg.RealImage.from_array(f), p, fg.RecursiveIIR(), fg.OpCounters(), precision="f32")
+        worst = max(worst, max_rel_err(out, O.gabor_filter(f, p.omega, p.theta, 32.0, ("iir",))))
+    assert worst <= TOL32, worst
+
+
 def test_config2_full_f64_validation_build(fg):
     """The fp64 validation build at config 2's full size: every frequency's
     direct / mirror pair and theta = pi/2 vs the float64 oracle at 1e-10."""
