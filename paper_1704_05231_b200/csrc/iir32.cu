@@ -23,7 +23,8 @@
 // Segment parallelism is exact.  A line is cut into segments of kM = 32
 // samples; a CTA owns 32 lines x kSY = 4 consecutive segments (a
 // "super-segment") of one job, with the input tile and the trig tables
-// staged in shared memory (cp.async).
+// staged in shared memory (column stages: one bulk async copy per 256-byte
+// sample row, completing on an mbarrier; row stages: cp.async).
 //   pass 1 (iir32_sum): per segment, modulate and run the forward sections
 //     from a zero state (segment 0: the true init); the end state e and the
 //     backward-start sums b = sum_i c q^i y_loc[n0 + i] (the start state the
@@ -56,7 +57,7 @@ namespace fgb {
 
 namespace {
 
-constexpr int kM = kIir32M;  // samples per segment (register window of pass 2)
+constexpr int kM = kIir32M;  // samples per segment (the unrolled inner loops)
 constexpr int kTX = 32;      // lines per CTA
 constexpr int kSY = 4;       // segments per CTA
 
@@ -107,11 +108,9 @@ __device__ __forceinline__ void sec_steady(Sec& s, float2 z0, const Iir32Par& q)
 
 // CTA tile: 32 lines x kSY segments (kSW samples from nb0) of one job.
 // Shared memory: the modulation table of the tile's samples, the
-// recombination table, then the input tile:
-//   ROWS (horizontal stage, real rows): [32 rows][kSW | 1] floats (odd pitch)
-//   COLS (lines contiguous in memory):  [kSW samples][32 lines] of S (float or float2)
-// The fin kernel of the ROWS layout reuses the input tile (after a barrier)
-// as its [32][kSW | 1] complex output tile.
+// recombination table, then the input tile of float2 slots:
+//   ROWS (horizontal stage, real rows): [32 rows][kSW | 1] (odd pitch)
+//   COLS (lines contiguous in memory):  [kSW samples][32 lines]
 constexpr int kSW = kSY * kM;
 
 // Grid: x = segment blocks (fastest, so the CTAs of one line block run
