@@ -122,6 +122,11 @@ int32_t fgb_device_sm_count(void);
 int32_t fgb_pad_radius(const fgb_smoother* kind, double sigma);
 int32_t fgb_sampled_gaussian(double sigma, double radius, double* out, int32_t cap, int32_t* half);
 int32_t fgb_iir_coeffs(double sigma, double out_b_a1_a2_a3[4]);
+/* The same filter in parallel form (what the fp32 kernels run): real pole q_r,
+ * complex pole q_c (Im > 0), residues c_r, c_c, with
+ * B / (1 + a1 z^-1 + a2 z^-2 + a3 z^-3) = c_r / (1 - q_r z^-1) + 2 Re[c_c / (1 - q_c z^-1)].
+ * out = (q_r, Re q_c, Im q_c, c_r, Re c_c, Im c_c). */
+int32_t fgb_iir_sections(double sigma, double out[6]);
 /* Number of output entries / bins a call writes (for allocation). */
 int64_t fgb_bank_entries(const fgb_bank_desc* d);
 int64_t fgb_sdft_bins(const fgb_sdft_desc* d);

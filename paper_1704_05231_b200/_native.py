@@ -100,6 +100,7 @@ _SIGS = {
     "fgb_pad_radius": (C.c_int32, [_P(fgb_smoother), C.c_double]),
     "fgb_sampled_gaussian": (C.c_int32, [C.c_double, C.c_double, _P(C.c_double), C.c_int32, _P(C.c_int32)]),
     "fgb_iir_coeffs": (C.c_int32, [C.c_double, _P(C.c_double)]),
+    "fgb_iir_sections": (C.c_int32, [C.c_double, _P(C.c_double)]),
     "fgb_bank_entries": (C.c_int64, [_P(fgb_bank_desc)]),
     "fgb_sdft_bins": (C.c_int64, [_P(fgb_sdft_desc)]),
     "fgb_bank_workspace_bytes": (C.c_int64, [_P(fgb_bank_desc)]),

@@ -1922,6 +1922,12 @@ int32_t fgb_sampled_gaussian(double sigma, double radius, double* out, int32_t c
 }
 
 int32_t fgb_iir_coeffs(double sigma, double out[4]) { return iir_coeffs(sigma, out); }
+int32_t fgb_iir_sections(double sigma, double out[6]) {
+    double cf[4];
+    FGB_TRY(iir_coeffs(sigma, cf));
+    iir32_sections(IirCoef{cf[0], cf[1], cf[2], cf[3]}, out);
+    return FGB_OK;
+}
 
 int64_t fgb_bank_entries(const fgb_bank_desc* d) {
     if (!d) return fail(FGB_EINVAL, "null descriptor");

@@ -641,9 +641,8 @@ __global__ void __launch_bounds__(kTX * kSY) iir32_fin(const IirArgs<float> a, c
 using cd = std::complex<double>;
 
 // L = padded samples per line
-void iir32_params(const IirCoef& c, int L, Iir32Par* out) {
-    const int nseg = (L + kM - 1) / kM, mlast = L - (nseg - 1) * kM;
-    const int nS = (nseg + kSY - 1) / kSY, mlastS = L - (nS - 1) * kSW, Klast = nseg - (nS - 1) * kSY;
+// parallel form of the direct-form coefficients: real pole qr, complex pole qc (Im > 0), residues cr, cc
+void sections(const IirCoef& c, cd& qr, cd& qc, cd& cr, cd& cc) {
     // roots of z^3 + a1 z^2 + a2 z + a3 (Durand-Kerner, then Newton polish)
     auto poly = [&](cd z) { return ((z + c.a1) * z + c.a2) * z + c.a3; };
     cd r[3] = {cd(0.4, 0.9), cd(0.4, 0.9) * cd(0.4, 0.9), cd(0.4, 0.9) * cd(0.4, 0.9) * cd(0.4, 0.9)};
@@ -665,7 +664,8 @@ void iir32_params(const IirCoef& c, int L, Iir32Par* out) {
     int ic = -1;
     for (int k = 0; k < 3; ++k)
         if (k != ir && (ic < 0 || r[k].imag() > r[ic].imag())) ic = k;
-    const cd qr(r[ir].real(), 0.0), qc = r[ic];
+    qr = cd(r[ir].real(), 0.0);
+    qc = r[ic];
     const cd qs[3] = {qr, qc, std::conj(qc)};
     auto resid = [&](int k) {
         cd d(1.0, 0.0);
@@ -673,7 +673,16 @@ void iir32_params(const IirCoef& c, int L, Iir32Par* out) {
             if (j != k) d *= 1.0 - qs[j] / qs[k];
         return c.B / d;
     };
-    const cd cr = resid(0), cc = resid(1);
+    cr = resid(0);
+    cc = resid(1);
+}
+
+void iir32_params(const IirCoef& c, int L, Iir32Par* out) {
+    const int nseg = (L + kM - 1) / kM, mlast = L - (nseg - 1) * kM;
+    const int nS = (nseg + kSY - 1) / kSY, mlastS = L - (nS - 1) * kSW, Klast = nseg - (nS - 1) * kSY;
+    cd qr, qc, cr, cc;
+    sections(c, qr, qc, cr, cc);
+
     Iir32Par& p = *out;
     std::memset(&p, 0, sizeof(p));
     p.ndr = (float)-(1.0 - qr.real());
@@ -785,6 +794,13 @@ cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream
 }
 
 }  // namespace
+
+void iir32_sections(const IirCoef& c, double out[6]) {
+    cd qr, qc, cr, cc;
+    sections(c, qr, qc, cr, cc);
+    const double v[6] = {qr.real(), qc.real(), qc.imag(), cr.real(), cc.real(), cc.imag()};
+    std::memcpy(out, v, sizeof(v));
+}
 
 bool iir32_enabled() {
     static const bool on = !std::getenv("FGB_IIR64");

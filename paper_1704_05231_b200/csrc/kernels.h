@@ -137,6 +137,8 @@ template <typename T> cudaError_t launch_iir(const IirArgs<T>& a, cudaStream_t s
 // planes (iir32.cu).  Segments of exactly kIir32M samples (nseg = ceil(L / kIir32M)).
 constexpr int kIir32M = 32;
 bool iir32_enabled();  // false when FGB_IIR64 is set (the fp64-state kernels of iir.cu for A/B runs)
+// (q_r, Re q_c, Im q_c, c_r, Re c_c, Im c_c): poles and residues of the parallel form
+void iir32_sections(const IirCoef& c, double out[6]);
 cudaError_t launch_iir32(const IirArgs<float>& a, cudaStream_t s);
 template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch);
 size_t iir_state_doubles(int lines, int nseg, int njobs, int batch);

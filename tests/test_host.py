@@ -61,6 +61,36 @@ def test_iir_coefficients_match_golden(fg, golden):
         assert c.B == pytest.approx(float(c.denominator().sum()), abs=1e-15)
 
 
+def test_iir_parallel_form_sections(fg):
+    """fgb_iir_sections (what the fp32 IIR kernels run, csrc/iir32.cu) against NumPy's roots
+    and residues of the reference coefficients, the unit DC gain, and the impulse response of
+    the direct form (gaussian.py:215-228 restated by the oracle)."""
+    import ctypes as C
+
+    from paper_1704_05231_b200 import _native as N
+
+    for sigma in (0.6, 2.0, 4.3, 16.0, 32.0, 50.0):
+        out = (C.c_double * 6)()
+        assert N.lib.fgb_iir_sections(sigma, out) == 0
+        qr, qc, cr, cc = out[0], complex(out[1], out[2]), out[3], complex(out[4], out[5])
+        B, a1, a2, a3 = O.iir_coeffs(sigma)
+        roots = np.roots([1.0, a1, a2, a3])
+        assert min(abs(roots - qr)) < 1e-12 and min(abs(roots - qc)) < 1e-12 and qc.imag > 0
+        assert abs(cr / (1 - qr) + 2 * (cc / (1 - qc)).real - 1.0) < 1e-10  # unit DC gain (B = sum a)
+        n = np.arange(200)
+        h_sec = cr * qr ** n + 2 * (cc * qc ** n).real
+        x = np.zeros(200)
+        x[0] = 1.0
+        y, p1, p2, p3 = np.empty(200), 0.0, 0.0, 0.0
+        for i in range(200):
+            y[i] = B * x[i] - a1 * p1 - a2 * p2 - a3 * p3
+            p3, p2, p1 = p2, p1, y[i]
+        assert np.max(abs(h_sec - y)) < 1e-12 * max(1.0, sigma)
+    with pytest.raises(Exception):
+        fg.make_coeffs(0.25)
+    assert N.lib.fgb_iir_sections(0.25, (C.c_double * 6)()) != 0  # same validation as fgb_iir_coeffs
+
+
 def test_sampled_gaussian_matches_golden(fg, golden):
     z, meta = golden
     for key, h in meta["gauss"].items():
