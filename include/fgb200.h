@@ -24,6 +24,9 @@
  *   fgb_iir_coeffs      make_coeffs           gaussian.py:164-185
  *   fgb_sampled_gaussian sampled_gaussian     gaussian.py:188-195
  *   fgb_pad_radius      pad_radius            gaussian.py:198-212
+ *   fgb_smooth_lines    smooth_lines          gaussian.py:245-285
+ *                       (smooth_1d / smooth_pair_1d gaussian.py:288-302 are
+ *                        one / two lines of it)
  *
  * The *_host variants take HOST buffers and do the host<->device copies
  * (through pinned staging) inside the call: they are what the reference-side
@@ -113,6 +116,28 @@ typedef struct fgb_sdft_desc {
     int32_t n_heads;
 } fgb_sdft_desc;
 
+/* Independent 1-D lines (smooth_lines gaussian.py:245-285): real rows of a
+ * [n_lines][pitch] array, each smoothed along its length; output dense
+ * [n_lines][len] of the same dtype.
+ *   FGB_SMOOTH_FIR: correlation with the unit-sum sampled Gaussian (half
+ *                   support max(1, ceil(radius*sigma))), replicate ("nearest")
+ *                   boundary (gaussian.py:231-233);
+ *   FGB_SMOOTH_IIR: replicate pad ceil(5 sigma)+2 (none with assume_padded),
+ *                   forward + backward recursion with lfilter_zi steady-state
+ *                   init, crop (gaussian.py:215-228); fp64 state;
+ *   FGB_SMOOTH_BOX: sum over offsets [box_lo, box_hi], zero outside the line
+ *                   (Box(h) = [-h, h], _AsymBox(lo, hi); gaussian.py:236-242);
+ *                   smoother.box_half is ignored. */
+typedef struct fgb_lines_desc {
+    int32_t n_lines, len;
+    int64_t pitch;            /* elements between lines (>= len)              */
+    int32_t dtype;            /* FGB_F32 or FGB_F64                           */
+    int32_t assume_padded;    /* IIR: caller padded already (gaussian.py:265) */
+    double sigma;
+    fgb_smoother smoother;
+    int32_t box_lo, box_hi;
+} fgb_lines_desc;
+
 /* ---- library ----------------------------------------------------------- */
 const char* fgb_last_error(void);
 int32_t fgb_version(void);                  /* major*10000 + minor*100 + patch */
@@ -145,6 +170,7 @@ int32_t fgb_vertical_stage(const fgb_filter_desc* d, const void* j_in, void* out
 int32_t fgb_sdft(const fgb_sdft_desc* d, const void* img, void* out, void* stream);
 int32_t fgb_sdft_bin(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img, void* out, void* stream);
 int32_t fgb_sdft_horizontal(const fgb_sdft_desc* d, int32_t u, const void* img, void* j_out, void* stream);
+int32_t fgb_smooth_lines(const fgb_lines_desc* d, const void* lines, void* out, void* stream);
 
 /* ---- host-buffer entry points (copies inside; synchronous) ------------- */
 int32_t fgb_bank_host(const fgb_bank_desc* d, const void* img_host, void* out_host);
@@ -154,6 +180,7 @@ int32_t fgb_horizontal_stage_host(const fgb_filter_desc* d, const void* img_host
 int32_t fgb_vertical_stage_host(const fgb_filter_desc* d, const void* j_host, void* out_host, int32_t conjugate);
 int32_t fgb_sdft_bin_host(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* img_host, void* out_host);
 int32_t fgb_sdft_horizontal_host(const fgb_sdft_desc* d, int32_t u, const void* img_host, void* j_host);
+int32_t fgb_smooth_lines_host(const fgb_lines_desc* d, const void* lines_host, void* out_host);
 /* Same calls returning the reference's ComplexImage layout directly:
  * [batch][entries][2][H][W] float64 (re plane, im plane per entry), converted
  * on the GPU; *nonfinite = 1 if any output value is NaN / inf (the reference

@@ -6,7 +6,8 @@ reference package's own entry points.
 Drop-in surface (same names/signatures as fastgabor/__init__.py:11-80 for the
 hot path): ``compute_bank``, ``compute_bank_noreuse``, ``gabor_filter``,
 ``horizontal_stage``, ``vertical_stage``, ``vertical_stage_conjugate``,
-``sdft_full``, ``sdft_bin``, ``sdft_horizontal`` plus their types.  Every
+``sdft_full``, ``sdft_bin``, ``sdft_horizontal``, ``smooth_lines``,
+``smooth_1d``, ``smooth_pair_1d`` plus their types.  Every
 call crosses the C ABI of ``lib/libfgb200.so`` (include/fgb200.h); there is no
 CPU fallback.  ``paper_1704_05231_b200.device`` is the device-tensor API used
 for throughput runs.
@@ -33,6 +34,9 @@ from .gaussian import (
     make_coeffs,
     pad_radius,
     sampled_gaussian,
+    smooth_1d,
+    smooth_lines,
+    smooth_pair_1d,
 )
 from .gabor import GaborParams, HorizontalStage, gabor_filter, horizontal_stage, vertical_stage
 from .bank import (
@@ -58,6 +62,9 @@ __all__ = [
     "make_coeffs",
     "sampled_gaussian",
     "pad_radius",
+    "smooth_lines",
+    "smooth_1d",
+    "smooth_pair_1d",
     "GaborParams",
     "HorizontalStage",
     "horizontal_stage",

@@ -86,6 +86,20 @@ class fgb_sdft_desc(C.Structure):
     ]
 
 
+class fgb_lines_desc(C.Structure):
+    _fields_ = [
+        ("n_lines", C.c_int32),
+        ("len", C.c_int32),
+        ("pitch", C.c_int64),
+        ("dtype", C.c_int32),
+        ("assume_padded", C.c_int32),
+        ("sigma", C.c_double),
+        ("smoother", fgb_smoother),
+        ("box_lo", C.c_int32),
+        ("box_hi", C.c_int32),
+    ]
+
+
 class fgb_prof_entry(C.Structure):
     _fields_ = [("name", C.c_char * 16), ("launches", C.c_int64), ("ms", C.c_double), ("flops", C.c_double),
                 ("bytes", C.c_double)]
@@ -112,6 +126,8 @@ _SIGS = {
     "fgb_sdft": (C.c_int32, [_P(fgb_sdft_desc), _vp, _vp, _vp]),
     "fgb_sdft_bin": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, C.c_int32, _vp, _vp, _vp]),
     "fgb_sdft_horizontal": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, _vp, _vp, _vp]),
+    "fgb_smooth_lines": (C.c_int32, [_P(fgb_lines_desc), _vp, _vp, _vp]),
+    "fgb_smooth_lines_host": (C.c_int32, [_P(fgb_lines_desc), _vp, _vp]),
     "fgb_bank_host": (C.c_int32, [_P(fgb_bank_desc), _vp, _vp]),
     "fgb_filter_host": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp]),
     "fgb_sdft_host": (C.c_int32, [_P(fgb_sdft_desc), _vp, _vp]),

@@ -611,7 +611,7 @@ template <typename T> cudaError_t launch_col(const ColArgs<T>& a_in, const cx_t<
         g_sm_count = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
     }
-    const bool c2ok = (sizeof(T) == 4 && a.W % 2 == 0 && a.W >= 2 && !std::getenv("FGB_COL1"));
+    const bool c2ok = (sizeof(T) == 4 && a.W % 2 == 0 && a.W >= 2 && !knobs().col1);
     // candidates: (mode, S) with mode 0 = 1 column/thread (32-col tiles, G=8),
     // 1 = 2 columns/thread 32-col tiles, 2 = 2 columns/thread 16-col tiles (G=4)
     double best = 1e300;
@@ -650,13 +650,13 @@ template <typename T> cudaError_t launch_col(const ColArgs<T>& a_in, const cx_t<
             }
         }
     }
-    if (const char* e = std::getenv("FGB_COL_MODE")) {  // experiment knobs: force mode / segment rows
-        const int m = std::atoi(e);
+    if (knobs().col_mode >= 0) {  // experiment knobs: force mode / segment rows
+        const int m = knobs().col_mode;
         if (m >= 0 && m <= 2 && (m == 0 || c2ok)) { bestMode = m; bestG = m == 0 ? 8 : 4; }
     }
-    if (const char* e = std::getenv("FGB_COL_SEG")) {
+    if (knobs().col_seg > 0) {
         const int TY = bestMode == 0 ? bestG * R : (bestMode == 2 ? 4 : 2) * bestG * R;
-        const int S = std::atoi(e) / TY * TY;
+        const int S = knobs().col_seg / TY * TY;
         if (S > 0) bestS = S;
     }
     a.col2 = bestMode;

@@ -425,7 +425,7 @@ template <typename T> struct Builder {
         // theta = pi/2 (last direct of a Gabor group): the phase step omega cos(theta) ~ 1e-17 leaves
         // Im J <= 1e-12 |J|, so the fp32 kernel accumulates Re J only (the column pass reads Re J, realj)
         st.rg.last_real = sizeof(T) == 4 && std::fabs(freq[nd - 1]) * (W + 2.0 * (h + 1)) < 1e-12 &&
-                          phase[nd - 1] == cd(1.0, 0.0) && !std::getenv("FGB_NO_REALJ");
+                          phase[nd - 1] == cd(1.0, 0.0) && !knobs().no_realj;
         for (int k = 0; k < nd; ++k) {
             st.rg.dst_off[k] = dst_off[k];
             st.rg.phase_re[k] = (T)phase[k].real();
@@ -792,7 +792,7 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 // theta = pi/2: the row stage's phase step omega cos(theta) ~ 1e-17 leaves Im J at
                 // ~1e-12 of |J| or less, so the fp32 column kernel reads Re J only (half the FMAs)
                 if (sizeof(T) == 4 && !col_only && !box && job.mode == 1 && job.has_b &&
-                    std::fabs(jobs[j].wc) * (W + 2.0 * (h + 1)) < 1e-12 && !std::getenv("FGB_NO_REALJ"))
+                    std::fabs(jobs[j].wc) * (W + 2.0 * (h + 1)) < 1e-12 && !knobs().no_realj)
                     job.realj = 1;
                 // theta = 0 (ws = 0) jobs need A only (half the work): they share the
                 // launch (per-CTA branch) and go last so heavy CTAs start first
@@ -867,13 +867,13 @@ template <typename T> static int64_t iir_scratch_need(const Plan<T>& p) {
     int64_t m = 0;
     for (const auto& s : p.steps)
         if (s.kind == ST_IIR) m = std::max<int64_t>(m, (int64_t)iir_scratch_elems<T>(s.H, s.W, s.P, s.njobs, 1));
-    return m;
+    return (m + 63) / 64 * 64;  // lane / image bases stay 256-byte aligned (16-byte vector paths)
 }
 template <typename T> static int64_t iir_state_need(const Plan<T>& p) {
     int64_t m = 0;
     for (const auto& s : p.steps)
         if (s.kind == ST_IIR) m = std::max<int64_t>(m, (int64_t)iir_state_doubles(s.W, s.nseg, s.njobs, 1));
-    return m;
+    return (m + 31) / 32 * 32;  // per-lane state bases 256-byte aligned (iir32 carry_io's 16-byte copies)
 }
 
 static int64_t ws_budget_bytes() {
@@ -1060,7 +1060,7 @@ static int32_t build_sdft_core(Builder<T>& b, const fgb_sdft_desc& d, const BinM
     const int64_t aux = need;
     auto slot = [&](int u, int v) { return out_base + (bm.row_slot.at(u) + v) * HW; };
 
-    if (sm.kind == FGB_SMOOTH_FIR && mx == my && ws0 == 0 && !std::getenv("FGB_SDFT_UNFUSED")) {
+    if (sm.kind == FGB_SMOOTH_FIR && mx == my && ws0 == 0 && !knobs().sdft_unfused) {
         int h = 0;
         std::vector<double> w = sampled_gaussian(sigma, sm.radius, &h);
         if (sdft_fused_supported(mx, h, sizeof(T)) && out.sel == SEL_OUT) {
@@ -1339,6 +1339,7 @@ struct Ctx {
         for (auto st : lanes) cudaStreamDestroy(st);
         for (auto e : lane_ev) cudaEventDestroy(e);
         if (fork_ev) cudaEventDestroy(fork_ev);
+        if (ws_ev) cudaEventDestroy(ws_ev);
     }
     DevBuf ws;
     std::map<std::string, std::shared_ptr<PlanBase>> plans;
@@ -1346,7 +1347,25 @@ struct Ctx {
     cudaStream_t copy_stream = nullptr;    // D2H of finished pieces while later pieces compute
     std::vector<cudaEvent_t> piece_ev;
     DevBuf hpl, hflag; // planar f64 staging + non-finite flag of the *_host_planar entry points
+    // The workspace is shared by every call on this device: each execute records ws_ev on its
+    // stream when it has enqueued its last use, and a call on a different stream first waits
+    // on it, so calls on distinct streams never overlap on the same J / state buffers.
+    cudaEvent_t ws_ev = nullptr;
+    cudaStream_t ws_stream = nullptr;
+    bool ws_pending = false;
+    std::map<std::string, std::unique_ptr<DevBuf>> line_taps;  // fgb_smooth_lines tap tables (immutable)
 };
+static int32_t ws_acquire(Ctx& cx, cudaStream_t s) {
+    if (!cx.ws_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.ws_ev, cudaEventDisableTiming));
+    if (cx.ws_pending && cx.ws_stream != s) FGB_CUDA(cudaStreamWaitEvent(s, cx.ws_ev, 0));
+    return FGB_OK;
+}
+static int32_t ws_release(Ctx& cx, cudaStream_t s) {
+    FGB_CUDA(cudaEventRecord(cx.ws_ev, s));
+    cx.ws_stream = s;
+    cx.ws_pending = true;
+    return FGB_OK;
+}
 static std::mutex g_mu;
 static std::map<int, std::unique_ptr<Ctx>> g_ctx;
 
@@ -1385,8 +1404,8 @@ template <typename T> static int64_t plan_ws_bytes(const Plan<T>& p, int batch) 
     const int chunk = std::min(p.chunk, batch);
     const int64_t ws_img_bytes = p.ws_img_c * (int64_t)sizeof(cx_t<T>);
     const int64_t scr_bytes = p.scratch_img_t * (int64_t)sizeof(T);
-    const int64_t stt_bytes = (p.state_img_d * (int64_t)sizeof(double) + 255) / 256 * 256;
-    return (ws_img_bytes + scr_bytes + stt_bytes) * chunk + 512;
+    const int64_t stt_bytes = p.state_img_d * (int64_t)sizeof(double);
+    return (ws_img_bytes * chunk + 255) / 256 * 256 + scr_bytes * chunk + stt_bytes * chunk + 512;
 }
 
 template <typename T>
@@ -1398,9 +1417,11 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     const int64_t scr_bytes = p.scratch_img_t * (int64_t)sizeof(T);
     FGB_TRY(cx.ws.ensure((size_t)plan_ws_bytes(p, batch)));
     C* ws = (C*)cx.ws.p;
-    T* scratch = (T*)((char*)cx.ws.p + ws_img_bytes * chunk);
+    // region bases and per-lane strides are multiples of 256 bytes (iir_*_need round the per-lane needs)
+    const int64_t scr0 = (ws_img_bytes * chunk + 255) / 256 * 256;
+    T* scratch = (T*)((char*)cx.ws.p + scr0);
     const int64_t scratch_lane = p.scratch_img_t / std::max(1, p.nlanes) * chunk;
-    double* states = (double*)((char*)cx.ws.p + ((ws_img_bytes + scr_bytes) * chunk + 255) / 256 * 256);
+    double* states = (double*)((char*)cx.ws.p + scr0 + scr_bytes * chunk);
     const int64_t state_lane = p.state_img_d / std::max(1, p.nlanes) * chunk;
     // lane streams: lane 0 is the caller's stream; lanes >= 1 are library streams forked
     // from / joined into it with events, per image chunk
@@ -1419,6 +1440,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
         lane_s[l] = cx.lanes[l - 1];
     }
     if (!cx.fork_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.fork_ev, cudaEventDisableTiming));
+    FGB_TRY(ws_acquire(cx, s));
     const int64_t img_bs = (batch > 1) ? im.batch_stride : (int64_t)im.height * im.pitch;
     for (int b0 = 0; b0 < batch; b0 += chunk) {
         const int nb = std::min(chunk, batch - b0);
@@ -1455,7 +1477,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
             *bs = 2 * p.ws_img_c;
             return (const T*)ws + r.off;
         };
-        static const bool detail = std::getenv("FGB_PROF_DETAIL") != nullptr;
+        const bool detail = knobs().prof_detail;
         int sidx = 0;
         for (const Step<T>& st : p.steps) {
             cudaStream_t s = lane_s[st.lane];  // shadows the caller's stream for this step
@@ -1484,7 +1506,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.W = st.W;
                     a.hp = st.hp;
                     a.batch = nb;
-                    FGB_CUDA(launch_row_sym<T>(a, st.rg, std::getenv("FGB_ROW_SMEM_TAPS") ? nullptr : p.wrow.data() + st.rg.wofs, s));
+                    FGB_CUDA(launch_row_sym<T>(a, st.rg, knobs().row_smem_taps ? nullptr : p.wrow.data() + st.rg.wofs, s));
                     break;
                 }
                 case ST_COL: {
@@ -1502,7 +1524,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.zero_boundary = st.zero_bnd;
                     a.njobs = st.njobs;
                     a.batch = nb;
-                    FGB_CUDA(launch_col<T>(a, std::getenv("FGB_COL_SMEM_TAPS") ? nullptr : st.pw.data(), s));
+                    FGB_CUDA(launch_col<T>(a, knobs().col_smem_taps ? nullptr : st.pw.data(), s));
                     break;
                 }
                 case ST_IIR: {
@@ -1600,9 +1622,10 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                         a.batch = nb;
                         a.col_w_off = st.bf_colw_off;
                         for (int k = 0; k < st.nheads; ++k) a.out[k] = st.bf_out[k];
-                        static BankFusedW w;
-                        std::memcpy(w.w, st.bf_w.data(), st.bf_w.size() * sizeof(float));
-                        FGB_CUDA(launch_bank_fused(a, w, s));
+                        // per-call parameter block (28 KB, copied into the launch's constant bank)
+                        auto w = std::make_unique<BankFusedW>();
+                        std::memcpy(w->w, st.bf_w.data(), st.bf_w.size() * sizeof(float));
+                        FGB_CUDA(launch_bank_fused(a, *w, s));
                     }
                     break;
                 }
@@ -1626,7 +1649,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
             }
         }
     }
-    return FGB_OK;
+    return ws_release(cx, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1737,6 +1760,85 @@ static int32_t sdft_t(const fgb_sdft_desc* d, int u, int v, const void* img, voi
     Plan<T>* p = nullptr;
     FGB_TRY(sdft_plan<T>(d, u, v, &p));
     return execute<T>(*p, ctx(), d->img, img, out, s);
+}
+
+// ===========================================================================
+// 1-D line smoothing (smooth_lines gaussian.py:245-285)
+// ===========================================================================
+static int32_t validate_lines(const fgb_lines_desc* d) {
+    if (!d) return fail(FGB_EINVAL, "null descriptor");
+    if (d->n_lines < 0 || d->len < 1) return fail(FGB_EINVAL, "signal must be a non-empty 1-D array");
+    if (d->dtype != FGB_F32 && d->dtype != FGB_F64) return fail(FGB_EINVAL, "dtype must be FGB_F32 or FGB_F64");
+    if (d->pitch < d->len) return fail(FGB_EINVAL, "pitch must be >= len");
+    const fgb_smoother& k = d->smoother;
+    if (k.kind == FGB_SMOOTH_BOX) {
+        if (d->box_lo > d->box_hi) return fail(FGB_EINVAL, "box offsets need lo <= hi");
+        return FGB_OK;
+    }
+    if (k.kind == FGB_SMOOTH_FIR && !(d->sigma > 0)) return fail(FGB_EINVAL, "sigma must be positive");
+    return check_smoother(k, d->sigma);
+}
+
+template <typename T> static int32_t smooth_lines_t(const fgb_lines_desc* d, const void* in, void* out, cudaStream_t s) {
+    Ctx& cx = ctx();
+    const fgb_smoother& k = d->smoother;
+    if (d->n_lines == 0) return FGB_OK;
+    if (k.kind == FGB_SMOOTH_IIR) {
+        double c[4];
+        FGB_TRY(iir_coeffs(d->sigma, c));
+        LinesIirArgs<T> a{};
+        a.in = (const T*)in;
+        a.out = (T*)out;
+        a.pitch = d->pitch;
+        a.out_pitch = d->len;
+        a.n_lines = d->n_lines;
+        a.len = d->len;
+        a.P = d->assume_padded ? 0 : (int)std::ceil(5.0 * d->sigma) + 2;
+        a.c = IirCoef{c[0], c[1], c[2], c[3]};
+        FGB_TRY(ws_acquire(cx, s));
+        FGB_TRY(cx.ws.ensure((size_t)(d->len + 2 * a.P) * d->n_lines * sizeof(double)));
+        a.scratch = (double*)cx.ws.p;
+        ++g_launches;
+        FGB_CUDA(launch_lines_iir<T>(a, s));
+        return ws_release(cx, s);
+    }
+    // FIR / box: correlation with a cached, immutable device tap table
+    std::ostringstream key;
+    key.precision(17);
+    int t0 = 0;
+    std::vector<double> w;
+    if (k.kind == FGB_SMOOTH_FIR) {
+        int half = 0;
+        w = sampled_gaussian(d->sigma, k.radius, &half);
+        t0 = -half;
+        key << "fir|" << sizeof(T) << '|' << d->sigma << '|' << k.radius;
+    } else {
+        w.assign((size_t)(d->box_hi - d->box_lo + 1), 1.0);
+        t0 = d->box_lo;
+        key << "box|" << sizeof(T) << '|' << w.size();
+    }
+    auto& buf = cx.line_taps[key.str()];
+    if (!buf) {
+        std::vector<T> wt(w.begin(), w.end());
+        std::unique_ptr<DevBuf> nb(new DevBuf());
+        FGB_TRY(nb->ensure(wt.size() * sizeof(T)));
+        FGB_CUDA(cudaMemcpy(nb->p, wt.data(), wt.size() * sizeof(T), cudaMemcpyHostToDevice));
+        buf = std::move(nb);
+    }
+    LinesCorrArgs<T> a{};
+    a.in = (const T*)in;
+    a.out = (T*)out;
+    a.w = (const T*)buf->p;
+    a.pitch = d->pitch;
+    a.out_pitch = d->len;
+    a.n_lines = d->n_lines;
+    a.len = d->len;
+    a.t0 = t0;
+    a.nt = (int)w.size();
+    a.zero_boundary = k.kind == FGB_SMOOTH_BOX;
+    ++g_launches;
+    FGB_CUDA(launch_lines_corr<T>(a, s));
+    return FGB_OK;
 }
 
 // ===========================================================================
@@ -2020,6 +2122,30 @@ int32_t fgb_sdft_bin(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* i
     return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, v, img, out, s) : sdft_t<double>(d, u, v, img, out, s);
 }
 
+int32_t fgb_smooth_lines(const fgb_lines_desc* d, const void* lines, void* out, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    FGB_TRY(validate_lines(d));
+    return d->dtype == FGB_F64 ? smooth_lines_t<double>(d, lines, out, (cudaStream_t)stream)
+                               : smooth_lines_t<float>(d, lines, out, (cudaStream_t)stream);
+}
+int32_t fgb_smooth_lines_host(const fgb_lines_desc* d, const void* lines_host, void* out_host) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    FGB_TRY(validate_lines(d));
+    if (d->n_lines == 0) return FGB_OK;
+    Ctx& cx = ctx();
+    const size_t es = elem_size(d->dtype);
+    const size_t in_b = ((size_t)(d->n_lines - 1) * d->pitch + d->len) * es;
+    const size_t out_b = (size_t)d->n_lines * d->len * es;
+    FGB_TRY(cx.hin.ensure(in_b));
+    FGB_TRY(cx.hout.ensure(out_b));
+    cudaStream_t s = 0;
+    FGB_CUDA(cudaMemcpyAsync(cx.hin.p, lines_host, in_b, cudaMemcpyHostToDevice, s));
+    FGB_TRY(d->dtype == FGB_F64 ? smooth_lines_t<double>(d, cx.hin.p, cx.hout.p, s)
+                                : smooth_lines_t<float>(d, cx.hin.p, cx.hout.p, s));
+    FGB_CUDA(cudaMemcpyAsync(out_host, cx.hout.p, out_b, cudaMemcpyDeviceToHost, s));
+    FGB_CUDA(cudaStreamSynchronize(s));
+    return FGB_OK;
+}
 int32_t fgb_sdft_horizontal(const fgb_sdft_desc* d, int32_t u, const void* img, void* j_out, void* stream) {
     FGB_TRY(validate_sdft(d));
     if (u < 0 || u >= d->mx) return fail(FGB_EINVAL, "bin index u=" + std::to_string(u) + " outside [0, " + std::to_string(d->mx) + ")");

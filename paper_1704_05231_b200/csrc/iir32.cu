@@ -276,7 +276,7 @@ __device__ __forceinline__ void sum_body(const In<ROWS, CPLX>& in, int i0, int m
 constexpr int kCL = kTX;
 __device__ __forceinline__ void carry_io(float* sm, float* g, int64_t NL, int j0, int nj, int nl, int k0, int k1, bool load) {
     const int tid = threadIdx.y * kTX + threadIdx.x;
-    if (nl == kCL && (NL & 3) == 0) {  // 16-byte runs: thread = 4 lines of one (segment, slot)
+    if (nl == kCL && (NL & 3) == 0 && ((uintptr_t)g & 15) == 0) {  // 16-byte runs: thread = 4 lines of one (segment, slot)
         constexpr int kGroups = kTX * kSY / 8;  // row groups of 8 threads
         const int l4 = (tid & 7) * 4, r0 = tid >> 3;
         const int nk = k1 - k0;
@@ -803,7 +803,7 @@ void iir32_sections(const IirCoef& c, double out[6]) {
 }
 
 bool iir32_enabled() {
-    static const bool on = !std::getenv("FGB_IIR64");
+    const bool on = !knobs().iir64;
     return on;
 }
 

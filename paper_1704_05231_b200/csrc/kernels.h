@@ -10,6 +10,24 @@
 
 namespace fgb {
 
+// A/B experiment knobs, read from the environment once
+// per process -- never per launch.
+struct Knobs {
+    bool col1, col_smem_taps, row_smem_taps, no_realj, sdft_unfused, prof_detail, iir64;
+    int col_mode;  // -1 = cost model
+    int col_seg;   // 0 = cost model
+};
+inline const Knobs& knobs() {
+    static const Knobs k = [] {
+        auto on = [](const char* n) { return std::getenv(n) != nullptr; };
+        auto num = [](const char* n, int d) { const char* e = std::getenv(n); return e ? std::atoi(e) : d; };
+        return Knobs{on("FGB_COL1"), on("FGB_COL_SMEM_TAPS"), on("FGB_ROW_SMEM_TAPS"), on("FGB_NO_REALJ"),
+                     on("FGB_SDFT_UNFUSED"), on("FGB_PROF_DETAIL"), on("FGB_IIR64"), num("FGB_COL_MODE", -1),
+                     num("FGB_COL_SEG", 0)};
+    }();
+    return k;
+}
+
 // ---- K1: symmetric-FIR row pass (row_fir.cu) ------------------------------
 template <typename T> struct RowArgs {
     const T* img;          // real input, batch 0
@@ -142,6 +160,26 @@ void iir32_sections(const IirCoef& c, double out[6]);
 cudaError_t launch_iir32(const IirArgs<float>& a, cudaStream_t s);
 template <typename T> size_t iir_scratch_elems(int len, int lines, int P, int njobs, int batch);
 size_t iir_state_doubles(int lines, int nseg, int njobs, int batch);
+
+// ---- 1-D line smoothing (smooth.cu; smooth_lines gaussian.py:245-285) -----
+template <typename T> struct LinesCorrArgs {
+    const T* in;             // [n_lines][pitch]
+    T* out;                  // [n_lines][out_pitch]
+    const T* w;              // device taps w[0..nt-1] at offsets t0..t0+nt-1
+    int64_t pitch, out_pitch;
+    int n_lines, len, t0, nt;
+    int zero_boundary;       // 0 = replicate (FIR "nearest"), 1 = zero (box)
+};
+template <typename T> struct LinesIirArgs {
+    const T* in;
+    T* out;
+    double* scratch;         // [len + 2P][n_lines] forward sequence
+    int64_t pitch, out_pitch;
+    int n_lines, len, P;
+    IirCoef c;
+};
+template <typename T> cudaError_t launch_lines_corr(const LinesCorrArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_lines_iir(const LinesIirArgs<T>& a, cudaStream_t s);
 
 // ---- output layout conversion (gbnk.cu) -----------------------------------
 // [entries][plane] interleaved complex -> [entries][2][plane] f64 (re plane,

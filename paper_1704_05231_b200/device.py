@@ -43,6 +43,20 @@ def _check_img(img: torch.Tensor):
     return img
 
 
+def _check_out(out: torch.Tensor, shape, prec: str, device) -> torch.Tensor:
+    """A caller-supplied output must be exactly what the kernels write: the plan's
+    shape, complex dtype of the plan precision, dense, on the image's device."""
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"out shape {tuple(out.shape)} != {tuple(shape)}")
+    if out.dtype != _cplx(prec):
+        raise ValueError(f"out dtype {out.dtype} != {_cplx(prec)}")
+    if out.device != device:
+        raise ValueError(f"out is on {out.device}, image on {device}")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
+    return out
+
+
 class BankPlan:
     """Reusable bank call: descriptor built once, output [B, E, H, W] complex."""
 
@@ -53,9 +67,13 @@ class BankPlan:
         self.desc, self._keep = bank_desc(h, w, spec, kind, precision, reuse, batch=b, units=units)
         self.entries = int(N.check(N.lib.fgb_bank_entries(C.byref(self.desc))))
 
-    def new_output(self, device="cuda") -> torch.Tensor:
+    @property
+    def out_shape(self):
         b, h, w = self.shape
-        return torch.empty((b, self.entries, h, w), dtype=_cplx(self.prec), device=device)
+        return (b, self.entries, h, w)
+
+    def new_output(self, device="cuda") -> torch.Tensor:
+        return torch.empty(self.out_shape, dtype=_cplx(self.prec), device=device)
 
     @property
     def workspace_bytes(self) -> int:
@@ -70,8 +88,7 @@ class BankPlan:
             raise ValueError("image dtype does not match the plan precision")
         self.desc.img.pitch = img.stride(1)
         self.desc.img.batch_stride = img.stride(0)
-        if out is None:
-            out = self.new_output(img.device)
+        out = self.new_output(img.device) if out is None else _check_out(out, self.out_shape, self.prec, img.device)
         N.check(N.lib.fgb_bank(C.byref(self.desc), C.c_void_p(img.data_ptr()), C.c_void_p(out.data_ptr()),
                                C.c_void_p(_stream(stream))))
         return out
@@ -87,9 +104,13 @@ class SdftPlan:
         self.desc, self._keep = sdft_desc(h, w, spec, precision, batch=b, heads=heads)
         self.bins = int(N.check(N.lib.fgb_sdft_bins(C.byref(self.desc))))
 
-    def new_output(self, device="cuda") -> torch.Tensor:
+    @property
+    def out_shape(self):
         b, h, w = self.shape
-        return torch.empty((b, self.bins, h, w), dtype=_cplx(self.prec), device=device)
+        return (b, self.bins, h, w)
+
+    def new_output(self, device="cuda") -> torch.Tensor:
+        return torch.empty(self.out_shape, dtype=_cplx(self.prec), device=device)
 
     @property
     def workspace_bytes(self) -> int:
@@ -100,10 +121,11 @@ class SdftPlan:
         img = _check_img(img)
         if tuple(img.shape) != self.shape:
             raise ValueError(f"image shape {tuple(img.shape)} != plan shape {self.shape}")
+        if _prec(img) != self.prec:
+            raise ValueError("image dtype does not match the plan precision")
         self.desc.img.pitch = img.stride(1)
         self.desc.img.batch_stride = img.stride(0)
-        if out is None:
-            out = self.new_output(img.device)
+        out = self.new_output(img.device) if out is None else _check_out(out, self.out_shape, self.prec, img.device)
         N.check(N.lib.fgb_sdft(C.byref(self.desc), C.c_void_p(img.data_ptr()), C.c_void_p(out.data_ptr()),
                                C.c_void_p(_stream(stream))))
         return out

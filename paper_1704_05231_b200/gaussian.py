@@ -111,3 +111,67 @@ def pad_radius(kind: SmootherKind, sigma: float) -> int:
     if isinstance(kind, RecursiveIIR):
         return math.ceil(5.0 * sigma) + 2
     return 0
+
+
+# ---- 1-D smoothing entry points (gaussian.py:245-302) ------------------------
+
+def _lines_desc(n_lines: int, length: int, kind, sigma: float, prec: str, assume_padded: bool) -> N.fgb_lines_desc:
+    lo = hi = 0
+    if isinstance(kind, Box):
+        sm = N.fgb_smoother(N.FGB_SMOOTH_BOX, int(kind.half_width), 0.0)
+        lo, hi = -int(kind.half_width), int(kind.half_width)
+    elif isinstance(kind, _AsymBox):
+        sm = N.fgb_smoother(N.FGB_SMOOTH_BOX, 0, 0.0)
+        lo, hi = int(kind.lo), int(kind.hi)
+    else:
+        sm = native_smoother(kind)  # TypeError for unknown kinds (gaussian.py:279-280)
+    return N.fgb_lines_desc(n_lines, length, length, N.dtype_code(prec), int(bool(assume_padded)), float(sigma), sm,
+                            lo, hi)
+
+
+def smooth_lines(lines: np.ndarray, kind: SmootherKind, sigma: float, counters, nominal_len: int | None = None,
+                 direction: str = "h", assume_padded: bool = False, precision: str | None = None) -> np.ndarray:
+    """Smooth each row of a 2-D array independently (gaussian.py:245-285).
+
+    Same dispatch, validation and counter charges as the reference; the lines
+    are smoothed on the GPU by ``fgb_smooth_lines_host`` (FIR / box: tiled
+    correlation; IIR: fp64-state recursion with the reference's padding and
+    steady-state init).  Returns float64 like the reference.
+    """
+    from ._precision import real_dtype, resolve
+    from .metrics import charge_smoothing
+
+    prec = resolve(precision)
+    arr = np.asarray(lines)
+    if arr.ndim != 2:
+        raise ValueError("lines must be a 2-D array")
+    rows, length = arr.shape
+    src = np.ascontiguousarray(arr, dtype=real_dtype(prec))
+    d = _lines_desc(rows, length, kind, sigma, prec, assume_padded)
+    out = np.empty((rows, length), dtype=real_dtype(prec))
+    if rows and length:
+        N.check(N.lib.fgb_smooth_lines_host(C.byref(d), src.ctypes.data, out.ctypes.data))
+    elif isinstance(kind, (ExactFIR, RecursiveIIR)):
+        # empty input: still raise the reference's parameter errors (sampled_gaussian / make_coeffs)
+        if isinstance(kind, RecursiveIIR):
+            make_coeffs(float(sigma))
+        else:
+            sampled_gaussian(float(sigma), kind.radius)
+    charge_smoothing(counters, kind, sigma, rows, nominal_len if nominal_len is not None else length, direction)
+    return out.astype(np.float64, copy=False)
+
+
+def smooth_1d(signal: np.ndarray, kind: SmootherKind, sigma: float, counters,
+              precision: str | None = None) -> np.ndarray:
+    """Smooth a single 1-D signal (gaussian.py:288-295)."""
+    signal = np.asarray(signal, dtype=np.float64)
+    if signal.ndim != 1 or signal.size < 1:
+        raise ValueError("signal must be a non-empty 1-D array")
+    return smooth_lines(signal[None, :], kind, sigma, counters, precision=precision)[0]
+
+
+def smooth_pair_1d(a: np.ndarray, b: np.ndarray, kind: SmootherKind, sigma: float, counters,
+                   precision: str | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Smooth two signals -- per-stage cost is visibly two smoothings (gaussian.py:298-302)."""
+    return (smooth_1d(a, kind, sigma, counters, precision=precision),
+            smooth_1d(b, kind, sigma, counters, precision=precision))
