@@ -159,6 +159,15 @@ for i, (om, th, sg) in enumerate(single[:3]):
 for kn, k in (("fir6", ("fir", 6.0)), ("box1", ("box", 1))):
     spec = fg.SdftSpec(4, 4, kind_obj(k))
     put(f"ldft.{kn}", fg.localized_dft(fg.RealImage.from_array(f3), 1, 3, spec))
+# 7b. Large supports at the configs' radius 3 (sigma 16 / 32: 97^2 / 193^2 taps, larger
+#     than the image), the case the GPU brute force runs as banded kernel rows.
+f7 = img(17, 120, 136)
+arrays["f7"] = f7
+for i, (om, th, sg) in enumerate(((math.pi / 16, 3 * math.pi / 8, 16.0), (math.pi / 32, 13 * math.pi / 16, 32.0))):
+    put(f"firgabor_r3.{i}", fg.fir_gabor(fg.RealImage.from_array(f7), fg.GaborParams(om, th, sg), fg.OracleConfig(3.0)))
+    meta["cases"][f"firgabor_r3.{i}"] = {"params": [om, th, sg]}
+put("ldft_r3", fg.localized_dft(fg.RealImage.from_array(f7), 5, 27, fg.SdftSpec(32, 32, fg.ExactFIR(3.0), 16.0),
+                                fg.OracleConfig(3.0)))
 
 # 8. I/O and metrics (image_io.py:136-212, metrics.py:63-83): bytes written by the
 #    reference for known inputs, SER of known pairs.

@@ -371,3 +371,50 @@ def test_workspace_bytes_query(env):
     out = cfg2(torch.rand(1, 1024, 1024, device="cuda"), cfg2.new_output())
     torch.cuda.synchronize()
     assert out.shape[1] == 32 and torch.cuda.memory_allocated() >= before  # torch's pool is separate
+
+
+def test_iir_lane_state_alignment_odd_shapes():
+    """odd N, two IIR frequencies, odd width, height % 4 == 0 put a
+    lane's segment states at an 8-mod-16 byte offset before the 256-byte rounding;
+    the fp32 recursion must run (16-byte copies) and match the oracle."""
+    import torch
+
+    import paper_1704_05231_b200 as fg
+    from oracle import fastgabor_oracle as O
+    from paper_1704_05231_b200.device import compute_bank
+
+    f = np.random.default_rng(21).uniform(0, 1, (256, 255))
+    for n, sig in ((3, (4.0, 2.0)), (5, (2.0, 3.0, 4.0))):
+        freqs = tuple(math.pi / 2 ** (j + 1) for j in range(len(sig)))
+        out = compute_bank(torch.from_numpy(f.astype(np.float32)).cuda(), fg.BankSpec(freqs, n, sig),
+                           fg.RecursiveIIR())[0].cpu().numpy()
+        ref = O.compute_bank(f, freqs, n, sig, ("iir",))
+        for e, r in enumerate(ref):
+            scale = max(np.abs(r[3]).max(), np.abs(r[4]).max())
+            err = max(np.abs(out[e].real - r[3]).max(), np.abs(out[e].imag - r[4]).max()) / scale
+            assert err <= 1e-5, (n, e, err)
+
+
+def test_two_streams_share_the_workspace_safely():
+    """ADVICE r1 (medium): calls on different streams reuse the one device workspace;
+    the library orders them (event wait), so concurrent banks on two streams equal
+    the serial results bit for bit."""
+    import torch
+
+    import paper_1704_05231_b200 as fg
+    from paper_1704_05231_b200.device import BankPlan
+
+    spec = fg.BankSpec((math.pi / 8, math.pi / 16), 8, (8.0, 16.0))
+    imgs = [torch.rand(1, 512, 512, device="cuda") for _ in range(2)]
+    plans = [BankPlan((1, 512, 512), spec, k, "f32") for k in (fg.ExactFIR(3.0), fg.RecursiveIIR())]
+    ref = [p(i).clone() for p, i in zip(plans, imgs)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [p.new_output("cuda") for p in plans]
+    for _ in range(3):
+        for p, i, o, s in zip(plans, imgs, outs, streams):
+            with torch.cuda.stream(s):
+                p(i, o, stream=s)
+        torch.cuda.synchronize()
+        for o, r in zip(outs, ref):
+            assert torch.equal(o, r)

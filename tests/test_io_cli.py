@@ -112,6 +112,21 @@ def test_gpu_bruteforce_matches_reference_goldens(fg, golden):
         ref = (z[f"ldft.{kn}.re"], z[f"ldft.{kn}.im"])
         scale = max(np.abs(ref[0]).max(), np.abs(ref[1]).max())
         assert max(np.abs(out.re - ref[0]).max(), np.abs(out.im - ref[1]).max()) / scale <= 1e-12
+    # radius 3 at sigma 16 / 32 (97^2 / 193^2 taps, wider than the 120x136 image): the banded
+    # large-support path the config-3/5 full-size checks run
+    f7 = fg.RealImage.from_array(z["f7"])
+    for i in range(2):
+        om, th, sg = meta["cases"][f"firgabor_r3.{i}"]["params"]
+        ref = (z[f"firgabor_r3.{i}.re"], z[f"firgabor_r3.{i}.im"])
+        scale = max(np.abs(ref[0]).max(), np.abs(ref[1]).max())
+        for prec, tol in (("f64", 1e-12), ("f32", 1e-5)):
+            out = fg.fir_gabor(f7, fg.GaborParams(om, th, sg), fg.OracleConfig(3.0), precision=prec)
+            assert max(np.abs(out.re - ref[0]).max(), np.abs(out.im - ref[1]).max()) / scale <= tol, (i, prec)
+    out = fg.localized_dft(f7, 5, 27, fg.SdftSpec(32, 32, fg.ExactFIR(3.0), 16.0), fg.OracleConfig(3.0),
+                           precision="f64")
+    ref = (z["ldft_r3.re"], z["ldft_r3.im"])
+    scale = max(np.abs(ref[0]).max(), np.abs(ref[1]).max())
+    assert max(np.abs(out.re - ref[0]).max(), np.abs(out.im - ref[1]).max()) / scale <= 1e-12
 
 
 @pytest.mark.gpu

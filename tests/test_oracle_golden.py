@@ -110,3 +110,9 @@ def test_bruteforce_oracles(golden):
         assert max_rel_err(O.fir_gabor(f1, om, th, sg), g(z, f"firgabor.{i}")) <= 1e-14
     for kn in ("fir6", "box1"):
         assert max_rel_err(O.localized_dft(f3, 1, 3, 4, 4, KINDS[kn]), g(z, f"ldft.{kn}")) <= 1e-14
+    # radius 3, supports larger than the image (sigma 16 / 32)
+    f7 = z["f7"]
+    for i in range(2):
+        om, th, sg = meta["cases"][f"firgabor_r3.{i}"]["params"]
+        assert max_rel_err(O.fir_gabor(f7, om, th, sg, radius=3.0), g(z, f"firgabor_r3.{i}")) <= 1e-13
+    assert max_rel_err(O.localized_dft(f7, 5, 27, 32, 32, ("fir", 3.0), 16.0, radius=3.0), g(z, "ldft_r3")) <= 1e-13
