@@ -1,5 +1,6 @@
-"""Measure the device time of every (frequency, direct k) unit of a bank config
-alone (CUDA events, 3 repeats, median), to calibrate parallel.bank_unit_costs.
+"""Measure device time of contiguous (frequency, direct k) unit ranges of a
+bank config, split into the row and column launches by libfgb200's live
+profile -- the data behind parallel.bank_unit_costs / partition_units.
 
     python tools/unit_costs.py [--config 5] > profiles/r02/unit_costs_c5.json
 """
@@ -16,8 +17,8 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_1704_05231_b200 as fg  # noqa: E402
+from paper_1704_05231_b200 import _native as N  # noqa: E402
 from paper_1704_05231_b200.device import BankPlan  # noqa: E402
-from paper_1704_05231_b200.parallel import bank_unit_costs  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
@@ -26,36 +27,31 @@ cfg = bench.CONFIGS[a.config]
 img = torch.from_numpy(bench.make_image(cfg, 0)[None]).cuda()
 spec = fg.BankSpec(tuple(cfg["freqs"]), cfg["n"], tuple(cfg["sigmas"]))
 nh = cfg["n"] // 2
-model = bank_unit_costs(cfg["freqs"], cfg["sigmas"], cfg["n"], 3.0)
-res = {}
+rows = []
 for i in range(len(cfg["freqs"])):
-    for k in range(nh + 1):
-        u = i * (nh + 1) + k
-        p = BankPlan(tuple(img.shape), spec, fg.ExactFIR(3.0), "f32", True, [u])
-        out = p.new_output("cuda")
-        ts = []
-        for _ in range(4):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+    for k0 in range(nh + 1):
+        for k1 in range(k0, nh + 1):
+            units = [i * (nh + 1) + k for k in range(k0, k1 + 1)]
+            p = BankPlan(tuple(img.shape), spec, fg.ExactFIR(3.0), "f32", True, units)
+            out = p.new_output("cuda")
             p(img, out)
-            e1.record()
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        res[u] = {"freq": i, "k": k, "sigma": cfg["sigmas"][i], "ms": float(np.median(ts[1:])), "model": model[u]}
-        del out
-# all units of one frequency together (the row launch is shared when a rank holds several)
-full = {}
-for i in range(len(cfg["freqs"])):
-    p = BankPlan(tuple(img.shape), spec, fg.ExactFIR(3.0), "f32", True, [i * (nh + 1) + k for k in range(nh + 1)])
-    out = p.new_output("cuda")
-    ts = []
-    for _ in range(4):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        p(img, out)
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    full[i] = float(np.median(ts[1:]))
-    del out
-print(json.dumps({"config": a.config, "units": res, "per_frequency_ms": full}, indent=1))
+            ts = []
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                p(img, out)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            N.lib.fgb_profile_enable(1)
+            N.profile_read()
+            for _ in range(3):
+                p(img, out)
+            torch.cuda.synchronize()
+            prof = {e["name"]: e["ms"] / 3 for e in N.profile_read()}
+            N.lib.fgb_profile_enable(0)
+            rows.append({"freq": i, "sigma": cfg["sigmas"][i], "k0": k0, "k1": k1, "ms": float(np.median(ts)),
+                         "prof": prof})
+            del out
+print(json.dumps({"config": a.config, "ranges": rows}))
