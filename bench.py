@@ -411,7 +411,7 @@ def build_workload(args, cfg, D):
     """(plan, device input, host input array, units of this rank per step, broadcast ms)."""
     import paper_1704_05231_b200 as fg
     from paper_1704_05231_b200.device import BankPlan, SdftPlan
-    from paper_1704_05231_b200.parallel import bank_unit_costs, lpt_assign, sdft_heads, shard_images
+    from paper_1704_05231_b200.parallel import partition_units, sdft_heads, shard_images
 
     kind = fg.ExactFIR(3.0) if args.smoother == "fir" else fg.RecursiveIIR()
     bcast = None
@@ -423,8 +423,8 @@ def build_workload(args, cfg, D):
             imgs = np.stack([make_image(cfg, i) for i in mine])
             timg = __import__("torch").from_numpy(imgs).to(D.dev)
         elif args.config == 5:
-            costs = bank_unit_costs(cfg["freqs"], cfg["sigmas"], cfg["n"], 3.0)
-            units = lpt_assign(costs, D.world)[D.rank] if D.world > 1 else None
+            units = (partition_units(cfg["freqs"], cfg["sigmas"], cfg["n"], D.world, 3.0)[D.rank]
+                     if D.world > 1 else None)
             imgs = make_image(cfg, 0)[None] if D.rank == 0 or D.backend != "nccl" else np.empty(
                 (1, cfg["size"], cfg["size"]), np.float32)
             timg, bcast = D.broadcast_image(imgs)

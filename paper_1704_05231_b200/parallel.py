@@ -5,8 +5,9 @@ The path shards into independent units:
 * batched banks (config 3): images, contiguous blocks per rank;
 * large single-image banks (config 5): (frequency i, direct orientation k)
   units -- unit id i*(N/2+1)+k, computing theta_k and, when it exists,
-  pi-theta_k from the same row pass (bank.py:109-116) -- balanced by LPT on
-  their FLOP cost;
+  pi-theta_k from the same row pass (bank.py:109-116) -- split into
+  contiguous runs per rank by an exact linear partition over a device-time
+  model measured on the B200 (partition_units);
 * the localized SDFT (config 4): conjugate u-pairs {u, M-u}; the pair (0, M/2)
   self-pairs are merged so that every shard holds 2*M bins when possible.
 
@@ -31,21 +32,137 @@ def shard_images(n_images: int, world: int) -> list[list[int]]:
     return out
 
 
-def bank_unit_costs(freqs, sigmas, n: int, radius: float = 3.0) -> dict[int, float]:
-    """Relative FP32 cost of every (frequency, direct k) unit.
+# Device-time model of the bank kernels (ms per megapixel), fitted to the B200
+# measurements in profiles/r02/unit_costs_c5.json (tools/unit_costs.py: every
+# contiguous k-range of every config-5 frequency, row / column launches split by
+# the live profile).  T = 2 ceil(r sigma) + 1 taps.
+#   row launch  (K1, up to 6 directs, symmetric pairs shared):  _ROW_A + _ROW_S*T per launch
+#                                                                + _ROW_B*T per direct
+#   column job  (K2, theta and pi - theta from one J):          _COL_A + _COL_T*T, times
+#                0.65 for theta = 0 (no B term) and 0.91 for theta = pi/2 (real J)
+#   fused small-sigma launch (K5, h <= 6, <= 5 directs):       _FUSED_A + _FUSED_G per direct
+_MPX = 67.108864  # the fit's 8192^2 image
+_ROW_A, _ROW_S, _ROW_B = 0.107 / _MPX, 0.00285 / _MPX, 0.0019 / _MPX
+_COL_A, _COL_T = 0.175 / _MPX, 0.00715 / _MPX
+_FUSED_A, _FUSED_G = 0.22 / _MPX, 0.225 / _MPX
+_ROW_GROUP = 6
 
-    Row pass ~ shared FIR over the input (amortised: T per direct), column pass
-    4T per emitted pair (2T when theta = 0 has no B term), per pixel.
-    """
+
+def run_cost(sigma: float, ks, n: int, radius: float = 3.0, mpx: float = 1.0) -> float:
+    """Modelled device ms of one rank computing the direct orientations ``ks`` of
+    one frequency (sharing its row launches) on an image of ``mpx`` megapixels."""
+    ks = list(ks)
+    if not ks:
+        return 0.0
+    h = max(1, math.ceil(radius * sigma))
+    t = 2 * h + 1
     nh = n // 2
-    costs = {}
-    for i, s in enumerate(sigmas):
-        t = 2 * max(1, math.ceil(radius * s)) + 1
-        for k in range(nh + 1):
-            mirror = nh < n - k < n
-            col = 2 * t if k == 0 else 4 * t
-            costs[i * (nh + 1) + k] = t * 1.2 + col + (0.0 if mirror else 0.0)
-    return costs
+    if h <= 6 and len(ks) <= 5:
+        return mpx * (_FUSED_A + _FUSED_G * len(ks))
+    launches = -(-len(ks) // _ROW_GROUP)
+    row = launches * (_ROW_A + _ROW_S * t) + len(ks) * _ROW_B * t
+    col = 0.0
+    for k in ks:
+        f = 0.65 if k == 0 else (0.91 if 2 * k == n and nh == k else 1.0)
+        col += f * (_COL_A + _COL_T * t)
+    return mpx * (row + col)
+
+
+def bank_unit_costs(freqs, sigmas, n: int, radius: float = 3.0) -> dict[int, float]:
+    """Modelled device cost of every (frequency i, direct k) unit computed alone
+    (unit id i*(N/2+1)+k; theta = 0 has no B term, theta = pi/2 a real J)."""
+    nh = n // 2
+    return {i * (nh + 1) + k: run_cost(s, [k], n, radius) for i, s in enumerate(sigmas) for k in range(nh + 1)}
+
+
+def partition_units(freqs, sigmas, n: int, world: int, radius: float = 3.0) -> list[list[int]]:
+    """Split the bank's (frequency, direct k) units over ``world`` ranks as
+    contiguous runs of the sequence ordered by frequency (largest sigma first)
+    then k, minimising the largest modelled rank cost (exact linear-partition
+    DP).  Contiguity keeps a rank's directs of one frequency together so they
+    share row launches (K1 forms the symmetric pair sums once for all of
+    them); a plain LPT over single units loses that sharing -- on config 5 it
+    costs ~24% more device time in total (sum of single-unit times 50.5 ms vs
+    40.7 ms for the grouped bank, profiles/r02/unit_costs_c5.json)."""
+    nh = n // 2
+    order = [(i, k) for i in sorted(range(len(sigmas)), key=lambda i: (-sigmas[i], i)) for k in range(nh + 1)]
+    m = len(order)
+    world = max(1, min(world, m))
+
+    def seg_cost(a, b):  # units order[a:b]
+        runs: dict[int, list[int]] = {}
+        for i, k in order[a:b]:
+            runs.setdefault(i, []).append(k)
+        return sum(run_cost(sigmas[i], ks, n, radius) for i, ks in runs.items())
+
+    cost = [[0.0] * (m + 1) for _ in range(m + 1)]
+    for a in range(m):
+        for b in range(a + 1, m + 1):
+            cost[a][b] = seg_cost(a, b)
+    inf = float("inf")
+    best = [[inf] * (m + 1) for _ in range(world + 1)]
+    cut = [[0] * (m + 1) for _ in range(world + 1)]
+    best[0][0] = 0.0
+    for r in range(1, world + 1):
+        for b in range(1, m + 1):
+            for a in range(r - 1, b):
+                v = max(best[r - 1][a], cost[a][b])
+                if v < best[r][b]:
+                    best[r][b], cut[r][b] = v, a
+    bounds, b = [], m
+    for r in range(world, 0, -1):
+        a = cut[r][b]
+        bounds.append((a, b))
+        b = a
+    bounds.reverse()
+    parts = [sorted(i * (nh + 1) + k for i, k in order[a:b]) for a, b in bounds]
+    return _refine(parts, sigmas, n, radius)
+
+
+def _refine(parts, sigmas, n: int, radius: float, rounds: int = 200):
+    """Local search on the partition: move a unit off the most loaded rank, or
+    swap it with another rank's unit, while that lowers the larger of the two
+    ranks' costs below the current maximum (deterministic; ends at a local
+    optimum)."""
+    parts = [list(p) for p in parts]
+    cost = partition_cost(parts, sigmas, n, radius)
+
+    def c1(p):
+        return partition_cost([p], sigmas, n, radius)[0]
+
+    for _ in range(rounds):
+        r = max(range(len(parts)), key=lambda j: (cost[j], -j))
+        top, best = cost[r], None
+        for u in parts[r]:
+            ru = [x for x in parts[r] if x != u]
+            for q in range(len(parts)):
+                if q == r:
+                    continue
+                cand = [(c1(ru), c1(parts[q] + [u]), ru, parts[q] + [u])]
+                for v in parts[q]:
+                    qv = [x for x in parts[q] if x != v] + [u]
+                    cand.append((c1(ru + [v]), c1(qv), ru + [v], qv))
+                for a, b, pa, pb in cand:
+                    m = max(a, b)
+                    if m < top - 1e-12 and (best is None or m < best[0] - 1e-12):
+                        best = (m, q, a, b, pa, pb)
+        if best is None:
+            break
+        _, q, a, b, pa, pb = best
+        parts[r], parts[q], cost[r], cost[q] = pa, pb, a, b
+    return [sorted(p) for p in parts]
+
+
+def partition_cost(parts, sigmas, n: int, radius: float = 3.0) -> list[float]:
+    """Modelled cost of each rank's unit list (row launches shared per frequency)."""
+    nh = n // 2
+    out = []
+    for p in parts:
+        runs: dict[int, list[int]] = {}
+        for u in p:
+            runs.setdefault(u // (nh + 1), []).append(u % (nh + 1))
+        out.append(sum(run_cost(sigmas[i], ks, n, radius) for i, ks in runs.items()))
+    return out
 
 
 def lpt_assign(costs: dict[int, float], world: int) -> list[list[int]]:
@@ -121,8 +238,7 @@ def sharded_bank(img, spec, kind, group=None, compute=None, radius: float = 3.0)
     if world > 1:
         dist.broadcast(img, 0, group=group)
     sig = [spec.sigma_for(i) for i in range(len(spec.frequencies))]
-    costs = bank_unit_costs(spec.frequencies, sig, spec.orientations_n, radius)
-    units = lpt_assign(costs, world)[rank]
+    units = partition_units(spec.frequencies, sig, spec.orientations_n, world, radius)[rank]
     if compute is None:
         from .device import compute_bank as compute_dev
 

@@ -294,9 +294,9 @@ def test_config5_all_entries_vs_gpu_bruteforce(fg):
     spec = fg.BankSpec(tuple(cfg["freqs"]), 16, tuple(cfg["sigmas"]))
     t32 = torch.from_numpy(f).cuda()
     t64 = torch.from_numpy(f.astype(np.float64)).cuda()
-    costs = P.bank_unit_costs(cfg["freqs"], cfg["sigmas"], 16, 3.0)
+
     worst = 0.0
-    for units in P.lpt_assign(costs, 8):
+    for units in P.partition_units(cfg["freqs"], cfg["sigmas"], 16, 8, 3.0):
         out = compute_bank(t32, spec, fg.ExactFIR(3.0), True, units)[0]
         worst = max(worst, _bruteforce_worst(fg, t64, spec, out, P.unit_entries(units, 16)))
         del out

@@ -34,6 +34,32 @@ def test_lpt_units_balanced_config5():
         assert sorted(ent) == sorted((i, k) for i in range(5) for k in range(16))
 
 
+def test_partition_units_config5():
+    """Contiguous runs per rank (shared row launches) + local search; every unit once;
+    modelled efficiency at 2/4/8 ranks against the measured cost model."""
+    freqs = [math.pi / 2 ** j for j in range(1, 6)]
+    sig = [2.0 ** j for j in range(1, 6)]
+    total = P.partition_cost([list(range(45))], sig, 16)[0]
+    assert abs(total * 67.108864 - 40.7) < 2.0  # the measured config-5 step (profiles/r02/unit_costs_c5.json)
+    for world, eff in ((1, 1.0), (2, 0.97), (4, 0.95), (8, 0.85)):
+        parts = P.partition_units(freqs, sig, 16, world)
+        assert sorted(u for p in parts for u in p) == list(range(45))
+        c = P.partition_cost(parts, sig, 16)
+        assert total / world / max(c) >= eff, (world, total / world / max(c))
+    # partition beats unit-LPT (which splits frequencies across ranks and loses row sharing)
+    lpt = P.lpt_assign(P.bank_unit_costs(freqs, sig, 16), 8)
+    assert max(P.partition_cost(P.partition_units(freqs, sig, 16, 8), sig, 16)) < max(P.partition_cost(lpt, sig, 16))
+
+
+def test_run_cost_model_matches_measurements():
+    """A few measured B200 points of profiles/r02/unit_costs_c5.json (ms, 8192^2)."""
+    mpx = 67.108864
+    for sigma, ks, ms in ((32.0, range(9), 18.53), (16.0, range(9), 9.45), (8.0, [3], 0.835), (4.0, range(5), 1.97),
+                          (2.0, [4], 0.479), (32.0, [8], 2.374)):
+        got = P.run_cost(sigma, ks, 16, 3.0, mpx)
+        assert abs(got - ms) / ms < 0.15, (sigma, list(ks), got, ms)
+
+
 def test_sdft_heads_cover_all_bins():
     for world in (1, 2, 4, 8):
         parts = P.sdft_heads(16, world)
