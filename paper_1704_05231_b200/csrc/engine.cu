@@ -698,53 +698,61 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
             // the halo and shared-memory footprint make it a wash (measured).
             // FGB_FUSED_BANK=<max h> overrides (0 disables).
             static const int fused_max_h = std::getenv("FGB_FUSED_BANK") ? std::atoi(std::getenv("FGB_FUSED_BANK")) : 6;
-            if (!box && !row_only && !col_only && nj <= std::min(kMaxND, 5) && h <= fused_max_h &&
-                bank_fused_ok(h, nj) && (int64_t)H * W >= 4096) {
-                Step<T> st;
-                st.kind = ST_BANKF;
-                st.name = "bank_fused";
-                st.H = H;
-                st.W = W;
-                st.src = img;
-                st.dst = out;
-                st.h = h;
-                st.nheads = nj;  // nd
-                const int ndp = (nj + 1) & ~1;
-                const int hp = bank_fused_pad(h);
-                const int ntp = bank_fused_pad(nt);
-                for (int t = 0; t <= hp; ++t)
-                    for (int k = 0; k < ndp; ++k) {
-                        double kr = 0.0, ki = 0.0;
-                        if (k < nj && t <= h) {
-                            kr = w[h + t] * std::cos(jobs[k].wc * t);
-                            ki = -w[h + t] * std::sin(jobs[k].wc * t);
+            // More than 5 directs (config 5: 9 per frequency) run as balanced groups of <= 5, one
+            // fused launch each: config 5's sigma = 2 frequency 2.5 ms instead of 3.4 ms for the
+            // row + column launches (profiles/r02/unit_costs_c5.json).
+            const int ng = (nj + 4) / 5;
+            if (!box && !row_only && !col_only && h <= fused_max_h && (int64_t)H * W >= 4096 &&
+                bank_fused_ok(h, (nj + ng - 1) / ng)) {
+                for (int gi = 0; gi < ng; ++gi) {
+                    const int g0 = gi * nj / ng, g1 = (gi + 1) * nj / ng, gn = g1 - g0;
+                    Step<T> st;
+                    st.kind = ST_BANKF;
+                    st.name = "bank_fused";
+                    st.H = H;
+                    st.W = W;
+                    st.src = img;
+                    st.dst = out;
+                    st.h = h;
+                    st.nheads = gn;  // nd
+                    const int ndp = (gn + 1) & ~1;
+                    const int hp = bank_fused_pad(h);
+                    const int ntp = bank_fused_pad(nt);
+                    for (int t = 0; t <= hp; ++t)
+                        for (int k = 0; k < ndp; ++k) {
+                            double kr = 0.0, ki = 0.0;
+                            if (k < gn && t <= h) {
+                                kr = w[h + t] * std::cos(jobs[g0 + k].wc * t);
+                                ki = -w[h + t] * std::sin(jobs[g0 + k].wc * t);
+                            }
+                            st.bf_w.push_back((float)kr);
+                            st.bf_w.push_back((float)ki);
                         }
-                        st.bf_w.push_back((float)kr);
-                        st.bf_w.push_back((float)ki);
-                    }
-                st.bf_colw_off = (int)st.bf_w.size();
-                int counted = 0;
-                for (int k = 0; k < nj; ++k) {
-                    for (int q = 0; q < ntp; ++q) {
-                        double ka = 0.0, kb = 0.0;
-                        if (q < nt) {
-                            const double t = (double)(q - h);
-                            ka = w[q] * std::cos(jobs[k].ws * t);
-                            kb = w[q] * std::sin(jobs[k].ws * t);
+                    st.bf_colw_off = (int)st.bf_w.size();
+                    int counted = 0;
+                    for (int k = 0; k < gn; ++k) {
+                        const DirectJob& jb = jobs[g0 + k];
+                        for (int q = 0; q < ntp; ++q) {
+                            double ka = 0.0, kb = 0.0;
+                            if (q < nt) {
+                                const double t = (double)(q - h);
+                                ka = w[q] * std::cos(jb.ws * t);
+                                kb = w[q] * std::sin(jb.ws * t);
+                            }
+                            st.bf_w.push_back((float)ka);
+                            st.bf_w.push_back((float)kb);
                         }
-                        st.bf_w.push_back((float)ka);
-                        st.bf_w.push_back((float)kb);
+                        BankFusedOut o;
+                        o.direct = jb.out_direct;
+                        o.mirror = jb.out_mirror;
+                        st.bf_out.push_back(o);
+                        counted += 1 + (jb.out_mirror >= 0 ? 1 : 0);
                     }
-                    BankFusedOut o;
-                    o.direct = jobs[k].out_direct;
-                    o.mirror = jobs[k].out_mirror;
-                    st.bf_out.push_back(o);
-                    counted += 1 + (jobs[k].out_mirror >= 0 ? 1 : 0);
+                    const double sfl = 4.0 * h + 1;
+                    st.flops = ((double)gn * (2.0 * sfl + 8.0) + (double)counted * (2.0 * sfl + 12.0)) * H * W;
+                    st.bytes = (double)H * W * sizeof(T) + (double)counted * H * W * sizeof(cx_t<T>);
+                    b.push(st);
                 }
-                const double sfl = 4.0 * h + 1;
-                st.flops = ((double)nj * (2.0 * sfl + 8.0) + (double)counted * (2.0 * sfl + 12.0)) * H * W;
-                st.bytes = (double)H * W * sizeof(T) + (double)counted * H * W * sizeof(cx_t<T>);
-                b.push(st);
                 *ws_need = std::max(*ws_need, need - (int64_t)nj * HW);
                 return FGB_OK;
             }

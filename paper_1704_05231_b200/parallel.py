@@ -40,7 +40,7 @@ def shard_images(n_images: int, world: int) -> list[list[int]]:
 #                                                                + _ROW_B*T per direct
 #   column job  (K2, theta and pi - theta from one J):          _COL_A + _COL_T*T, times
 #                0.65 for theta = 0 (no B term) and 0.91 for theta = pi/2 (real J)
-#   fused small-sigma launch (K5, h <= 6, <= 5 directs):       _FUSED_A + _FUSED_G per direct
+#   fused small-sigma launch (K5, h <= 6, groups of <= 5 directs): _FUSED_A per launch + _FUSED_G per direct
 _MPX = 67.108864  # the fit's 8192^2 image
 _ROW_A, _ROW_S, _ROW_B = 0.107 / _MPX, 0.00285 / _MPX, 0.0019 / _MPX
 _COL_A, _COL_T = 0.175 / _MPX, 0.00715 / _MPX
@@ -57,8 +57,8 @@ def run_cost(sigma: float, ks, n: int, radius: float = 3.0, mpx: float = 1.0) ->
     h = max(1, math.ceil(radius * sigma))
     t = 2 * h + 1
     nh = n // 2
-    if h <= 6 and len(ks) <= 5:
-        return mpx * (_FUSED_A + _FUSED_G * len(ks))
+    if h <= 6:  # fused launches of <= 5 directs each
+        return mpx * (_FUSED_A * -(-len(ks) // 5) + _FUSED_G * len(ks))
     launches = -(-len(ks) // _ROW_GROUP)
     row = launches * (_ROW_A + _ROW_S * t) + len(ks) * _ROW_B * t
     col = 0.0
