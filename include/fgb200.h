@@ -24,6 +24,7 @@
  *   fgb_iir_coeffs      make_coeffs           gaussian.py:164-185
  *   fgb_sampled_gaussian sampled_gaussian     gaussian.py:188-195
  *   fgb_pad_radius      pad_radius            gaussian.py:198-212
+ *   fgb_ser_sums        ser                   metrics.py:63-83  (device reduction)
  *   fgb_smooth_lines    smooth_lines          gaussian.py:245-285
  *                       (smooth_1d / smooth_pair_1d gaussian.py:288-302 are
  *                        one / two lines of it)
@@ -199,6 +200,13 @@ int32_t fgb_localized_dft(const fgb_sdft_desc* d, int32_t u, int32_t v, double r
 int32_t fgb_fir_gabor_host(const fgb_filter_desc* d, double radius, const void* img_host, void* out_host);
 int32_t fgb_localized_dft_host(const fgb_sdft_desc* d, int32_t u, int32_t v, double radius, const void* img_host,
                                void* out_host);
+
+/* ---- SER on the device (metrics.py:63-83) ------------------------------ */
+/* approx, truth: n interleaved complex device elements (FGB_F32 / FGB_F64).
+ * out = (sum tr^2, sum (ar - tr)^2, sum ti^2, sum (ai - ti)^2) in fp64, a
+ * deterministic reduction; SER(part) = 10 log10(signal / error) with the
+ * reference's +inf / -inf sentinels applied by the caller.  Synchronous. */
+int32_t fgb_ser_sums(const void* approx, const void* truth, int64_t n, int32_t dtype, double out[4], void* stream);
 
 /* ---- GBNK container from device outputs (image_io.py:157-179) ---------- */
 /* Writes n_entries interleaved-complex [H][W] device planes (dtype FGB_F32 /

@@ -127,6 +127,7 @@ _SIGS = {
     "fgb_sdft_bin": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, C.c_int32, _vp, _vp, _vp]),
     "fgb_sdft_horizontal": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, _vp, _vp, _vp]),
     "fgb_smooth_lines": (C.c_int32, [_P(fgb_lines_desc), _vp, _vp, _vp]),
+    "fgb_ser_sums": (C.c_int32, [_vp, _vp, C.c_int64, C.c_int32, _P(C.c_double), _vp]),
     "fgb_smooth_lines_host": (C.c_int32, [_P(fgb_lines_desc), _vp, _vp]),
     "fgb_bank_host": (C.c_int32, [_P(fgb_bank_desc), _vp, _vp]),
     "fgb_filter_host": (C.c_int32, [_P(fgb_filter_desc), _vp, _vp]),

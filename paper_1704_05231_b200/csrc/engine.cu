@@ -39,6 +39,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fgb200.h"
 #include "kernels.h"
 
@@ -54,6 +56,10 @@ double probe_ffma2_tflops(int mode);
 // errors
 // ===========================================================================
 static thread_local std::string g_err;
+struct NvtxRange {  // scoped NVTX range (balanced on every return path)
+    explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 static int32_t fail(int32_t code, const std::string& msg) {
     g_err = msg;
     return code;
@@ -1362,6 +1368,7 @@ struct Ctx {
     cudaStream_t ws_stream = nullptr;
     bool ws_pending = false;
     std::map<std::string, std::unique_ptr<DevBuf>> line_taps;  // fgb_smooth_lines tap tables (immutable)
+    DevBuf ser_scratch;                                         // fgb_ser_sums partials
 };
 static int32_t ws_acquire(Ctx& cx, cudaStream_t s) {
     if (!cx.ws_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.ws_ev, cudaEventDisableTiming));
@@ -1492,6 +1499,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
             ProfRec pr{detail ? std::string(st.name) + "." + std::to_string(sidx) : std::string(st.name), nullptr, nullptr,
                        st.flops * nb, st.bytes * nb};
             ++sidx;
+            const NvtxRange nvtx_step(st.name);  // per-step NVTX range (no-op without an attached tool)
             if (g_prof) {
                 pr.e0 = pool_event();
                 pr.e1 = pool_event();
@@ -2130,6 +2138,25 @@ int32_t fgb_sdft_bin(const fgb_sdft_desc* d, int32_t u, int32_t v, const void* i
     return d->img.dtype == FGB_F32 ? sdft_t<float>(d, u, v, img, out, s) : sdft_t<double>(d, u, v, img, out, s);
 }
 
+int32_t fgb_ser_sums(const void* approx, const void* truth, int64_t n, int32_t dtype, double out[4], void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (n < 0 || !out) return fail(FGB_EINVAL, "bad SER arguments");
+    if (dtype != FGB_F32 && dtype != FGB_F64) return fail(FGB_EINVAL, "dtype must be FGB_F32 or FGB_F64");
+    if (n == 0) {
+        for (int k = 0; k < 4; ++k) out[k] = 0.0;
+        return FGB_OK;
+    }
+    Ctx& cx = ctx();
+    cudaStream_t s = (cudaStream_t)stream;
+    FGB_TRY(cx.ser_scratch.ensure(ser_scratch_doubles() * sizeof(double)));
+    double* scr = (double*)cx.ser_scratch.p;
+    g_launches += 2;
+    if (dtype == FGB_F32) FGB_CUDA(launch_ser<float>((const float2*)approx, (const float2*)truth, n, scr, s));
+    else FGB_CUDA(launch_ser<double>((const double2*)approx, (const double2*)truth, n, scr, s));
+    FGB_CUDA(cudaMemcpyAsync(out, scr, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FGB_CUDA(cudaStreamSynchronize(s));
+    return FGB_OK;
+}
 int32_t fgb_smooth_lines(const fgb_lines_desc* d, const void* lines, void* out, void* stream) {
     std::lock_guard<std::mutex> lk(g_mu);
     FGB_TRY(validate_lines(d));

@@ -181,6 +181,13 @@ template <typename T> struct LinesIirArgs {
 template <typename T> cudaError_t launch_lines_corr(const LinesCorrArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_lines_iir(const LinesIirArgs<T>& a, cudaStream_t s);
 
+// ---- SER on the device (ser.cu; metrics.py:63-83) -------------------------
+// scratch[0..3] <- (sum tr^2, sum (ar-tr)^2, sum ti^2, sum (ai-ti)^2); scratch holds
+// ser_scratch_doubles() doubles.  Deterministic (fixed-order two-pass reduction).
+size_t ser_scratch_doubles();
+template <typename T>
+cudaError_t launch_ser(const cx_t<T>* a, const cx_t<T>* t, int64_t n, double* scratch, cudaStream_t s);
+
 // ---- output layout conversion (gbnk.cu) -----------------------------------
 // [entries][plane] interleaved complex -> [entries][2][plane] f64 (re plane,
 // im plane), *nonfinite |= 1 if any value is NaN / inf.

@@ -139,3 +139,48 @@ def compute_bank(img: torch.Tensor, spec: BankSpec, kind, reuse: bool = True, un
 def sdft_full(img: torch.Tensor, spec: SdftSpec, heads=None) -> torch.Tensor:
     img3 = _check_img(img)
     return SdftPlan(tuple(img3.shape), spec, _prec(img3), heads)(img3)
+
+
+def gabor_filter(img: torch.Tensor, p, kind) -> torch.Tensor:
+    """One filter on a device image [H, W] (gabor.py:172-176): complex [H, W] on the device."""
+    from .gabor import _filter_desc
+
+    img3 = _check_img(img)
+    b, h, w = img3.shape
+    d = _filter_desc(h, w, p, kind, _prec(img3))
+    d.img.pitch, d.img.batch, d.img.batch_stride = img3.stride(1), b, img3.stride(0)
+    out = torch.empty((b, h, w), dtype=_cplx(_prec(img3)), device=img3.device)
+    N.check(N.lib.fgb_filter(C.byref(d), C.c_void_p(img3.data_ptr()), C.c_void_p(out.data_ptr()),
+                             C.c_void_p(_stream(None))))
+    return out[0] if img.dim() == 2 else out
+
+
+def fir_gabor(img: torch.Tensor, p, radius: float = 6.0) -> torch.Tensor:
+    """GPU brute-force 2-D tap sum (oracle.py:53-66) of a device image."""
+    from .gabor import _filter_desc
+    from .gaussian import ExactFIR
+
+    img3 = _check_img(img)
+    b, h, w = img3.shape
+    d = _filter_desc(h, w, p, ExactFIR(radius), _prec(img3))
+    d.img.pitch, d.img.batch, d.img.batch_stride = img3.stride(1), b, img3.stride(0)
+    out = torch.empty((b, h, w), dtype=_cplx(_prec(img3)), device=img3.device)
+    N.check(N.lib.fgb_fir_gabor(C.byref(d), float(radius), C.c_void_p(img3.data_ptr()), C.c_void_p(out.data_ptr()),
+                                C.c_void_p(_stream(None))))
+    return out[0] if img.dim() == 2 else out
+
+
+def ser_sums(approx: torch.Tensor, truth: torch.Tensor):
+    """(signal_re, error_re, signal_im, error_im) of two device complex tensors,
+    reduced on the GPU in fp64 (fgb_ser_sums, deterministic)."""
+    if approx.shape != truth.shape:
+        raise ValueError("SER operands must share dimensions")
+    if approx.dtype != truth.dtype or approx.dtype not in (torch.complex64, torch.complex128):
+        raise ValueError("SER operands must be complex64 or complex128 of one dtype")
+    if not (approx.is_cuda and truth.is_cuda and approx.is_contiguous() and truth.is_contiguous()):
+        raise ValueError("SER operands must be contiguous CUDA tensors")
+    out = (C.c_double * 4)()
+    dt = N.FGB_F32 if approx.dtype == torch.complex64 else N.FGB_F64
+    N.check(N.lib.fgb_ser_sums(C.c_void_p(approx.data_ptr()), C.c_void_p(truth.data_ptr()), approx.numel(), dt, out,
+                               C.c_void_p(_stream(None))))
+    return tuple(out)

@@ -302,3 +302,37 @@ def test_config5_all_entries_vs_gpu_bruteforce(fg):
         del out
         torch.cuda.empty_cache()
     assert worst <= 1e-5, worst
+
+
+@pytest.mark.gpu
+def test_gpu_ser_device_reduction(fg, golden):
+    """SER (metrics.py:63-83) reduced on the device equals the reference's golden
+    values and the host formula; sentinels +inf / -inf; deterministic."""
+    import torch
+
+    z, meta = golden
+    f3 = z["f3"]
+    a = torch.from_numpy(f3 * 1.0 - 1j * (f3 / 2)).cuda()                 # _ents[0][1] of make_golden.py
+    b = torch.from_numpy((f3 * 1.01 + 0.3) + 1j * (-f3 / 2 + 0.01)).cuda()  # _b
+    for part in ("real", "imag"):
+        got = fg.ser(b, a, part)
+        assert abs(got - meta["ser"][part]) <= 1e-9 * abs(meta["ser"][part]), (part, got)
+        assert fg.ser(b, a, part) == got  # bit-identical rerun
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(333, 517)) + 1j * rng.normal(size=(333, 517))
+    y = x + 1e-3 * (rng.normal(size=x.shape) + 1j * rng.normal(size=x.shape))
+    hx, hy = fg.ComplexImage.from_planes(x.real, x.imag), fg.ComplexImage.from_planes(y.real, y.imag)
+    for dt in (torch.complex128, torch.complex64):
+        tx, ty = torch.from_numpy(x).to(dt).cuda(), torch.from_numpy(y).to(dt).cuda()
+        hx2 = fg.ComplexImage.from_planes(tx.real.double().cpu().numpy(), tx.imag.double().cpu().numpy())
+        hy2 = fg.ComplexImage.from_planes(ty.real.double().cpu().numpy(), ty.imag.double().cpu().numpy())
+        for part in ("real", "imag"):
+            assert abs(fg.ser(ty, tx, part) - fg.ser(hy2, hx2, part)) < 1e-9
+    assert fg.ser(torch.from_numpy(x).cuda(), torch.from_numpy(x).cuda(), "real") == math.inf
+    zero = torch.zeros((4, 4), dtype=torch.complex128, device="cuda")
+    assert fg.ser(zero + 1, zero, "imag") == math.inf and fg.ser(zero + 1, zero, "real") == -math.inf
+    with pytest.raises(ValueError):
+        fg.ser(zero, zero, "both")
+    with pytest.raises(ValueError):
+        fg.ser(zero, torch.zeros((4, 5), dtype=torch.complex128, device="cuda"), "real")
+    del hx, hy
