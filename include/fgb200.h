@@ -54,6 +54,7 @@ extern "C" {
 #define FGB_ECUDA (-2)         /* CUDA runtime error                            */
 #define FGB_ENOMEM (-3)        /* device / pinned allocation failed             */
 #define FGB_EUNSUPPORTED (-4)  /* smoother kind not valid here (TypeError)      */
+#define FGB_ENCCL (-5)         /* NCCL error (fgb_mgpu_*)                       */
 
 #define FGB_F32 0
 #define FGB_F64 1
@@ -215,6 +216,32 @@ int32_t fgb_ser_sums(const void* approx, const void* truth, int64_t n, int32_t d
  * the D2H of entry k+1 overlaps the file write of entry k. */
 int32_t fgb_gbnk_write_device(const char* path, const double* params, int32_t n_entries, int32_t height, int32_t width,
                               int32_t dtype, const void* dev_entries, int32_t sdft, void* stream);
+
+/* ---- multi-GPU: one process per GPU, library-owned NCCL communicator ---- */
+/* (replaces the reference's orientation thread pool,
+ * bank.py:77-87.)  Rank 0 calls fgb_mgpu_unique_id and the host shares the
+ * 128 bytes (torch.distributed / MPI / a file); every rank calls
+ * fgb_mgpu_init.  The only collective is one ncclBroadcast of rank 0's input
+ * image into every rank's device buffer `img` (same geometry everywhere), then
+ * each rank computes its share into its own compact output:
+ *   bank: the (frequency, direct k) units of fgb_mgpu_bank_units -- contiguous
+ *         runs per rank from an exact linear partition over a B200-measured
+ *         device-time model + local search (parallel.py:partition_units);
+ *         output layout as fgb_bank_desc.units; fgb_mgpu_bank_entries gives its
+ *         entry count;
+ *   SDFT: the conjugate u-pair heads of fgb_mgpu_sdft_heads (layout as
+ *         fgb_sdft_desc.u_heads).
+ * The *_units / *_heads partition functions are host-only (no GPU, no NCCL). */
+#define FGB_MGPU_ID_BYTES 128
+int32_t fgb_mgpu_unique_id(unsigned char id[FGB_MGPU_ID_BYTES]);
+int32_t fgb_mgpu_init(const unsigned char id[FGB_MGPU_ID_BYTES], int32_t world, int32_t rank, int32_t device);
+int32_t fgb_mgpu_finalize(void);
+int32_t fgb_mgpu_bank_units(const fgb_bank_desc* d, int32_t world, int32_t rank, int32_t* units, int32_t cap);
+int32_t fgb_mgpu_sdft_heads(int32_t m, int32_t world, int32_t rank, int32_t* heads, int32_t cap);
+int32_t fgb_mgpu_bank_entries(const fgb_bank_desc* d);
+int32_t fgb_mgpu_bank(const fgb_bank_desc* d, void* img, void* out, void* stream);
+int32_t fgb_mgpu_sdft(const fgb_sdft_desc* d, void* img, void* out, void* stream);
+const char* fgb_mgpu_last_error(void);
 
 /* ---- measurement ------------------------------------------------------- */
 /* Live per-kernel timing: while enabled, every launch is bracketed by CUDA

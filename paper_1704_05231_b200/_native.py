@@ -28,6 +28,8 @@ FGB_EINVAL = -1
 FGB_ECUDA = -2
 FGB_ENOMEM = -3
 FGB_EUNSUPPORTED = -4
+FGB_ENCCL = -5
+FGB_MGPU_ID_BYTES = 128
 FGB_F32 = 0
 FGB_F64 = 1
 FGB_SMOOTH_FIR = 0
@@ -145,6 +147,15 @@ _SIGS = {
     "fgb_localized_dft_host": (C.c_int32, [_P(fgb_sdft_desc), C.c_int32, C.c_int32, C.c_double, _vp, _vp]),
     "fgb_gbnk_write_device": (C.c_int32, [C.c_char_p, _P(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                           _vp, C.c_int32, _vp]),
+    "fgb_mgpu_unique_id": (C.c_int32, [_P(C.c_ubyte)]),
+    "fgb_mgpu_init": (C.c_int32, [_P(C.c_ubyte), C.c_int32, C.c_int32, C.c_int32]),
+    "fgb_mgpu_finalize": (C.c_int32, []),
+    "fgb_mgpu_bank_units": (C.c_int32, [_P(fgb_bank_desc), C.c_int32, C.c_int32, _P(C.c_int32), C.c_int32]),
+    "fgb_mgpu_sdft_heads": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, _P(C.c_int32), C.c_int32]),
+    "fgb_mgpu_bank_entries": (C.c_int32, [_P(fgb_bank_desc)]),
+    "fgb_mgpu_bank": (C.c_int32, [_P(fgb_bank_desc), _vp, _vp, _vp]),
+    "fgb_mgpu_sdft": (C.c_int32, [_P(fgb_sdft_desc), _vp, _vp, _vp]),
+    "fgb_mgpu_last_error": (C.c_char_p, []),
     "fgb_profile_enable": (None, [C.c_int32]),
     "fgb_profile_read": (C.c_int32, [_P(fgb_prof_entry), C.c_int32]),
     "fgb_launch_count": (C.c_int64, []),
@@ -166,11 +177,11 @@ def last_error() -> str:
     return (lib.fgb_last_error() or b"").decode()
 
 
-def check(rc: int) -> int:
+def check(rc: int, mgpu: bool = False) -> int:
     """Map a negative status to the reference's exception types."""
     if rc >= 0:
         return rc
-    msg = last_error()
+    msg = (lib.fgb_mgpu_last_error() or b"").decode() if mgpu else last_error()
     if rc == FGB_EINVAL:
         raise ValueError(msg)
     if rc == FGB_EUNSUPPORTED:

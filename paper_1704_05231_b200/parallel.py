@@ -90,10 +90,7 @@ def partition_units(freqs, sigmas, n: int, world: int, radius: float = 3.0) -> l
     world = max(1, min(world, m))
 
     def seg_cost(a, b):  # units order[a:b]
-        runs: dict[int, list[int]] = {}
-        for i, k in order[a:b]:
-            runs.setdefault(i, []).append(k)
-        return sum(run_cost(sigmas[i], ks, n, radius) for i, ks in runs.items())
+        return partition_cost([[i * (nh + 1) + k for i, k in order[a:b]]], sigmas, n, radius)[0]
 
     cost = [[0.0] * (m + 1) for _ in range(m + 1)]
     for a in range(m):
@@ -161,7 +158,10 @@ def partition_cost(parts, sigmas, n: int, radius: float = 3.0) -> list[float]:
         runs: dict[int, list[int]] = {}
         for u in p:
             runs.setdefault(u // (nh + 1), []).append(u % (nh + 1))
-        out.append(sum(run_cost(sigmas[i], ks, n, radius) for i, ks in runs.items()))
+        c = 0.0  # fixed summation order (frequency, then k) -- mgpu.cu sums the same way
+        for i in sorted(runs):
+            c += run_cost(sigmas[i], sorted(runs[i]), n, radius)
+        out.append(c)
     return out
 
 
@@ -246,3 +246,46 @@ def sharded_bank(img, spec, kind, group=None, compute=None, radius: float = 3.0)
             return compute_dev(im, sp, kd, True, un)[0]
     out = compute(img, spec, kind, units)
     return out, unit_entries(units, spec.orientations_n)
+
+
+class LibComm:
+    """The C ABI's own multi-GPU driver (fgb_mgpu_*, csrc/mgpu.cu): one process
+    per GPU, libfgb200 owns the NCCL communicator; the 128-byte NCCL id is
+    shared over ``torch.distributed`` (any backend).  ``bank`` / ``sdft``
+    broadcast rank 0's device image (one ncclBroadcast) and compute this
+    rank's partition -- the same partition as ``partition_units`` /
+    ``sdft_heads`` (restated in C++; a CPU test checks they agree)."""
+
+    def __init__(self, world: int, rank: int, device: int, group=None):
+        import ctypes as C
+
+        from . import _native as N
+
+        self.N, self.C = N, C
+        self.world, self.rank = world, rank
+        idb = (C.c_ubyte * N.FGB_MGPU_ID_BYTES)()
+        if rank == 0:
+            N.check(N.lib.fgb_mgpu_unique_id(idb), mgpu=True)
+        if world > 1:
+            import torch.distributed as dist
+
+            obj = [bytes(idb) if rank == 0 else None]
+            dist.broadcast_object_list(obj, 0, group=group)
+            idb = (C.c_ubyte * N.FGB_MGPU_ID_BYTES).from_buffer_copy(obj[0])
+        N.check(N.lib.fgb_mgpu_init(idb, world, rank, device), mgpu=True)
+
+    def units(self, desc) -> list[int]:
+        buf = (self.C.c_int32 * 4096)()
+        n = self.N.check(self.N.lib.fgb_mgpu_bank_units(self.C.byref(desc), self.world, self.rank, buf, 4096), mgpu=True)
+        return list(buf[:n])
+
+    def bank(self, desc, img, out, stream=0):
+        self.N.check(self.N.lib.fgb_mgpu_bank(self.C.byref(desc), self.C.c_void_p(img.data_ptr()),
+                                              self.C.c_void_p(out.data_ptr()), self.C.c_void_p(stream)), mgpu=True)
+
+    def sdft(self, desc, img, out, stream=0):
+        self.N.check(self.N.lib.fgb_mgpu_sdft(self.C.byref(desc), self.C.c_void_p(img.data_ptr()),
+                                              self.C.c_void_p(out.data_ptr()), self.C.c_void_p(stream)), mgpu=True)
+
+    def close(self):
+        self.N.lib.fgb_mgpu_finalize()

@@ -137,3 +137,48 @@ def test_bench_two_ranks_gloo(config, size):
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["dist_backend"] == "gloo"
     assert line["scaling"] == "strong" and line["e2e"]["value"] > 0
+
+
+def test_library_nccl_driver_world1():
+    """fgb_mgpu_* (library-owned NCCL communicator) at world size 1 on this GPU:
+    the 'broadcast' is a no-op, the rank owns every unit / head, and the outputs
+    equal the plain calls bit for bit.  (Multi-rank NCCL needs one GPU per rank.)"""
+    import torch
+
+    import paper_1704_05231_b200 as fg
+    from paper_1704_05231_b200.device import BankPlan, SdftPlan
+    from paper_1704_05231_b200 import _native as N
+    from paper_1704_05231_b200.parallel import LibComm, partition_units
+
+    comm = LibComm(1, 0, 0)
+    try:
+        img = torch.from_numpy(np.random.default_rng(4).uniform(0, 1, (1, 256, 288)).astype(np.float32)).cuda()
+        plan = BankPlan(tuple(img.shape), fg.BankSpec(FREQS, 16, SIGMAS), fg.ExactFIR(3.0), "f32", True)
+        full = plan(img)
+        assert comm.units(plan.desc) == partition_units(FREQS, SIGMAS, 16, 1, 3.0)[0] == list(range(45))
+        assert N.lib.fgb_mgpu_bank_entries(C_byref(plan.desc)) == 80
+        out = torch.empty_like(full)
+        comm.bank(plan.desc, img, out, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        # world 1 owns all 45 units: compact order = per unit direct then mirror
+        from paper_1704_05231_b200.parallel import unit_entries
+
+        for j, (i, k) in enumerate(unit_entries(list(range(45)), 16)):
+            assert torch.equal(out[0, j], full[0, i * 16 + k])
+        sp = SdftPlan(tuple(img.shape), fg.SdftSpec(16, 16, fg.ExactFIR(3.0), 4.0), "f32")
+        sfull = sp(img)
+        sout = torch.empty_like(sfull)
+        comm.sdft(sp.desc, img, sout, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        from paper_1704_05231_b200.parallel import head_bins
+
+        for j, (u, v) in enumerate(head_bins(list(range(9)), 16)):
+            assert torch.equal(sout[0, j], sfull[0, u * 16 + v])
+    finally:
+        comm.close()
+
+
+def C_byref(x):
+    import ctypes
+
+    return ctypes.byref(x)

@@ -136,3 +136,35 @@ def test_gloo_world2_sharded_bank_equals_full():
             assert np.max(np.abs(plane.real - ref[3])) < 1e-12 and np.max(np.abs(plane.imag - ref[4])) < 1e-12
             seen.add((i, k))
     assert seen == {(i, k) for i in range(2) for k in range(8)}
+
+
+def test_c_abi_partition_equals_python():
+    """fgb_mgpu_bank_units / fgb_mgpu_sdft_heads (csrc/mgpu.cu, host-only) give the
+    same shards as parallel.partition_units / sdft_heads."""
+    import ctypes as C
+
+    from paper_1704_05231_b200 import _native as N
+    from paper_1704_05231_b200.bank import BankSpec, bank_desc
+    from paper_1704_05231_b200.gaussian import ExactFIR
+
+    cases = [([math.pi / 2 ** j for j in range(1, 6)], [2.0 ** j for j in range(1, 6)], 16),
+             ([math.pi / 2 ** j for j in range(1, 6)], [2.0 ** j for j in range(1, 6)], 8),
+             ([math.pi / 2 ** j for j in (1, 2, 3, 4)], [2.0, 4.0, 8.0, 16.0], 8),
+             ([0.5, 1.0, 2.0], [5.0, 1.5, 0.9], 7), ([1.0], [3.0], 1)]
+    for freqs, sig, n in cases:
+        d, _keep = bank_desc(64, 64, BankSpec(tuple(freqs), n, tuple(sig)), ExactFIR(3.0), "f32", True)
+        for world in (1, 2, 3, 4, 8, 64):
+            py = P.partition_units(freqs, sig, n, world, 3.0)
+            for r in range(world):
+                buf = (C.c_int32 * 512)()
+                cnt = N.check(N.lib.fgb_mgpu_bank_units(C.byref(d), world, r, buf, 512), mgpu=True)
+                assert list(buf[:cnt]) == (py[r] if r < len(py) else []), (freqs, n, world, r)
+    for m in (1, 4, 16, 32):
+        for world in (1, 2, 4, 8):
+            py = P.sdft_heads(m, world)
+            for r in range(world):
+                buf = (C.c_int32 * 64)()
+                cnt = N.check(N.lib.fgb_mgpu_sdft_heads(m, world, r, buf, 64), mgpu=True)
+                assert list(buf[:cnt]) == py[r], (m, world, r)
+    with pytest.raises(ValueError):
+        N.check(N.lib.fgb_mgpu_sdft_heads(16, 2, 2, (C.c_int32 * 4)(), 4), mgpu=True)
