@@ -766,8 +766,11 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
         // ---- row stage ----
         if (!col_only) {
             if (!box) {
-                for (int g0 = 0; g0 < nj; g0 += kMaxND) {
-                    const int g1 = std::min(nj, g0 + kMaxND);
+                // row launches of <= gmax directs, balanced (9 -> 5 + 4 with gmax 5)
+                static const int gmax = std::max(1, std::min(kMaxND, std::getenv("FGB_ROW_GROUP") ? std::atoi(std::getenv("FGB_ROW_GROUP")) : kMaxND));
+                const int ngr = (nj + gmax - 1) / gmax;
+                for (int gi = 0; gi < ngr; ++gi) {
+                    const int g0 = gi * nj / ngr, g1 = (gi + 1) * nj / ngr;
                     std::vector<double> fr;
                     std::vector<cd> ph;
                     std::vector<int64_t> dst;

@@ -5,7 +5,7 @@ path, regex, skip = sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) 
 out = subprocess.run(['ncu', '-i', path, '--page', 'source', '--csv', '--kernel-name', 'regex:' + regex,
                       '--launch-skip', str(skip), '--launch-count', '1'], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hdr = rows[1]
+hdr = rows[1] if len(rows) > 1 and "Source" in rows[1] else rows[0]
 iS, iE = hdr.index('Source'), hdr.index('Instructions Executed')
 iW = hdr.index('Warp Stall Sampling (All Samples)')
 ops, samp, tot, ts = collections.Counter(), collections.Counter(), 0, 0

@@ -1,5 +1,5 @@
 """DRAM bytes per launch of each kernel family (ncu --metrics dram__bytes_*,
---clock-control none, cold-cache replay) -> profiles/r01/traffic.json, the
+--clock-control none, cold-cache replay) -> profiles/r02/traffic.json, the
 `roofline.traffic` figure bench.py reports for the dominant kernel.
 
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
@@ -18,7 +18,7 @@ NAMES = {"row_sym_kernel": "row_fir", "col_kernel": "col_fir", "bank_fused_kerne
 STAGE_HEADS = ("iir32_sum", "iir_fwd")
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
-out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r01", "traffic.json")
+out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02", "traffic.json")
 res = json.load(open(out_path)) if os.path.exists(out_path) else {}  # merged: configs not given keep their entries
 res["_how"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --metrics ... --clock-control none; "
                "cold-cache replay), averaged over the launches of one step; IIR: per stage (tools/traffic.py)")
