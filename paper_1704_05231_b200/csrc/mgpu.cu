@@ -36,7 +36,7 @@ constexpr double kMpx = 67.108864;
 constexpr double kRowA = 0.107 / kMpx, kRowS = 0.00285 / kMpx, kRowB = 0.0019 / kMpx;
 constexpr double kColA = 0.175 / kMpx, kColT = 0.00715 / kMpx;
 constexpr double kFusedA = 0.22 / kMpx, kFusedG = 0.225 / kMpx;
-constexpr int kRowGroup = 6;
+constexpr int kRowGroup = 8;  // engine: balanced row launches of <= kMaxND = 8 directs
 
 double run_cost(double sigma, const std::vector<int>& ks, int n, double radius) {
     if (ks.empty()) return 0.0;

@@ -36,7 +36,7 @@ def shard_images(n_images: int, world: int) -> list[list[int]]:
 # measurements in profiles/r02/unit_costs_c5.json (tools/unit_costs.py: every
 # contiguous k-range of every config-5 frequency, row / column launches split by
 # the live profile).  T = 2 ceil(r sigma) + 1 taps.
-#   row launch  (K1, up to 6 directs, symmetric pairs shared):  _ROW_A + _ROW_S*T per launch
+#   row launch  (K1, up to 8 directs, symmetric pairs shared):  _ROW_A + _ROW_S*T per launch
 #                                                                + _ROW_B*T per direct
 #   column job  (K2, theta and pi - theta from one J):          _COL_A + _COL_T*T, times
 #                0.65 for theta = 0 (no B term) and 0.91 for theta = pi/2 (real J)
@@ -45,7 +45,7 @@ _MPX = 67.108864  # the fit's 8192^2 image
 _ROW_A, _ROW_S, _ROW_B = 0.107 / _MPX, 0.00285 / _MPX, 0.0019 / _MPX
 _COL_A, _COL_T = 0.175 / _MPX, 0.00715 / _MPX
 _FUSED_A, _FUSED_G = 0.22 / _MPX, 0.225 / _MPX
-_ROW_GROUP = 6
+_ROW_GROUP = 8  # engine: balanced row launches of <= kMaxND = 8 directs
 
 
 def run_cost(sigma: float, ks, n: int, radius: float = 3.0, mpx: float = 1.0) -> float:
