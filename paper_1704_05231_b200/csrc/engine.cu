@@ -1372,6 +1372,8 @@ struct Ctx {
     bool ws_pending = false;
     std::map<std::string, std::unique_ptr<DevBuf>> line_taps;  // fgb_smooth_lines tap tables (immutable)
     DevBuf ser_scratch;                                         // fgb_ser_sums partials
+    DevBuf iir_cnt;                                             // iir32 arrival counters, zero between launches
+    size_t iir_cnt_zeroed = 0;                                  // bytes of iir_cnt known to be zero
 };
 static int32_t ws_acquire(Ctx& cx, cudaStream_t s) {
     if (!cx.ws_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.ws_ev, cudaEventDisableTiming));
@@ -1459,6 +1461,21 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     }
     if (!cx.fork_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.fork_ev, cudaEventDisableTiming));
     FGB_TRY(ws_acquire(cx, s));
+    // iir32 arrival counters (shared like the workspace, so after ws_acquire): one int per
+    // 32-line block, job and image of a chunk, per lane; zeroed once when (re)allocated
+    size_t cnt_lane = 0;
+    for (const auto& st : p.steps)
+        if (st.kind == ST_IIR) cnt_lane = std::max(cnt_lane, (size_t)((st.W + 31) / 32) * st.njobs * chunk);
+    int* cnt = nullptr;
+    if (cnt_lane) {
+        const size_t need = cnt_lane * std::max(1, p.nlanes) * sizeof(int);
+        if (need > cx.iir_cnt_zeroed) {
+            FGB_TRY(cx.iir_cnt.ensure(need));
+            FGB_CUDA(cudaMemsetAsync(cx.iir_cnt.p, 0, cx.iir_cnt.n, s));
+            cx.iir_cnt_zeroed = cx.iir_cnt.n;
+        }
+        cnt = (int*)cx.iir_cnt.p;
+    }
     const int64_t img_bs = (batch > 1) ? im.batch_stride : (int64_t)im.height * im.pitch;
     for (int b0 = 0; b0 < batch; b0 += chunk) {
         const int nb = std::min(chunk, batch - b0);
@@ -1586,6 +1603,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                         return fail(FGB_EINVAL, "internal: IIR scratch too small");
                     a.g = p.d_dbls() + st.g_off;
                     a.tab32 = p.d_tabs32();
+                    a.counters = cnt + (size_t)st.lane * cnt_lane;
                     if constexpr (sizeof(T) == 4) {
                         if (iir32_enabled()) {
                             FGB_CUDA(launch_iir32(a, s));

@@ -141,21 +141,25 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
     const int len = a.len, P = a.P, L = len + 2 * P;
     const int nb0 = sblk() * kSW;
     const int tid = threadIdx.y * kTX + threadIdx.x;
-    float4* tabm = reinterpret_cast<float4*>(smem);
-    float4* tabr = tabm + kSW;
-    const float sgn = (job.need >> 1) ? -1.f : 1.f;
-    const float osg = (job.sdft ? -1.f : 1.f) * (job.conj[0] ? -1.f : 1.f);
-    for (int i = tid; i < kSW; i += kTX * kSY) {
-        const int n = nb0 + i;
-        if (n < L) {
-            const float2 cs = a.tab32[job.tabm_off + n];
-            tabm[i] = make_float4(cs.x, cs.y, sgn * cs.y, -sgn * cs.x);
+    // the tables are built AFTER the input copies are issued (their global loads then overlap
+    // the tile's flight instead of delaying its issue)
+    auto tables = [&]() {
+        float4* tabm = reinterpret_cast<float4*>(smem);
+        float4* tabr = tabm + kSW;
+        const float sgn = (job.need >> 1) ? -1.f : 1.f;
+        const float osg = (job.sdft ? -1.f : 1.f) * (job.conj[0] ? -1.f : 1.f);
+        for (int i = tid; i < kSW; i += kTX * kSY) {
+            const int n = nb0 + i;
+            if (n < L) {
+                const float2 cs = a.tab32[job.tabm_off + n];
+                tabm[i] = make_float4(cs.x, cs.y, sgn * cs.y, -sgn * cs.x);
+            }
+            if (want_tabr && n >= P && n < P + len) {
+                const float2 cs = a.tab32[job.tabr_off + (n - P)];
+                tabr[i] = make_float4(cs.x, osg * cs.y, cs.y, -osg * cs.x);
+            }
         }
-        if (want_tabr && n >= P && n < P + len) {
-            const float2 cs = a.tab32[job.tabr_off + (n - P)];
-            tabr[i] = make_float4(cs.x, osg * cs.y, cs.y, -osg * cs.x);
-        }
-    }
+    };
     unsigned char* tile = smem + kTabBytes;
     // tile samples [nb0, nb0 + kSW) need no clamping when they map into [0, len)
     const bool inner = nb0 >= P && nb0 + kSW <= P + len;
@@ -201,6 +205,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
                 for (int r = tid; r < nrows; r += kTX * kSY)
                     bulk_g2s(t + r * kTX, blk + (int64_t)clampi(nb0 + r - P, 0, len - 1) * a.src_ss,
                              kTX * sizeof(float2), &bar);
+                tables();
                 mbar_wait(&bar, 0);
                 __syncthreads();  // (tables)
                 return;
@@ -221,6 +226,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
             }
         }
     }
+    tables();
     cp_async_wait_all();
     __syncthreads();
 }
@@ -784,10 +790,10 @@ cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream
     }
     const dim3 block(kTX, kSY);
     const dim3 grid((a.nseg + kSY - 1) / kSY, (a.lines + kTX - 1) / kTX, a.njobs * a.batch);
-    // arrival counters (one int per 32-line block and job) after the states; zeroed once per launch
-    const int64_t nS = grid.x;  // super-segments per line
-    int* counters = reinterpret_cast<int*>(a.state32 + (int64_t)a.njobs * a.batch * (a.nseg + nS) * 12 * a.lines);
-    cudaMemsetAsync(counters, 0, sizeof(int) * (size_t)grid.y * grid.z, s);
+    // arrival counters (one int per 32-line block and job): a library-owned buffer zeroed
+    // once at allocation; every launch leaves them zero again (the last CTA of a block
+    // resets its counter), so no memset launch per stage
+    int* counters = a.counters;
     iir32_sum<ROWS, CPLX><<<grid, block, smem, s>>>(a, q, counters);
     iir32_fin<ROWS, CPLX><<<grid, block, smem, s>>>(a, q);
     return cudaGetLastError();

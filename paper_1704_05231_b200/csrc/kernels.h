@@ -138,6 +138,8 @@ template <typename T> struct IirArgs {
     const double* g;         // [seglen][3]: first row of A^(m+1)
     const float2* tab32;     // fp32 copy of the tables (same offsets as tab_base; iir32.cu)
     float* state32;          // iir32.cu: [njobs*batch][nseg][12][lines] segment states (aliases `state`)
+    int* counters;           // iir32.cu: arrival counter per 32-line block and job; zero on entry, the
+                             // last CTA of each block resets its own (library-owned, zeroed once)
     double Aseg[9];          // A^seglen
     double Alast[9];         // A^(length of the last segment)
     int64_t src_bstride, dst_bstride;  // per image, in source / complex elements
