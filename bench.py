@@ -444,6 +444,17 @@ def build_workload(args, cfg, D):
     return plan, timg, imgs, units_step, bcast
 
 
+def fma_pipe(config, name):
+    """ncu FMA-pipe utilisation (%) of a kernel family on this config (profiles/r02/fma_pipe.json, committed):
+    the hardware-utilisation figure beside the reference-flop roofline (the row kernel's symmetric pairs
+    issue fewer flops than the reference counts, so its reference-flop `frac` can exceed 1)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "fma_pipe.json")) as fh:
+            return json.load(fh).get(f"cfg{config}/{name}")
+    except (OSError, ValueError):
+        return None
+
+
 def roofline(args, cfg, prof, nprof, fp32, hbm):
     """Dominant kernel (longest total time in the live profile) against its bound."""
     top = max(prof, key=lambda e: e["ms"]) if prof else None
@@ -458,13 +469,15 @@ def roofline(args, cfg, prof, nprof, fp32, hbm):
             continue
         if traffic is not None:
             break
+    fma = fma_pipe(args.config, top["name"])
     if cfg["kind"] == "sdft":
         ach = top["bytes"] / (top["ms"] * 1e-3) / 1e9
-        return {"bound": "hbm", "kernel": top["name"], "achieved": ach, "peak": hbm, "unit": "GB/s",
+        return {"bound": "hbm", "kernel": top["name"], "ncu_fma_pipe_pct": fma, "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": top["bytes"] / top["launches"],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
-    r = {"bound": "fp32", "kernel": top["name"], "achieved": ach, "peak": fp32, "unit": "TFLOP/s",
+    r = {"bound": "fp32", "kernel": top["name"], "ncu_fma_pipe_pct": fma, "achieved": ach, "peak": fp32,
+         "unit": "TFLOP/s",
          "frac": ach / fp32 if fp32 > 0 else None, "traffic": traffic,
          "algorithmic_flops_per_launch": top["flops"] / top["launches"],
          "peak_source": "live FFMA probe (fgb_probe_fp32_tflops); flops = reference OpCounters M+A"}
@@ -535,7 +548,8 @@ def run_ours(args, cfg, world, rank, local_rank):
         kernels = {e["name"]: {"launches_per_step": e["launches"] / nprof, "ms_per_launch": e["ms"] / e["launches"],
                                "share": e["ms"] / tot_ms,
                                "tflops": e["flops"] / (e["ms"] * 1e-3) / 1e12 if e["ms"] > 0 else None,
-                               "gbs": e["bytes"] / (e["ms"] * 1e-3) / 1e9 if e["ms"] > 0 else None} for e in prof}
+                               "gbs": e["bytes"] / (e["ms"] * 1e-3) / 1e9 if e["ms"] > 0 else None,
+                               "ncu_fma_pipe_pct": fma_pipe(args.config, e["name"])} for e in prof}
         roof = roofline(args, cfg, prof, nprof, fp32, hbm)
         step_roof = None
         if prof:
