@@ -207,7 +207,10 @@ __device__ __forceinline__ void stage_tile(unsigned char* smem, const IirArgs<fl
                              kTX * sizeof(float2), &bar);
                 tables();
                 mbar_wait(&bar, 0);
-                __syncthreads();  // (tables)
+                // each warp built exactly the table entries of its own segment (entry i = tid,
+                // segment ty = samples [32 ty, 32 ty + 32)) and every thread waited on the tile's
+                // mbarrier itself: a warp barrier is enough
+                __syncwarp();
                 return;
             }
             const float2* src = blk + threadIdx.x;
