@@ -3,7 +3,8 @@
 
 * linearity of the bank (config 5, 8192^2): bank(f + 2 g) = bank(f) + 2 bank(g);
 * conjugate symmetry of the localized DFT (config 4, 2048^2):
-  F(M-u, M-v) = conj F(u, v) exactly (sdft.py:209-212 fills them that way);
+  F(M-u, M-v) = conj F(u, v), bit-exact for the bins sdft.py:209-212 fills
+  that way (v > M/2), to rounding for pairs that are both computed;
 * batch independence (config 3): a batched call equals per-image calls bit for bit;
 * a constant image gives a constant response equal to the reference's DC gain of
   the filter (replicate padding keeps the constant up to the borders).
@@ -61,9 +62,15 @@ def test_config4_conjugate_symmetry_and_batch(fg):
     img = torch.from_numpy(bench.make_image(cfg, 0)[None]).cuda()
     for kind in (fg.ExactFIR(3.0), fg.RecursiveIIR()):
         out = SdftPlan(tuple(img.shape), fg.SdftSpec(m, m, kind, cfg["sigma"]), "f32")(img)[0]
+        scale = out.abs().amax()
         for u in range(m):
             for v in range(m):
-                assert torch.equal(out[((m - u) % m) * m + (m - v) % m], out[u * m + v].conj()), (u, v)
+                pu, pv = (m - u) % m, (m - v) % m
+                a, b = out[pu * m + pv], out[u * m + v].conj()
+                if v > m // 2:  # filled as the conjugate of a computed bin (sdft.py:209-212): bit-exact
+                    assert torch.equal(out[u * m + v], out[pu * m + pv].conj()), (u, v)
+                else:  # both computed: equal up to rounding (self-paired bins: real up to rounding)
+                    assert float((a - b).abs().amax() / scale) <= 1e-6, (u, v)
         del out
         torch.cuda.empty_cache()
 
