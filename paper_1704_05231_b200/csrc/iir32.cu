@@ -259,10 +259,33 @@ __device__ __forceinline__ In<ROWS, CPLX> make_in(unsigned char* smem, const Iir
     return in;
 }
 
+// Column stages, pass 1: no input tile.  Lines are adjacent threads and contiguous in
+// memory, so each sample row of a warp is one coalesced 256-byte (complex) / 128-byte
+// (real) load straight into registers; the thread never shares its samples, and pass 1
+// keeps nothing for later, so the 32 KB tile only cost occupancy (6 CTAs / SM).  Shared
+// memory holds the warp's own modulation-table entries, then the CTA summaries.
+template <bool CPLX> struct InS {
+    const float4* tabm;  // [i]: padded sample nb0 + i (this CTA's entries, built per warp)
+    const void* src;     // this thread's line (clamped to the last line)
+    int64_t ss;          // source elements between samples
+    int nb0, P, len;
+    __device__ __forceinline__ float2 z(int i) const {
+        const float4 t = tabm[i];
+        const int64_t n = clampi(nb0 + i - P, 0, len - 1);
+        if constexpr (CPLX) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(src) + n * ss);
+            return __ffma2_rn(make_float2(t.x, t.y), dup(v.x), __fmul2_rn(make_float2(t.z, t.w), dup(v.y)));
+        } else {
+            const float v = __ldg(reinterpret_cast<const float*>(src) + n * ss);
+            return __fmul2_rn(make_float2(t.x, t.y), dup(v));
+        }
+    }
+};
+
 // ---- pass 1: local forward sections -> end state e, backward-start sums b ----
-template <bool ROWS, bool CPLX, bool FULL>
-__device__ __forceinline__ void sum_body(const In<ROWS, CPLX>& in, int i0, int m, Sec& s, float2& br, float2& bcr,
-                                         float2& bci, const Iir32Par& q) {
+template <bool FULL, typename IN>
+__device__ __forceinline__ void sum_body(const IN& in, int i0, int m, Sec& s, float2& br, float2& bcr, float2& bci,
+                                         const Iir32Par& q) {
     // the short last segment of a line runs rolled (keeps the kernel's code small)
 #pragma unroll(FULL ? kM : 1)
     for (int i = 0; i < (FULL ? kM : m); ++i) {
@@ -385,29 +408,56 @@ __device__ void carry_block(float* sm, int kCS, float* g, int64_t NL, int nl, in
     }
 }
 
-template <bool ROWS, bool CPLX>
-__global__ void __launch_bounds__(kTX * kSY) iir32_sum(const IirArgs<float> a, const __grid_constant__ Iir32Par q, int* counters) {
+template <bool ROWS, bool CPLX, bool STREAM>
+__global__ void __launch_bounds__(kTX * kSY, STREAM ? 8 : 1) iir32_sum(const IirArgs<float> a, const __grid_constant__ Iir32Par q,
+                                                                     int* counters) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int jb = blockIdx.z % a.njobs, b = blockIdx.z / a.njobs;
     const IirJob<float>& job = a.jobs[jb];
-    stage_tile<ROWS, CPLX>(smem, a, job, b, false);
     const int x = lblk() * kTX + threadIdx.x;
     const int seg = sblk() * kSY + threadIdx.y;
     const int L = a.len + 2 * a.P, NL = a.lines;
     const int n0 = seg * kM;
+    if constexpr (STREAM) {
+        // each warp builds the table entries of its own segment (entry i = tid)
+        const int i = threadIdx.y * kTX + threadIdx.x, n = sblk() * kSW + i;
+        if (n < L) {
+            const float sgn = (job.need >> 1) ? -1.f : 1.f;
+            const float2 cs = a.tab32[job.tabm_off + n];
+            reinterpret_cast<float4*>(smem)[i] = make_float4(cs.x, cs.y, sgn * cs.y, -sgn * cs.x);
+        }
+        __syncwarp();
+    } else {
+        stage_tile<ROWS, CPLX>(smem, a, job, b, false);
+    }
     float sub[12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) sub[k] = 0.f;
     if (x < NL && n0 < L) {
         const int m = min(kM, L - n0);
-        const In<ROWS, CPLX> in = make_in<ROWS, CPLX>(smem, job);
         const int i0 = threadIdx.y * kM;
-        Sec s;
-        if (seg == 0) sec_steady(s, in.z(0), q);
-        else s.r = s.cr = s.ci = dup(0.f);
         float2 br = dup(0.f), bcr = dup(0.f), bci = dup(0.f);
-        if (m == kM) sum_body<ROWS, CPLX, true>(in, i0, m, s, br, bcr, bci, q);
-        else sum_body<ROWS, CPLX, false>(in, i0, m, s, br, bcr, bci, q);
+        Sec s;
+        auto run = [&](const auto& in) {
+            if (seg == 0) sec_steady(s, in.z(0), q);
+            else s.r = s.cr = s.ci = dup(0.f);
+            if (m == kM) sum_body<true>(in, i0, m, s, br, bcr, bci, q);
+            else sum_body<false>(in, i0, m, s, br, bcr, bci, q);
+        };
+        if constexpr (STREAM) {
+            InS<CPLX> in;
+            in.tabm = reinterpret_cast<const float4*>(smem);
+            const int64_t bo = job.src_off + (int64_t)b * a.src_bstride;
+            if constexpr (CPLX) in.src = reinterpret_cast<const float2*>(a.src_base) + bo + x;
+            else in.src = reinterpret_cast<const float*>(a.src_base) + bo + x;
+            in.ss = a.src_ss;
+            in.nb0 = sblk() * kSW;
+            in.P = a.P;
+            in.len = a.len;
+            run(in);
+        } else {
+            run(make_in<ROWS, CPLX>(smem, job));
+        }
         const float v[12] = {s.r.x, s.cr.x, s.ci.x, s.r.y, s.cr.y, s.ci.y, br.x, bcr.x, bci.x, br.y, bcr.y, bci.y};
 #pragma unroll
         for (int k = 0; k < 12; ++k) sub[k] = v[k];
@@ -420,10 +470,13 @@ __global__ void __launch_bounds__(kTX * kSY) iir32_sum(const IirArgs<float> a, c
     for (int k = 0; k < 12; ++k) sm[(threadIdx.y * 12 + k) * kTX + threadIdx.x] = sub[k];
     __syncthreads();
     const int nS = gridDim.x, K = min(kSY, a.nseg - sblk() * kSY);
-    if (threadIdx.y < 2 && x < NL) {
+    if (x < NL) {
         // local chains with zero super carries: s_loc_k (forward, entering sub k) and
-        // T_loc_k (backward, entering sub k from above); e_S / b_S close them
-        const int pl = threadIdx.y;
+        // T_loc_k (backward, entering sub k from above); e_S / b_S close them.  All four
+        // warps work: warps 0 / 1 (planes a / b) write the forward chain, warps 2 / 3 redo
+        // that short chain for their plane and run + write the backward one.
+        const int pl = threadIdx.y & 1;
+        const bool bwd = threadIdx.y >= 2;
         float sl[kSY][3];
         float r0 = 0.f, r1 = 0.f, r2 = 0.f;
 #pragma unroll
@@ -437,37 +490,45 @@ __global__ void __launch_bounds__(kTX * kSY) iir32_sum(const IirArgs<float> a, c
             const float n2_ = fmaf(Q[1], r2, fmaf(Q[2], r1, p[2 * kTX]));
             r0 = n0_; r1 = n1_; r2 = n2_;
         }
-        float t0 = 0.f, t1 = 0.f, t2 = 0.f;
         float* sb = a.state32 + ((int64_t)blockIdx.z * a.nseg + sblk() * kSY) * 12 * NL + x;  // sub 0 of this CTA
-#pragma unroll
-        for (int k = kSY - 1; k >= 0; --k) {
-            if (k >= K) continue;
-            float* d = sb + (int64_t)k * 12 * NL;
-            d[(int64_t)(3 * pl) * NL] = sl[k][0];
-            d[(int64_t)(3 * pl + 1) * NL] = sl[k][1];
-            d[(int64_t)(3 * pl + 2) * NL] = sl[k][2];
-            d[(int64_t)(6 + 3 * pl) * NL] = t0;
-            d[(int64_t)(7 + 3 * pl) * NL] = t1;
-            d[(int64_t)(8 + 3 * pl) * NL] = t2;
-            const float* p = sm + (k * 12 + 6 + 3 * pl) * kTX + threadIdx.x;
-            const int lt = sblk() * kSY + k == a.nseg - 1;
-            const float* Q = q.Q[lt];
-            const float* M = q.Mb[lt];
-            const float c0 = fmaf(M[0], sl[k][0], fmaf(M[1], sl[k][1], fmaf(M[2], sl[k][2], p[0])));
-            const float c1 = fmaf(M[3], sl[k][0], fmaf(M[4], sl[k][1], fmaf(M[5], sl[k][2], p[kTX])));
-            const float c2 = fmaf(M[6], sl[k][0], fmaf(M[7], sl[k][1], fmaf(M[8], sl[k][2], p[2 * kTX])));
-            const float n0_ = fmaf(Q[0], t0, c0);
-            const float n1_ = fmaf(Q[1], t1, fmaf(-Q[2], t2, c1));
-            const float n2_ = fmaf(Q[1], t2, fmaf(Q[2], t1, c2));
-            t0 = n0_; t1 = n1_; t2 = n2_;
-        }
         float* su = a.state32 + ((int64_t)gridDim.z * a.nseg + (int64_t)blockIdx.z * nS + sblk()) * 12 * NL + x;
-        su[(int64_t)(3 * pl) * NL] = r0;
-        su[(int64_t)(3 * pl + 1) * NL] = r1;
-        su[(int64_t)(3 * pl + 2) * NL] = r2;
-        su[(int64_t)(6 + 3 * pl) * NL] = t0;
-        su[(int64_t)(7 + 3 * pl) * NL] = t1;
-        su[(int64_t)(8 + 3 * pl) * NL] = t2;
+        if (!bwd) {
+#pragma unroll
+            for (int k = 0; k < kSY; ++k) {
+                if (k >= K) break;
+                float* d = sb + (int64_t)k * 12 * NL;
+                d[(int64_t)(3 * pl) * NL] = sl[k][0];
+                d[(int64_t)(3 * pl + 1) * NL] = sl[k][1];
+                d[(int64_t)(3 * pl + 2) * NL] = sl[k][2];
+            }
+            su[(int64_t)(3 * pl) * NL] = r0;
+            su[(int64_t)(3 * pl + 1) * NL] = r1;
+            su[(int64_t)(3 * pl + 2) * NL] = r2;
+        } else {
+            float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+#pragma unroll
+            for (int k = kSY - 1; k >= 0; --k) {
+                if (k >= K) continue;
+                float* d = sb + (int64_t)k * 12 * NL;
+                d[(int64_t)(6 + 3 * pl) * NL] = t0;
+                d[(int64_t)(7 + 3 * pl) * NL] = t1;
+                d[(int64_t)(8 + 3 * pl) * NL] = t2;
+                const float* p = sm + (k * 12 + 6 + 3 * pl) * kTX + threadIdx.x;
+                const int lt = sblk() * kSY + k == a.nseg - 1;
+                const float* Q = q.Q[lt];
+                const float* M = q.Mb[lt];
+                const float c0 = fmaf(M[0], sl[k][0], fmaf(M[1], sl[k][1], fmaf(M[2], sl[k][2], p[0])));
+                const float c1 = fmaf(M[3], sl[k][0], fmaf(M[4], sl[k][1], fmaf(M[5], sl[k][2], p[kTX])));
+                const float c2 = fmaf(M[6], sl[k][0], fmaf(M[7], sl[k][1], fmaf(M[8], sl[k][2], p[2 * kTX])));
+                const float n0_ = fmaf(Q[0], t0, c0);
+                const float n1_ = fmaf(Q[1], t1, fmaf(-Q[2], t2, c1));
+                const float n2_ = fmaf(Q[1], t2, fmaf(Q[2], t1, c2));
+                t0 = n0_; t1 = n1_; t2 = n2_;
+            }
+            su[(int64_t)(6 + 3 * pl) * NL] = t0;
+            su[(int64_t)(7 + 3 * pl) * NL] = t1;
+            su[(int64_t)(8 + 3 * pl) * NL] = t2;
+        }
     }
     // arrival: the last CTA of this line block runs its carries
     // (the barrier orders the CTA's state writes before thread 0's cumulative
@@ -785,9 +846,12 @@ cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream
     // (pass 1's carry scans stage their states in chunks of what the tile
     // leaves: reserving room for a single chunk cost more in occupancy)
     constexpr size_t smem = Tile<ROWS, CPLX>::smem;
+    // column stages stream pass 1 (no tile): tables, then summaries / carry staging
+    constexpr bool kStream = !ROWS;
+    constexpr size_t smem1 = kStream ? 12 * 1024 : smem;
     static bool attr = false;  // launches are serialised by the engine lock
     if (!attr) {
-        cudaFuncSetAttribute(iir32_sum<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(iir32_sum<ROWS, CPLX, kStream>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
         cudaFuncSetAttribute(iir32_fin<ROWS, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
@@ -797,7 +861,7 @@ cudaError_t launch_passes(const IirArgs<float>& a, const Iir32Par& q, cudaStream
     // once at allocation; every launch leaves them zero again (the last CTA of a block
     // resets its counter), so no memset launch per stage
     int* counters = a.counters;
-    iir32_sum<ROWS, CPLX><<<grid, block, smem, s>>>(a, q, counters);
+    iir32_sum<ROWS, CPLX, kStream><<<grid, block, smem1, s>>>(a, q, counters);
     iir32_fin<ROWS, CPLX><<<grid, block, smem, s>>>(a, q);
     return cudaGetLastError();
 }
