@@ -108,7 +108,7 @@ def scaling_of(config):
 def config_dict(args, cfg, world):
     """The `config` object of the JSON line -- identical for both arms."""
     par = {2: "image per rank (weak)", 3: "images sharded", 4: "conjugate u-pairs sharded",
-           5: "(frequency, theta/pi-theta) units LPT-sharded"}[args.config]
+           5: "(frequency, theta/pi-theta) units partitioned (partition_units)"}[args.config]
     return {"workload": cfg["workload"], "smoother": args.smoother,
             "l2": "256 MiB flush between timed steps (inputs and outputs also exceed L2)" if args.config in (4, 5)
             else "256 MiB flush between timed steps",
