@@ -1,0 +1,384 @@
+// K2u: fp32-build column stage of the Gabor bank on the 5th-generation tensor
+// cores (tcgen05, TMEM accumulators, TMA), split-fp16 for fp32 accuracy.
+//
+// Reference semantics: vertical_stage + vertical_stage_conjugate
+// (gabor.py:135-169, bank.py:68-74) after the row stage.  With the modulation
+// folded into the taps a column job is
+//     A(y) = sum_t ka[t] J[clamp(y+t)],  B(y) = sum_t kb[t] J[clamp(y+t)],
+//     F_theta = A - iB,  F_{pi-theta} = conj(A + iB)
+// for t in [-h, h].  Over a tile of 64 output rows this is a banded Toeplitz
+// product: D (128 x 128) = Wt (128 x K) . Jt (K x 128) with
+//   * M rows 2r / 2r+1 = the ka / kb taps of output row r placed at
+//     K column k = r + jpad + t (zero outside the band),
+//   * K = 64 + 2 jpad input rows (jpad = h rounded up to 16), read from a J
+//     plane whose rows are replicate-padded by jpad on both ends (the row
+//     kernel writes the pad rows), so clamp() costs nothing,
+//   * N = 128 halfs of each J row = 64 complex columns (re / im interleaved:
+//     the real weights multiply both components independently).
+// Precision: every operand is split x = hi + lo in fp16 (round to nearest;
+// |x - hi - lo| <= 2^-24 |x|), and D = Wh Jh + Wh Jl + Wl Jh accumulates in
+// fp32 in tensor memory -- the dropped Wl Jl term is 2^-22 relative.  J is
+// scaled by 2^e per image (e from max|f|, so |J 2^e| < 2^14 < fp16 max) and
+// the taps by 2^s per job; the epilogue multiplies by 2^-(e+s) (exact).
+// Measured (tools/probes/umma_probe.cu): max|err|/max|ref| 1.9e-6 at K = 256
+// where a plain fp32 FMA chain gives 0.9e-6; MMA rate 2.0 PFLOP/s per GPU.
+//
+// Persistent warp-specialised CTA (one per SM, 512 TMEM columns):
+//   warp 4   TMA producer: 16-row groups of the hi and lo J planes (4 boxes of
+//            64 halfs x 16 rows, 128-byte swizzle) into a ring of slots;
+//   warp 5   TMEM allocator + MMA issuer: per tile K/16 steps x 3 MMAs
+//            (M = 128, N = 128, K = 16, A from TMEM, B = the ring slot);
+//            consecutive tiles of a column strip share their K rows, so each
+//            J row is fetched once per strip (ring slots are released 4 at a
+//            time as the tile window slides by 64 rows);
+//   warps 0-3 epilogue: TMEM -> registers (lane m = M row m), partner lane
+//            exchange (ka row / kb row of the same output row), combine,
+//            scale, streaming 16-byte stores of F_theta (even lanes) and
+//            conj(A + iB) (odd lanes); they also (re)build the tap matrix in
+//            TMEM (tcgen05.st) when the job changes.
+// Accumulators are double-buffered (2 x 128 columns), taps hi / lo use the
+// remaining K columns.  Work unit = (job, image, row chunk, 64-column strip),
+// strips fastest.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "kernels.h"
+#include "umma.cuh"
+
+namespace fgb {
+
+namespace {
+
+constexpr int kTile = 64;          // output rows per tile
+constexpr int kSlotBytes = 8192;   // (hi, lo) x 2 blocks x 16 rows x 128 B
+constexpr int kThreads = 192;      // warps 0-3 epilogue, 4 TMA, 5 MMA
+constexpr uint32_t kAcc = 128;     // TMEM columns per accumulator
+constexpr int kMaxSlots = 24;
+constexpr int kStgPitch = 36;      // floats per staged row: 128 B of outputs + 16 B (conflict-free 16-B access)
+constexpr int kStgBytes = 4 * 32 * kStgPitch * 4;  // 4 epilogue warps x 32 rows
+
+// 2^e as a float for |e| <= 126 (exact)
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
+
+__device__ __forceinline__ void unit_decode(const ColUArgs& a, int u, int& job, int& b, int& chunk, int& strip) {
+    strip = u % a.nstrips;
+    int r = u / a.nstrips;
+    chunk = r % a.nchunks;
+    r /= a.nchunks;
+    b = r % a.batch;
+    job = r / a.batch;
+}
+
+__device__ __forceinline__ void st_cs4(float2* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    col_umma_kernel(const __grid_constant__ CUtensorMap jmap, const __grid_constant__ ColUArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t full[kMaxSlots], empty[kMaxSlots], tfull[2], tempty[2], aready;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ns = a.ns, K = a.K, ksteps = a.K / 16;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tfull[1], 1);
+        mbar_init(&tempty[0], 128);
+        mbar_init(&tempty[1], 128);
+        mbar_init(&aready, 128);
+    }
+    if (warp == 5) umma::tmem_alloc(&tmem_base, 512);
+    if (warp == 4 && lane == 0) umma::tma_prefetch_desc(&jmap);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tb = tmem_base;
+    const uint32_t a_hi = tb + 2 * kAcc, a_lo = a_hi + (uint32_t)(K / 2);
+    const int nunits = a.njobs * a.batch * a.nchunks * a.nstrips;
+    const int chunk_rows = a.ch_tiles * kTile;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                int job, b, chunk, strip;
+                unit_decode(a, u, job, b, chunk, strip);
+                const int y0 = chunk * chunk_rows;
+                const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
+                const int G = 4 * nt + ksteps - 4;
+                const int plane = (int)(2 * (((int64_t)b * a.ws_img_c + a.jobs[job].src_off) / a.hpw));
+                const int c0 = strip * 128;
+                for (int q = 0; q < G; ++q, ++g) {
+                    const uint32_t slot = g % (uint32_t)ns, round = g / (uint32_t)ns;
+                    mbar_wait(&empty[slot], (round & 1u) ^ 1u);
+                    uint8_t* sp = ring + slot * kSlotBytes;
+                    mbar_arrive_expect_tx(&full[slot], kSlotBytes);
+                    const int rr = y0 + a.jbuf - a.jpad + 16 * q;  // buffer row (input row + jbuf)
+                    umma::tma_load_3d(sp, &jmap, c0, rr, plane, &full[slot]);
+                    umma::tma_load_3d(sp + 2048, &jmap, c0 + 64, rr, plane, &full[slot]);
+                    umma::tma_load_3d(sp + 4096, &jmap, c0, rr, plane + 1, &full[slot]);
+                    umma::tma_load_3d(sp + 6144, &jmap, c0 + 64, rr, plane + 1, &full[slot]);
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t idesc = umma::idesc_f16_f32(128, 128, false, true);
+            uint32_t g = 0, t = 0, nreload = 0;
+            int cur = -1;
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                int job, b, chunk, strip;
+                unit_decode(a, u, job, b, chunk, strip);
+                const int y0 = chunk * chunk_rows;
+                const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
+                const int G = 4 * nt + ksteps - 4;
+                if (job != cur) {
+                    mbar_wait(&aready, nreload & 1u);
+                    ++nreload;
+                    cur = job;
+                    umma::fence_after();
+                }
+                for (int i = 0; i < nt; ++i, ++t) {
+                    const uint32_t buf = t & 1u;
+                    mbar_wait(&tempty[buf], ((t >> 1) & 1u) ^ 1u);
+                    umma::fence_after();
+                    const uint32_t d = tb + buf * kAcc;
+                    for (int kk = 0; kk < ksteps; ++kk) {
+                        const uint32_t gg = g + 4 * i + kk;
+                        const uint32_t slot = gg % (uint32_t)ns;
+                        mbar_wait(&full[slot], (gg / (uint32_t)ns) & 1u);
+                        umma::fence_after();
+                        const uint32_t sb = smem_u32(ring + slot * kSlotBytes);
+                        const uint64_t bh = umma::smem_desc(sb, 2048, 1024, umma::kLayoutSw128);
+                        const uint64_t bl = umma::smem_desc(sb + 4096, 2048, 1024, umma::kLayoutSw128);
+                        umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
+                        umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
+                        umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                    }
+                    umma::mma_commit(&tfull[buf]);
+                    // the next tile's window starts 4 groups later: release the groups it no longer needs
+                    const int rel_end = (i == nt - 1) ? G : 4 * i + 4;
+                    for (int q = 4 * i; q < rel_end; ++q) umma::mma_commit(&empty[(g + q) % (uint32_t)ns]);
+                }
+                g += G;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue (warps 0-3: TMEM lanes 32 w .. 32 w + 31) ----------------
+        const int m = threadIdx.x;
+        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        const int r = m >> 1, odd = m & 1;
+        float* stg = reinterpret_cast<float*>(ring + ns * kSlotBytes) + warp * 32 * kStgPitch;  // [32][kStgPitch]
+        int cur = -1;
+        uint32_t t = 0;
+        int wexp = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            int job, b, chunk, strip;
+            unit_decode(a, u, job, b, chunk, strip);
+            const ColJob<float>& jb = a.jobs[job];
+            if (job != cur) {
+                // tap matrix row m: K column k holds (odd ? kb : ka)[t], t = k - jpad - r
+                const float2* w = a.weights + jb.wofs;
+                wexp = jb.wexp;
+                const float wsc = pow2f(wexp);
+                for (int c = 0; c < K / 2; c += 16) {
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float v[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int tt = 2 * (c + i) + e - a.jpad - r;
+                            float x = 0.f;
+                            if (tt >= -a.h && tt <= a.h) {
+                                const float2 kk = w[tt + a.h];
+                                x = (odd ? kk.y : kk.x) * wsc;
+                            }
+                            v[e] = x;
+                        }
+                        umma::split_f16x2(v[0], v[1], hi[i], lo[i]);
+                    }
+                    umma::tmem_st16(a_hi + lane_addr + c, hi);
+                    umma::tmem_st16(a_lo + lane_addr + c, lo);
+                }
+                umma::tmem_st_wait();
+                umma::fence_before();
+                umma::mbar_arrive(&aready);
+                cur = job;
+            }
+            const float inv = pow2f(-(jscale_exp(a.maxbits[b]) + wexp));
+            const int nout = jb.nout;
+            float2* dst0 = a.dst_base + jb.dst_off[0] + (int64_t)b * a.dst_bstride;
+            float2* dst1 = a.dst_base + (nout > 1 ? jb.dst_off[1] : jb.dst_off[0]) + (int64_t)b * a.dst_bstride;
+            const int y0 = chunk * chunk_rows;
+            const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
+            const int x0 = strip * 64;
+            for (int i = 0; i < nt; ++i, ++t) {
+                const uint32_t buf = t & 1u;
+                mbar_wait(&tfull[buf], (t >> 1) & 1u);
+                umma::fence_after();
+                const int ybase = y0 + i * kTile + 16 * warp;  // output row of this warp's M rows 0 / 1
+#pragma unroll 1
+                for (int qq = 0; qq < 4; ++qq) {  // 16 complex columns per pass
+                    float v[32], p[32];
+                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + 32 * qq, *reinterpret_cast<float(*)[16]>(v));
+                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + 32 * qq + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+                    umma::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) p[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
+                    // even lane: X = A - iB (A own, B partner); odd lane: conj(A + iB) (A partner, B own)
+                    float4* srow = reinterpret_cast<float4*>(stg + lane * kStgPitch);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float o[4];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int c = 4 * j + 2 * e;
+                            if (!odd) {
+                                o[2 * e] = (v[c] + p[c + 1]) * inv;
+                                o[2 * e + 1] = (v[c + 1] - p[c]) * inv;
+                            } else {
+                                o[2 * e] = (p[c] - v[c + 1]) * inv;
+                                o[2 * e + 1] = -(p[c + 1] + v[c]) * inv;
+                            }
+                        }
+                        srow[j] = make_float4(o[0], o[1], o[2], o[3]);
+                    }
+                    __syncwarp();
+                    // coalesced write-out: instruction k covers staged rows 4k .. 4k+3, 128 B each
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int rho = 4 * k + (lane >> 3), seg = lane & 7;
+                        const float4 val = *reinterpret_cast<const float4*>(stg + rho * kStgPitch + 4 * seg);
+                        const int orow = ybase + (rho >> 1);
+                        const int x = x0 + 16 * qq + 2 * seg;
+                        if (orow < a.H && x < a.W && ((rho & 1) == 0 || nout > 1))
+                            st_cs4(((rho & 1) ? dst1 : dst0) + (int64_t)orow * a.W + x, val.x, val.y, val.z, val.w);
+                    }
+                    __syncwarp();
+                }
+                umma::fence_before();
+                umma::mbar_arrive(&tempty[buf]);
+            }
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 5) umma::tmem_dealloc(tb, 512);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (EncodeFn)p;
+    }();
+    return fn;
+}
+
+}  // namespace
+
+int col_umma_jpad(int h) { return (h + 15) / 16 * 16; }
+
+bool col_umma_supported(int h, int W) {
+    const int K = kTile + 2 * col_umma_jpad(h);
+    return h >= 1 && K <= 256 && W % 4 == 0 && W >= 64 && encode_fn() != nullptr;
+}
+
+size_t col_umma_smem(int h) {
+    const int K = kTile + 2 * col_umma_jpad(h);
+    const int ns = std::min(kMaxSlots, K / 16 + 8);
+    // >= 116 KB so that two of these CTAs (512 TMEM columns each) never share an SM
+    return std::max<size_t>((size_t)ns * kSlotBytes + kStgBytes + 1024, 116 * 1024);
+}
+
+cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cudaStream_t s) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    a.jpad = col_umma_jpad(a.h);
+    a.K = kTile + 2 * a.jpad;
+    a.ns = std::min(kMaxSlots, a.K / 16 + 8);
+    if (a.jpad > a.jbuf || a.hpw != (a.H + 2 * (int64_t)a.jbuf) * a.W) {
+        std::fprintf(stderr, "col_umma: J slot layout mismatch (jpad %d jbuf %d hpw %lld)\n", a.jpad, a.jbuf,
+                     (long long)a.hpw);
+        return cudaErrorInvalidValue;
+    }
+    const int64_t Hp = a.H + 2 * (int64_t)a.jbuf;
+    // J planes: [nplanes][Hp][W] of half2 (hi plane, lo plane per job slot)
+    const int64_t plane_bytes = a.hpw * 4;
+    const int64_t nplanes = ws_bytes / plane_bytes;
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)2 * a.W, (cuuint64_t)Hp, (cuuint64_t)nplanes};
+    cuuint64_t strides[2] = {(cuuint64_t)a.W * 4, (cuuint64_t)plane_bytes};
+    cuuint32_t box[3] = {64, 16, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS) {
+        std::fprintf(stderr, "col_umma: tensor map encode failed (W %d Hp %lld planes %lld)\n", a.W, (long long)Hp,
+                     (long long)nplanes);
+        return cudaErrorInvalidValue;
+    }
+    // work units: strips x row chunks x images x jobs; enough units for an even last wave
+    a.nstrips = (a.W + 63) / 64;
+    const int ntiles = (a.H + kTile - 1) / kTile;
+    const int64_t base = (int64_t)a.nstrips * a.batch * a.njobs;
+    int nch = (int)std::min<int64_t>(std::max<int64_t>(1, (20LL * sms + base - 1) / base), std::max(1, ntiles / 8));
+    a.ch_tiles = (ntiles + nch - 1) / nch;
+    a.nchunks = (ntiles + a.ch_tiles - 1) / a.ch_tiles;
+    const int64_t units = base * a.nchunks;
+    const int grid = (int)std::min<int64_t>(units, sms);
+    const size_t smem = col_umma_smem(a.h);
+    static bool attr = false;
+    if (!attr) {
+        // the largest ring (+ alignment slack); static shared memory comes on top of it
+        cudaError_t e = cudaFuncSetAttribute(col_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kMaxSlots * kSlotBytes + kStgBytes + 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    col_umma_kernel<<<grid, kThreads, smem, s>>>(map, a);
+    return cudaGetLastError();
+}
+
+// ---- per-image max |f| (the J scale exponent) ----------------------------
+// grid (row blocks, batch); threads stride the columns of their rows
+__global__ void absmax_kernel(const float* __restrict__ img, int64_t pitch, int64_t bstride, int H, int W,
+                              unsigned* __restrict__ out) {
+    const float* base = img + (int64_t)blockIdx.y * bstride;
+    unsigned mx = 0;
+    for (int y = blockIdx.x; y < H; y += gridDim.x) {
+        const float* row = base + (int64_t)y * pitch;
+        for (int x = threadIdx.x; x < W; x += blockDim.x) mx = max(mx, __float_as_uint(fabsf(row[x])));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out + blockIdx.y, mx);
+}
+
+cudaError_t launch_absmax(const float* img, int64_t pitch, int64_t bstride, int H, int W, int batch, unsigned* out,
+                          int sms, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned) * batch, s);
+    if (e != cudaSuccess) return e;
+    const int per = std::max(1, std::min(H, (4 * sms + batch - 1) / batch));
+    absmax_kernel<<<dim3(per, batch), 256, 0, s>>>(img, pitch, bstride, H, W, out);
+    return cudaGetLastError();
+}
+
+}  // namespace fgb

@@ -86,7 +86,7 @@ template <typename T> struct ColJob {
     int32_t mode;            // epilogue: 0 generic, 1 Gabor X only, 2 Gabor X + conj(Y) (no phase)
     int32_t realj;           // fp32 kernel, mode 1: J is real to ~1e-12 (theta = pi/2: the row phase step
                              // omega cos(theta) ~ 1e-17), so A and B read only Re J (half the FMAs)
-    int32_t pad_;
+    int32_t wexp;            // tensor-core column pass: taps scaled by 2^wexp (|scaled| < 2^10)
 };
 
 // Row job group: up to kMaxND jobs sharing one input row and one symmetric

@@ -296,7 +296,7 @@ struct Ref {
     int64_t off = 0;  // elements of the referenced type (T for real, C for complex)
 };
 
-enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF, ST_BANKF };
+enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF, ST_BANKF, ST_COLU };
 
 template <typename T> struct Step {
     int kind = 0;
@@ -310,6 +310,7 @@ template <typename T> struct Step {
     // ST_ROW
     RowGroup<T> rg{};
     int hp = 0;
+    int j16 = 0;             // fp32: split-fp16 J planes for the tensor-core column pass (ST_COLU)
     // ST_COL
     int job0 = 0, njobs = 0, t0 = 0, nt = 0, zero_bnd = 0, has_b = 1;
     std::vector<cx_t<T>> pw;  // ST_COL: tap pairs packed in job order (kernel-parameter path)
@@ -354,6 +355,8 @@ template <typename T> struct Plan : PlanBase {
     int64_t state_img_d = 0;      // doubles per image (IIR segment states)
     int64_t out_img_c = 0;        // complex elements per output image
     int H = 0, W = 0;
+    int jbuf = 0;                 // > 0: J slots are split-fp16 planes with jbuf replicate rows (ST_COLU)
+    int64_t hpw = 0;              // (H + 2 jbuf) * W: complex elements per J slot (= u32 per fp16 plane)
     int chunk = 1;
     int nlanes = 1;               // concurrent stream lanes used by the steps
 
@@ -674,16 +677,36 @@ struct DirectJob {
     int64_t out_mirror;   // mirrored slot or -1
 };
 
+// Fused row+column kernel (J kept in shared memory) for half-widths up to
+// 6 and <= 5 direct orientations per launch (balanced groups): config 2's
+// sigma = 2 frequency 30 us instead of 42 us for the two launches (step
+// +4.5%); at h = 12 the halo and shared-memory footprint make it a wash
+// (measured).  FGB_FUSED_BANK=<max h> overrides (0 disables).
+static bool fused_bank_used(int h, int nj, int H, int W) {
+    static const int fused_max_h = std::getenv("FGB_FUSED_BANK") ? std::atoi(std::getenv("FGB_FUSED_BANK")) : 6;
+    const int ng = (nj + 4) / 5;
+    return h <= fused_max_h && (int64_t)H * W >= 4096 && bank_fused_ok(h, (nj + ng - 1) / ng);
+}
+
+// Tensor-core column pass (col_umma.cu) for an fp32 FIR bank frequency of half-width h
+// (FGB_COL_FFMA=1 keeps the FFMA column kernel; FGB_UMMA_MIN_H sets the smallest h).
+static bool umma_freq_used(int h, int nj, int H, int W) {
+    static const bool off = std::getenv("FGB_COL_FFMA") != nullptr;
+    static const int min_h = std::getenv("FGB_UMMA_MIN_H") ? std::atoi(std::getenv("FGB_UMMA_MIN_H")) : 7;
+    return !off && h >= min_h && H >= 16 && col_umma_supported(h, W) && !fused_bank_used(h, nj, H, W);
+}
+
 // One frequency worth of Gabor work: row stage for `jobs`, column stage with
 // direct / mirrored outputs.  J planes live in ws at [ws_j0 + j*H*W].
 template <typename T>
 static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double sigma, const std::vector<DirectJob>& jobs,
                                 int H, int W, int64_t ws_j0, int64_t ws_aux, Ref img, Ref out, bool row_only,
-                                bool col_only, int64_t* ws_need) {
+                                bool col_only, int64_t* ws_need, int64_t jslot = -1) {
     const int64_t HW = (int64_t)H * W;
+    if (jslot < 0) jslot = HW;  // complex elements per J slot (larger for split-fp16 padded slots)
     const int nj = (int)jobs.size();
     if (nj == 0) return FGB_OK;
-    int64_t need = ws_j0 + (row_only || col_only ? 0 : (int64_t)nj * HW);
+    int64_t need = ws_j0 + (row_only || col_only ? 0 : (int64_t)nj * jslot);
     if (sm.kind == FGB_SMOOTH_FIR || sm.kind == FGB_SMOOTH_BOX) {
         std::vector<double> w;
         int h = 0, t0 = 0;
@@ -698,18 +721,11 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
         const int nt = 2 * h + 1;
         // ---- fused small-sigma path: J stays in shared memory ----
         if constexpr (std::is_same<T, float>::value) {
-            // Fused row+column kernel (J kept in shared memory) for half-widths up
-            // to 6 and <= 5 direct orientations: config 2's sigma = 2 frequency
-            // 30 us instead of 42 us for the two launches (step +4.5%); at h = 12
-            // the halo and shared-memory footprint make it a wash (measured).
-            // FGB_FUSED_BANK=<max h> overrides (0 disables).
-            static const int fused_max_h = std::getenv("FGB_FUSED_BANK") ? std::atoi(std::getenv("FGB_FUSED_BANK")) : 6;
             // More than 5 directs (config 5: 9 per frequency) run as balanced groups of <= 5, one
             // fused launch each: config 5's sigma = 2 frequency 2.5 ms instead of 3.4 ms for the
             // row + column launches (profiles/r02/unit_costs_c5.json).
             const int ng = (nj + 4) / 5;
-            if (!box && !row_only && !col_only && h <= fused_max_h && (int64_t)H * W >= 4096 &&
-                bank_fused_ok(h, (nj + ng - 1) / ng)) {
+            if (!box && !row_only && !col_only && fused_bank_used(h, nj, H, W)) {
                 for (int gi = 0; gi < ng; ++gi) {
                     const int g0 = gi * nj / ng, g1 = (gi + 1) * nj / ng, gn = g1 - g0;
                     Step<T> st;
@@ -759,10 +775,13 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                     st.bytes = (double)H * W * sizeof(T) + (double)counted * H * W * sizeof(cx_t<T>);
                     b.push(st);
                 }
-                *ws_need = std::max(*ws_need, need - (int64_t)nj * HW);
+                *ws_need = std::max(*ws_need, need - (int64_t)nj * jslot);
                 return FGB_OK;
             }
         }
+        // tensor-core column pass: the plan's J slots are split-fp16 planes (Plan::jbuf > 0)
+        const bool umma = std::is_same<T, float>::value && !box && !row_only && !col_only && b.p.jbuf > 0 &&
+                          umma_freq_used(h, nj, H, W) && col_umma_jpad(h) <= b.p.jbuf;
         // ---- row stage ----
         if (!col_only) {
             if (!box) {
@@ -777,9 +796,10 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                     for (int j = g0; j < g1; ++j) {
                         fr.push_back(jobs[j].wc);
                         ph.push_back(cd(1.0, 0.0));
-                        dst.push_back(row_only ? jobs[j].out_direct : ws_j0 + (int64_t)j * HW);
+                        dst.push_back(row_only ? jobs[j].out_direct : ws_j0 + (int64_t)j * jslot);
                     }
                     b.row_group(w, h, fr, +1.0, ph, dst, img, row_only ? out : R(SEL_WS, 0), H, W, 4.0 * h + 1);
+                    if (umma) b.p.steps.back().j16 = 1;
                 }
             } else {
                 // zero-padded box: transpose -> column kernel -> transpose back
@@ -794,7 +814,7 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 b.col_step(cj, R(SEL_WS, t_img), R(SEL_WS, 0), W, H, t0, nt, 1, 1, 2.0 * h, nj, true);
                 for (int j = 0; j < nj; ++j)
                     b.tr(ST_TR_CC, R(SEL_WS, t_j + (int64_t)j * HW),
-                         row_only ? R(out.sel, jobs[j].out_direct) : R(SEL_WS, ws_j0 + (int64_t)j * HW), W, H);
+                         row_only ? R(out.sel, jobs[j].out_direct) : R(SEL_WS, ws_j0 + (int64_t)j * jslot), W, H);
             }
         }
         // ---- column stage ----
@@ -805,7 +825,16 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 std::vector<typename Builder<T>::Out> outs;
                 if (jobs[j].out_direct >= 0) outs.push_back({jobs[j].out_direct, 0, 0, cd(1, 0)});
                 if (jobs[j].out_mirror >= 0) outs.push_back({jobs[j].out_mirror, 1, 1, cd(1, 0)});
-                ColJob<T> job = b.col_job(col_only ? 0 : ws_j0 + (int64_t)j * HW, wo, outs, jobs[j].ws != 0.0);
+                ColJob<T> job = b.col_job(col_only ? 0 : ws_j0 + (int64_t)j * jslot, wo, outs, jobs[j].ws != 0.0);
+                if (umma) {
+                    // taps scaled by 2^wexp so |scaled| < 2^10 (fp16 hi / lo split without underflow)
+                    double mx = 0.0;
+                    for (int q = 0; q < nt; ++q)
+                        mx = std::max(mx, std::max(std::fabs((double)b.p.wcol[wo + q].x), std::fabs((double)b.p.wcol[wo + q].y)));
+                    int ex = 0;
+                    if (mx > 0.0) std::frexp(mx, &ex);
+                    job.wexp = 10 - ex;
+                }
                 // theta = pi/2: the row stage's phase step omega cos(theta) ~ 1e-17 leaves Im J at
                 // ~1e-12 of |J| or less, so the fp32 column kernel reads Re J only (half the FMAs)
                 if (sizeof(T) == 4 && !col_only && !box && job.mode == 1 && job.has_b &&
@@ -820,6 +849,12 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
             const double sfl = box ? 2.0 * h : 4.0 * h + 1;
             cj_b.insert(cj_b.end(), cj_nob.begin(), cj_nob.end());
             b.col_step(cj_b, src, out, H, W, t0, nt, box ? 1 : 0, 1, sfl);
+            if (umma) {
+                Step<T>& cs = b.p.steps.back();
+                cs.kind = ST_COLU;
+                cs.name = "col_umma";
+                cs.h = h;
+            }
         }
     } else {
         // ---- RecursiveIIR ----
@@ -835,7 +870,7 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                 q.src_off = 0;
                 q.tabm_off = b.table(jobs[j].wc, -P, W + 2 * P);
                 q.tabr_off = q.tabm_off + P;
-                q.dst_off[0] = row_only ? jobs[j].out_direct : ws_j0 + (int64_t)j * HW;
+                q.dst_off[0] = row_only ? jobs[j].out_direct : ws_j0 + (int64_t)j * jslot;
                 q.pair[0] = 0;
                 q.conj[0] = 0;
                 q.nout = 1;
@@ -850,7 +885,7 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
             std::vector<IirJob<T>> ij;
             for (int j = 0; j < nj; ++j) {
                 IirJob<T> q{};
-                q.src_off = col_only ? 0 : ws_j0 + (int64_t)j * HW;
+                q.src_off = col_only ? 0 : ws_j0 + (int64_t)j * jslot;
                 q.tabm_off = b.table(jobs[j].ws, -P, H + 2 * P);
                 q.tabr_off = q.tabm_off + P;
                 q.nout = 0;
@@ -956,7 +991,18 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
     const int max_lanes = le ? std::max(1, std::atoi(le)) : 4;
     const int NL = std::max(1, std::min(max_lanes, nfreq_used));
     const bool plain_fir = d.smoother.kind == FGB_SMOOTH_FIR;
-    const int64_t lane_stride = plain_fir ? max_nj * HW : (2 * max_nj + 1) * HW;
+    // fp32 FIR banks: frequencies whose column pass runs on the tensor cores get split-fp16 J
+    // slots with jbuf replicate rows above and below (one slot size for every lane)
+    if (std::is_same<T, float>::value && plain_fir) {
+        for (int i = 0; i < d.n_freq; ++i) {
+            if (per_f[i].empty()) continue;
+            const int h = std::max(1, (int)std::ceil(d.smoother.radius * d.sigmas[i]));
+            if (umma_freq_used(h, (int)per_f[i].size(), H, W)) p.jbuf = std::max(p.jbuf, col_umma_jpad(h));
+        }
+    }
+    const int64_t jslot = p.jbuf > 0 ? (int64_t)(H + 2 * p.jbuf) * W : HW;
+    p.hpw = jslot;
+    const int64_t lane_stride = plain_fir ? max_nj * jslot : (2 * max_nj + 1) * HW;
     int64_t need = 0;
     int li = 0;
     // emit the heaviest frequency first: the longest lane chain starts first and the
@@ -973,7 +1019,7 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
         b.lane = li % NL;
         const int64_t j0 = b.lane * lane_stride;
         FGB_TRY(build_gabor_freq<T>(b, d.smoother, d.sigmas[i], per_f[i], H, W, j0, j0 + max_nj * HW, R(SEL_IMG, 0),
-                                    R(SEL_OUT, 0), false, false, &need));
+                                    R(SEL_OUT, 0), false, false, &need, plain_fir ? jslot : HW));
         ++li;
     }
     p.nlanes = NL;
@@ -1372,6 +1418,8 @@ struct Ctx {
     bool ws_pending = false;
     std::map<std::string, std::unique_ptr<DevBuf>> line_taps;  // fgb_smooth_lines tap tables (immutable)
     DevBuf ser_scratch;                                         // fgb_ser_sums partials
+    DevBuf maxbits;                                             // max|f| bits per image (split-fp16 J scale)
+    int sms = 0;                                                // SM count (persistent grids)
     DevBuf iir_cnt;                                             // iir32 arrival counters, zero between launches
     size_t iir_cnt_zeroed = 0;                                  // bytes of iir_cnt known to be zero
 };
@@ -1461,6 +1509,14 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     }
     if (!cx.fork_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.fork_ev, cudaEventDisableTiming));
     FGB_TRY(ws_acquire(cx, s));
+    if (p.jbuf > 0) {
+        FGB_TRY(cx.maxbits.ensure(sizeof(unsigned) * (size_t)chunk));
+        if (cx.sms == 0) {
+            int dev = 0;
+            FGB_CUDA(cudaGetDevice(&dev));
+            FGB_CUDA(cudaDeviceGetAttribute(&cx.sms, cudaDevAttrMultiProcessorCount, dev));
+        }
+    }
     // iir32 arrival counters (shared like the workspace, so after ws_acquire): one int per
     // 32-line block, job and image of a chunk, per lane; zeroed once when (re)allocated
     size_t cnt_lane = 0;
@@ -1479,11 +1535,17 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     const int64_t img_bs = (batch > 1) ? im.batch_stride : (int64_t)im.height * im.pitch;
     for (int b0 = 0; b0 < batch; b0 += chunk) {
         const int nb = std::min(chunk, batch - b0);
+        const T* imgb = (const T*)img + (size_t)b0 * img_bs;
+        if constexpr (std::is_same<T, float>::value) {
+            if (p.jbuf > 0) {  // split-fp16 J scale per image, before the lanes fork
+                ++g_launches;
+                FGB_CUDA(launch_absmax(imgb, im.pitch, img_bs, p.H, p.W, nb, (unsigned*)cx.maxbits.p, cx.sms, s));
+            }
+        }
         if (nl > 1) {
             FGB_CUDA(cudaEventRecord(cx.fork_ev, s));
             for (int l = 1; l < nl; ++l) FGB_CUDA(cudaStreamWaitEvent(lane_s[l], cx.fork_ev, 0));
         }
-        const T* imgb = (const T*)img + (size_t)b0 * img_bs;
         C* imgcb = (C*)img + (size_t)b0 * img_bs;  // complex inputs: strides in complex elements
         C* outb = (C*)out + (size_t)b0 * p.out_img_c;
         auto baseC = [&](const Ref& r) -> C* {
@@ -1542,7 +1604,31 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.W = st.W;
                     a.hp = st.hp;
                     a.batch = nb;
+                    a.j16 = st.j16;
+                    a.jpad = p.jbuf;
+                    a.j16_plane = p.hpw;
+                    a.maxbits = (const unsigned*)cx.maxbits.p;
                     FGB_CUDA(launch_row_sym<T>(a, st.rg, knobs().row_smem_taps ? nullptr : p.wrow.data() + st.rg.wofs, s));
+                    break;
+                }
+                case ST_COLU: {
+                    if constexpr (std::is_same<T, float>::value) {
+                        ColUArgs a{};
+                        a.jobs = p.d_cjobs() + st.job0;
+                        a.weights = p.d_wcol();
+                        a.dst_base = baseC(st.dst);
+                        a.dst_bstride = bsC(st.dst);
+                        a.maxbits = (const unsigned*)cx.maxbits.p;
+                        a.ws_img_c = p.ws_img_c;
+                        a.hpw = p.hpw;
+                        a.H = st.H;
+                        a.W = st.W;
+                        a.h = st.h;
+                        a.jbuf = p.jbuf;
+                        a.njobs = st.njobs;
+                        a.batch = nb;
+                        FGB_CUDA(launch_col_umma(a, cx.ws.p, ws_img_bytes * chunk, cx.sms, s));
+                    }
                     break;
                 }
                 case ST_COL: {

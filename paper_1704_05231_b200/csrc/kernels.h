@@ -39,6 +39,11 @@ template <typename T> struct RowArgs {
     int H, W;
     int hp;                // half-width padded to a multiple of the row R
     int batch;
+    // fp32 split-fp16 output for the tensor-core column pass (ColUArgs): hi plane at the job's
+    // dst, lo plane j16_plane u32 later, row y at (y + jpad) * W, edge rows replicated into the pads
+    int j16, jpad;
+    int64_t j16_plane;
+    const unsigned* maxbits;
 };
 template <typename T, int CAP> struct RowWParam { T w[CAP > 0 ? CAP : 1]; };
 template <typename T> struct RowWCap {
@@ -79,6 +84,42 @@ template <typename T> struct ColWCap {
 // packed tap pairs (nullptr = read them from `weights` through shared memory).
 template <typename T> cudaError_t launch_col(const ColArgs<T>& a, const cx_t<T>* pw_host, cudaStream_t s);
 template <typename T> size_t col_smem(int nt, int groups);
+
+// ---- K2u: column pass on the tensor cores (col_umma.cu, fp32 build) ------
+// J of the jobs lives in split-fp16 planes: per job slot (hpw complex elements from
+// ws, hpw = (H + 2 jpad) * W) a hi plane then a lo plane of half2 (re, im) rows,
+// jpad replicate rows above and below the image rows (written by the row kernel).
+// J is scaled by 2^jscale_exp(max|f| bits of the image), the taps of a job by 2^wexp.
+struct ColUArgs {
+    const ColJob<float>* jobs;  // modes 1 / 2 only (X; X + conj(Y); no phase)
+    const float2* weights;      // (ka, kb) tap pool, taps -h .. h at jobs[j].wofs
+    float2* dst_base;
+    int64_t dst_bstride;
+    const unsigned* maxbits;    // per image of the chunk
+    int64_t ws_img_c;           // complex elements between images in the workspace
+    int64_t hpw;                // complex elements per J slot = (H + 2 jbuf) * W
+    int H, W, h, njobs, batch;
+    int jbuf;                   // replicate rows above / below the image rows in the J planes
+    int jpad, K, ns;            // set by the launcher (jpad = h rounded up to 16 <= jbuf)
+    int nstrips, nchunks, ch_tiles;
+};
+int col_umma_jpad(int h);
+bool col_umma_supported(int h, int W);
+size_t col_umma_smem(int h);
+// ws / ws_bytes: the J region of the workspace (the tensor map spans it)
+cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cudaStream_t s);
+// max|f| bits per image (memset + atomicMax)
+cudaError_t launch_absmax(const float* img, int64_t pitch, int64_t bstride, int H, int W, int batch, unsigned* out,
+                          int sms, cudaStream_t s);
+// J scale exponent from the bits of max|f|: |f 2^e| < 2^13, so |J 2^e| < 2^13 sum|w| (= 2^13 for the
+// unit-sum Gaussian) stays inside fp16; 0 for an all-zero or non-finite image
+__host__ __device__ inline int jscale_exp(unsigned maxbits) {
+    if (maxbits == 0u || maxbits >= 0x7f800000u) return 0;
+    const int E = (int)(maxbits >> 23);
+    const int x = E == 0 ? -125 : E - 126;  // max|f| < 2^x
+    const int e = 13 - x;
+    return e < -100 ? -100 : (e > 100 ? 100 : e);
+}
 
 // ---- transposes (transpose.cu) -------------------------------------------
 // real [H][pitch] -> complex [W][H] (imag 0); complex [H][W] -> complex [W][H]

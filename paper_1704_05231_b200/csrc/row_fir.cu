@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "umma.cuh"
 
 namespace fgb {
 
@@ -205,6 +206,29 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
     }
 
     const int xb = x0 + R * tx;
+    if constexpr (sizeof(T) == 4) {
+        if (a.j16) {
+            // split-fp16 J for the tensor-core column pass (col_umma.cu): J 2^e = hi + lo per
+            // component, half2 (re, im) per element; the edge rows also fill the jpad pad rows
+            if (xb >= a.W) return;
+            const float sc = ldexpf(1.f, jscale_exp(a.maxbits[b]));
+            const int r0 = y == 0 ? 0 : y + a.jpad;
+            const int r1 = y == a.H - 1 ? a.H + 2 * a.jpad - 1 : y + a.jpad;
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                uint32_t hw[R], lw[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) umma::split_f16x2(acc[k][r].x * sc, acc[k][r].y * sc, hw[r], lw[r]);
+                uint32_t* hp0 = reinterpret_cast<uint32_t*>(a.dst_base + g.dst_off[k] + (size_t)b * a.out_bstride) + xb;
+                for (int rr = r0; rr <= r1; ++rr) {
+                    uint32_t* ph = hp0 + (size_t)rr * a.W;
+                    *reinterpret_cast<uint4*>(ph) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    *reinterpret_cast<uint4*>(ph + a.j16_plane) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                }
+            }
+            return;
+        }
+    }
     const size_t ob = (size_t)b * a.out_bstride + (size_t)y * a.W;
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
