@@ -41,6 +41,7 @@
 // strips fastest.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
@@ -51,12 +52,16 @@ namespace fgb {
 namespace {
 
 constexpr int kTile = 64;          // output rows per tile
-constexpr int kSlotBytes = 8192;   // (hi, lo) x 2 blocks x 16 rows x 128 B
-constexpr int kThreads = 192;      // warps 0-3 epilogue, 4 TMA, 5 MMA
+constexpr int kStageBytes = 32768; // 64 J rows: (hi, lo) x 2 column blocks x 64 rows x 128 B
+constexpr int kStages = 5;         // ring depth (a tile's window spans <= 4 stages)
+constexpr int kEpiWarps = 8;       // two per SM sub-partition: TMEM lane quadrant w % 4, column half w / 4
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr uint32_t kAcc = 128;     // TMEM columns per accumulator
-constexpr int kMaxSlots = 24;
-constexpr int kStgPitch = 36;      // floats per staged row: 128 B of outputs + 16 B (conflict-free 16-B access)
-constexpr int kStgBytes = 4 * 32 * kStgPitch * 4;  // 4 epilogue warps x 32 rows
+constexpr int kStgPitch = 36;      // floats per staged row: 128 B of accumulators + 16 B (conflict-free 16-B access)
+constexpr int kStgBytes = kEpiWarps * 32 * kStgPitch * 4;
+
 
 // 2^e as a float for |e| <= 126 (exact)
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
@@ -77,24 +82,25 @@ __device__ __forceinline__ void st_cs4(float2* p, float a, float b, float c, flo
 __global__ void __launch_bounds__(kThreads, 1)
     col_umma_kernel(const __grid_constant__ CUtensorMap jmap, const __grid_constant__ ColUArgs a) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t full[kMaxSlots], empty[kMaxSlots], tfull[2], tempty[2], aready;
+    // 1024-byte aligned ring (128-byte swizzle atoms); offsets from smem_raw keep the shared state space
+    uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], aready;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ns = a.ns, K = a.K, ksteps = a.K / 16;
+    const int K = a.K, ksteps = a.K / 16, wst = (ksteps + 3) / 4;  // stages spanned by a tile's window
     if (threadIdx.x == 0) {
-        for (int s = 0; s < ns; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         mbar_init(&tfull[0], 1);
         mbar_init(&tfull[1], 1);
-        mbar_init(&tempty[0], 128);
-        mbar_init(&tempty[1], 128);
-        mbar_init(&aready, 128);
+        mbar_init(&tempty[0], kEpiThreads);
+        mbar_init(&tempty[1], kEpiThreads);
+        mbar_init(&aready, kEpiThreads);
     }
-    if (warp == 5) umma::tmem_alloc(&tmem_base, 512);
-    if (warp == 4 && lane == 0) umma::tma_prefetch_desc(&jmap);
+    if (warp == kMmaWarp) umma::tmem_alloc(&tmem_base, 512);
+    if (warp == kTmaWarp && lane == 0) umma::tma_prefetch_desc(&jmap);
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
@@ -103,32 +109,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nunits = a.njobs * a.batch * a.nchunks * a.nstrips;
     const int chunk_rows = a.ch_tiles * kTile;
 
-    if (warp == 4) {
-        // ---------------- TMA producer ----------------
+    if (warp == kTmaWarp) {
+        // ---------------- TMA producer: one 64-row stage (hi / lo x 2 column blocks) per barrier ----------------
         if (lane == 0) {
-            uint32_t g = 0;
+            uint32_t g = 0;  // stage counter over the CTA's units
             for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
                 int job, b, chunk, strip;
                 unit_decode(a, u, job, b, chunk, strip);
                 const int y0 = chunk * chunk_rows;
                 const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
-                const int G = 4 * nt + ksteps - 4;
+                const int Gs = nt + wst - 1;
                 const int plane = (int)(2 * (((int64_t)b * a.ws_img_c + a.jobs[job].src_off) / a.hpw));
                 const int c0 = strip * 128;
-                for (int q = 0; q < G; ++q, ++g) {
-                    const uint32_t slot = g % (uint32_t)ns, round = g / (uint32_t)ns;
+                for (int q = 0; q < Gs; ++q, ++g) {
+                    const uint32_t slot = g % (uint32_t)kStages, round = g / (uint32_t)kStages;
                     mbar_wait(&empty[slot], (round & 1u) ^ 1u);
-                    uint8_t* sp = ring + slot * kSlotBytes;
-                    mbar_arrive_expect_tx(&full[slot], kSlotBytes);
-                    const int rr = y0 + a.jbuf - a.jpad + 16 * q;  // buffer row (input row + jbuf)
+                    uint8_t* sp = ring + slot * kStageBytes;
+                    if (a.dbg & 4) {  // A/B knob: no J loads
+                        umma::mbar_arrive(&full[slot]);
+                        continue;
+                    }
+                    mbar_arrive_expect_tx(&full[slot], kStageBytes);
+                    const int rr = y0 + a.jbuf - a.jpad + kTile * q;  // buffer row (input row + jbuf)
                     umma::tma_load_3d(sp, &jmap, c0, rr, plane, &full[slot]);
-                    umma::tma_load_3d(sp + 2048, &jmap, c0 + 64, rr, plane, &full[slot]);
-                    umma::tma_load_3d(sp + 4096, &jmap, c0, rr, plane + 1, &full[slot]);
-                    umma::tma_load_3d(sp + 6144, &jmap, c0 + 64, rr, plane + 1, &full[slot]);
+                    umma::tma_load_3d(sp + 8192, &jmap, c0 + 64, rr, plane, &full[slot]);
+                    umma::tma_load_3d(sp + 16384, &jmap, c0, rr, plane + 1, &full[slot]);
+                    umma::tma_load_3d(sp + 24576, &jmap, c0 + 64, rr, plane + 1, &full[slot]);
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == kMmaWarp) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             const uint32_t idesc = umma::idesc_f16_f32(128, 128, false, true);
@@ -139,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 unit_decode(a, u, job, b, chunk, strip);
                 const int y0 = chunk * chunk_rows;
                 const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
-                const int G = 4 * nt + ksteps - 4;
+                const int Gs = nt + wst - 1;
                 if (job != cur) {
                     mbar_wait(&aready, nreload & 1u);
                     ++nreload;
@@ -151,46 +161,52 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&tempty[buf], ((t >> 1) & 1u) ^ 1u);
                     umma::fence_after();
                     const uint32_t d = tb + buf * kAcc;
+                    // K step kk = group kk of the window: stage i + kk / 4, 16-row group kk % 4
                     for (int kk = 0; kk < ksteps; ++kk) {
-                        const uint32_t gg = g + 4 * i + kk;
-                        const uint32_t slot = gg % (uint32_t)ns;
-                        mbar_wait(&full[slot], (gg / (uint32_t)ns) & 1u);
-                        umma::fence_after();
-                        const uint32_t sb = smem_u32(ring + slot * kSlotBytes);
-                        const uint64_t bh = umma::smem_desc(sb, 2048, 1024, umma::kLayoutSw128);
-                        const uint64_t bl = umma::smem_desc(sb + 4096, 2048, 1024, umma::kLayoutSw128);
+                        const uint32_t gs = g + i + (kk >> 2);
+                        const uint32_t slot = gs % (uint32_t)kStages;
+                        if ((kk & 3) == 0) {
+                            mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
+                            umma::fence_after();
+                        }
+                        const uint32_t sb = smem_u32(ring + slot * kStageBytes) + 2048u * (kk & 3);
+                        const uint64_t bh = umma::smem_desc(sb, 8192, 1024, umma::kLayoutSw128);
+                        const uint64_t bl = umma::smem_desc(sb + 16384, 8192, 1024, umma::kLayoutSw128);
+                        if (a.dbg & 2) continue;  // A/B knob: no MMAs
                         umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
                         umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
                         umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
                     }
+                    // one commit per tile: the epilogue's first thread releases the ring stages
+                    // (stage i; all the unit's remaining stages after its last tile) once it has
+                    // seen this tile's accumulator complete
                     umma::mma_commit(&tfull[buf]);
-                    // the next tile's window starts 4 groups later: release the groups it no longer needs
-                    const int rel_end = (i == nt - 1) ? G : 4 * i + 4;
-                    for (int q = 4 * i; q < rel_end; ++q) umma::mma_commit(&empty[(g + q) % (uint32_t)ns]);
                 }
-                g += G;
+                g += Gs;
             }
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue (warps 0-3: TMEM lanes 32 w .. 32 w + 31) ----------------
-        const int m = threadIdx.x;
-        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        // ---------------- epilogue (warps 0-7: TMEM lanes 32 (w % 4) + 0..31, columns 64 (w / 4) + 0..63) ----------------
+        const int quad = warp & 3, half = warp >> 2;
+        const int m = 32 * quad + lane;  // TMEM lane = M row
+        const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
         const int r = m >> 1, odd = m & 1;
-        float* stg = reinterpret_cast<float*>(ring + ns * kSlotBytes) + warp * 32 * kStgPitch;  // [32][kStgPitch]
+        float* stg = reinterpret_cast<float*>(ring + kStages * kStageBytes) + warp * 32 * kStgPitch;  // [32][kStgPitch]
         int cur = -1;
-        uint32_t t = 0;
+        uint32_t t = 0, gst = 0;  // tiles; the producer's ring-stage counter at the start of the unit
         int wexp = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
             int job, b, chunk, strip;
             unit_decode(a, u, job, b, chunk, strip);
             const ColJob<float>& jb = a.jobs[job];
             if (job != cur) {
-                // tap matrix row m: K column k holds (odd ? kb : ka)[t], t = k - jpad - r
+                // tap matrix row m: K column k holds (odd ? kb : ka)[t], t = k - jpad - r; the two
+                // warps of a lane quadrant build alternate 16-column blocks
                 const float2* w = a.weights + jb.wofs;
                 wexp = jb.wexp;
                 const float wsc = pow2f(wexp);
-                for (int c = 0; c < K / 2; c += 16) {
+                for (int c = 16 * half; c < K / 2; c += 32) {
                     uint32_t hi[16], lo[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -221,59 +237,58 @@ __global__ void __launch_bounds__(kThreads, 1)
             float2* dst1 = a.dst_base + (nout > 1 ? jb.dst_off[1] : jb.dst_off[0]) + (int64_t)b * a.dst_bstride;
             const int y0 = chunk * chunk_rows;
             const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
-            const int x0 = strip * 64;
+            // read-back item of this lane: output row rloc (of the warp's 16) and 16-byte segment seg
+            const int seg = lane & 7;
+            const int Gs = nt + wst - 1;
             for (int i = 0; i < nt; ++i, ++t) {
                 const uint32_t buf = t & 1u;
                 mbar_wait(&tfull[buf], (t >> 1) & 1u);
                 umma::fence_after();
-                const int ybase = y0 + i * kTile + 16 * warp;  // output row of this warp's M rows 0 / 1
+                if (threadIdx.x == 0) {  // the MMAs of this tile are done: its first stage is free
+                    const int rel_end = (i == nt - 1) ? Gs : i + 1;
+                    for (int q = i; q < rel_end; ++q) umma::mbar_arrive(&empty[(gst + q) % (uint32_t)kStages]);
+                }
+                const int ybase = y0 + i * kTile + 16 * quad;  // output row of M rows 0 / 1 of the quadrant
 #pragma unroll 1
-                for (int qq = 0; qq < 4; ++qq) {  // 16 complex columns per pass
-                    float v[32], p[32];
-                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + 32 * qq, *reinterpret_cast<float(*)[16]>(v));
-                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + 32 * qq + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+                for (int qq = 0; qq < 2; ++qq) {  // 32 accumulator columns = 16 complex per pass
+                    const int col = 64 * half + 32 * qq;
+                    float v[32];
+                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + col, *reinterpret_cast<float(*)[16]>(v));
+                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + col + 16, *reinterpret_cast<float(*)[16]>(v + 16));
                     umma::tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) p[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
-                    // even lane: X = A - iB (A own, B partner); odd lane: conj(A + iB) (A partner, B own)
+                    // stage the raw accumulator row (A of output row r on even lanes, B on odd lanes)
                     float4* srow = reinterpret_cast<float4*>(stg + lane * kStgPitch);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        float o[4];
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int c = 4 * j + 2 * e;
-                            if (!odd) {
-                                o[2 * e] = (v[c] + p[c + 1]) * inv;
-                                o[2 * e + 1] = (v[c + 1] - p[c]) * inv;
-                            } else {
-                                o[2 * e] = (p[c] - v[c + 1]) * inv;
-                                o[2 * e + 1] = -(p[c + 1] + v[c]) * inv;
-                            }
-                        }
-                        srow[j] = make_float4(o[0], o[1], o[2], o[3]);
-                    }
+                    for (int j = 0; j < 8; ++j) srow[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                     __syncwarp();
-                    // coalesced write-out: instruction k covers staged rows 4k .. 4k+3, 128 B each
+                    // combine + coalesced write-out: pass k covers output rows 4k .. 4k+3 of the 16
+                    const int x = strip * 64 + col / 2 + 2 * seg;
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int rho = 4 * k + (lane >> 3), seg = lane & 7;
-                        const float4 val = *reinterpret_cast<const float4*>(stg + rho * kStgPitch + 4 * seg);
-                        const int orow = ybase + (rho >> 1);
-                        const int x = x0 + 16 * qq + 2 * seg;
-                        if (orow < a.H && x < a.W && ((rho & 1) == 0 || nout > 1))
-                            st_cs4(((rho & 1) ? dst1 : dst0) + (int64_t)orow * a.W + x, val.x, val.y, val.z, val.w);
+                    for (int k = 0; k < 4; ++k) {
+                        const int rl = 4 * k + (lane >> 3);
+                        const float4 A = *reinterpret_cast<const float4*>(stg + (2 * rl) * kStgPitch + 4 * seg);
+                        const float4 B = *reinterpret_cast<const float4*>(stg + (2 * rl + 1) * kStgPitch + 4 * seg);
+                        const int orow = ybase + rl;
+                        if (orow < a.H && x < a.W && !(a.dbg & 1)) {
+                            const int64_t o = (int64_t)orow * a.W + x;
+                            // F_theta = A - iB; F_{pi - theta} = conj(A + iB)
+                            st_cs4(dst0 + o, (A.x + B.y) * inv, (A.y - B.x) * inv, (A.z + B.w) * inv, (A.w - B.z) * inv);
+                            if (nout > 1)
+                                st_cs4(dst1 + o, (A.x - B.y) * inv, -(A.y + B.x) * inv, (A.z - B.w) * inv,
+                                       -(A.w + B.z) * inv);
+                        }
                     }
                     __syncwarp();
                 }
                 umma::fence_before();
                 umma::mbar_arrive(&tempty[buf]);
             }
+            gst += Gs;
         }
     }
     umma::fence_before();
     __syncthreads();
-    if (warp == 5) umma::tmem_dealloc(tb, 512);
+    if (warp == kMmaWarp) umma::tmem_dealloc(tb, 512);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -301,19 +316,18 @@ bool col_umma_supported(int h, int W) {
     return h >= 1 && K <= 256 && W % 4 == 0 && W >= 64 && encode_fn() != nullptr;
 }
 
-size_t col_umma_smem(int h) {
-    const int K = kTile + 2 * col_umma_jpad(h);
-    const int ns = std::min(kMaxSlots, K / 16 + 8);
-    // >= 116 KB so that two of these CTAs (512 TMEM columns each) never share an SM
-    return std::max<size_t>((size_t)ns * kSlotBytes + kStgBytes + 1024, 116 * 1024);
+size_t col_umma_smem(int) {
+    // ring + staging + alignment slack (> 114 KB: two of these CTAs, 512 TMEM columns each, never share an SM)
+    return (size_t)kStages * kStageBytes + kStgBytes + 1024;
 }
 
 cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cudaStream_t s) {
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
+    static const int dbg = std::getenv("FGB_UMMA_DBG") ? std::atoi(std::getenv("FGB_UMMA_DBG")) : 0;
+    a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no J loads); results are wrong when set
     a.jpad = col_umma_jpad(a.h);
     a.K = kTile + 2 * a.jpad;
-    a.ns = std::min(kMaxSlots, a.K / 16 + 8);
     if (a.jpad > a.jbuf || a.hpw != (a.H + 2 * (int64_t)a.jbuf) * a.W) {
         std::fprintf(stderr, "col_umma: J slot layout mismatch (jpad %d jbuf %d hpw %lld)\n", a.jpad, a.jbuf,
                      (long long)a.hpw);
@@ -326,7 +340,7 @@ cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cud
     CUtensorMap map;
     cuuint64_t dims[3] = {(cuuint64_t)2 * a.W, (cuuint64_t)Hp, (cuuint64_t)nplanes};
     cuuint64_t strides[2] = {(cuuint64_t)a.W * 4, (cuuint64_t)plane_bytes};
-    cuuint32_t box[3] = {64, 16, 1};
+    cuuint32_t box[3] = {64, kTile, 1};  // one 64-row stage block per load
     cuuint32_t estr[3] = {1, 1, 1};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
@@ -349,7 +363,7 @@ cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cud
     if (!attr) {
         // the largest ring (+ alignment slack); static shared memory comes on top of it
         cudaError_t e = cudaFuncSetAttribute(col_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kMaxSlots * kSlotBytes + kStgBytes + 1024);
+                                             (int)col_umma_smem(0));
         if (e != cudaSuccess) return e;
         attr = true;
     }

@@ -100,8 +100,9 @@ struct ColUArgs {
     int64_t hpw;                // complex elements per J slot = (H + 2 jbuf) * W
     int H, W, h, njobs, batch;
     int jbuf;                   // replicate rows above / below the image rows in the J planes
-    int jpad, K, ns;            // set by the launcher (jpad = h rounded up to 16 <= jbuf)
+    int jpad, K;                // set by the launcher (jpad = h rounded up to 16 <= jbuf)
     int nstrips, nchunks, ch_tiles;
+    int dbg;                    // set by the launcher from FGB_UMMA_DBG (ablation only)
 };
 int col_umma_jpad(int h);
 bool col_umma_supported(int h, int W);

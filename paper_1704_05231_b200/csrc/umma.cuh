@@ -106,6 +106,16 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
 }
 
+// Spin on an mbarrier phase (try_wait without a suspend-time hint): the hand-offs of the
+// column pipeline are short, so the waiter polls instead of parking.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 // Non-blocking probe of an mbarrier phase (the waiting loop lives in mbar_wait).
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
