@@ -296,7 +296,7 @@ struct Ref {
     int64_t off = 0;  // elements of the referenced type (T for real, C for complex)
 };
 
-enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF, ST_BANKF, ST_COLU };
+enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF, ST_BANKF, ST_COLU, ST_ROWU };
 
 template <typename T> struct Step {
     int kind = 0;
@@ -356,6 +356,7 @@ template <typename T> struct Plan : PlanBase {
     int64_t out_img_c = 0;        // complex elements per output image
     int H = 0, W = 0;
     int jbuf = 0;                 // > 0: J slots are split-fp16 planes with jbuf replicate rows (ST_COLU)
+    int xbuf = 0;                 // > 0: some row stages run on the tensor cores (ST_ROWU) from x-padded prep planes
     int64_t hpw = 0;              // (H + 2 jbuf) * W: complex elements per J slot (= u32 per fp16 plane)
     int chunk = 1;
     int nlanes = 1;               // concurrent stream lanes used by the steps
@@ -690,6 +691,10 @@ static bool fused_bank_used(int h, int nj, int H, int W) {
 
 // Tensor-core column pass (col_umma.cu) for an fp32 FIR bank frequency of half-width h
 // (FGB_COL_FFMA=1 keeps the FFMA column kernel; FGB_UMMA_MIN_H sets the smallest h).
+static bool rowu_used(int h, int W) {
+    static const bool off = std::getenv("FGB_ROW_FFMA") != nullptr;
+    return !off && row_umma_supported(h, W);
+}
 static bool umma_freq_used(int h, int nj, int H, int W) {
     static const bool off = std::getenv("FGB_COL_FFMA") != nullptr;
     static const int min_h = std::getenv("FGB_UMMA_MIN_H") ? std::atoi(std::getenv("FGB_UMMA_MIN_H")) : 7;
@@ -783,7 +788,39 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
         const bool umma = std::is_same<T, float>::value && !box && !row_only && !col_only && b.p.jbuf > 0 &&
                           umma_freq_used(h, nj, H, W) && col_umma_jpad(h) <= b.p.jbuf;
         // ---- row stage ----
-        if (!col_only) {
+        if (!col_only && umma && b.p.xbuf > 0 && rowu_used(h, W) && row_umma_jpad(h) <= b.p.xbuf) {
+            // tensor-core row pass: every direct of the frequency in one persistent launch
+            Step<T> st;
+            st.kind = ST_ROWU;
+            st.name = "row_umma";
+            const double sflops = 4.0 * h + 1;
+            st.flops = nj * (2.0 * sflops + 8.0) * H * W;
+            st.bytes = (double)H * W * sizeof(T) + (double)nj * H * W * sizeof(cx_t<T>);
+            st.H = H;
+            st.W = W;
+            st.h = h;
+            st.src = img;
+            st.dst = R(SEL_WS, 0);
+            st.job0 = (int)b.p.cjobs.size();
+            st.njobs = nj;
+            for (int j = 0; j < nj; ++j) {
+                ColJob<T> q{};
+                q.wofs = (int32_t)b.p.wcol.size();
+                double mx = 0.0;
+                for (int t = 0; t <= h; ++t) {
+                    const double kr = w[h + t] * std::cos(jobs[j].wc * t), ki = -w[h + t] * std::sin(jobs[j].wc * t);
+                    b.p.wcol.push_back(mk<T>((T)kr, (T)ki));
+                    mx = std::max(mx, std::max(std::fabs(kr), std::fabs(ki)));
+                }
+                int ex = 0;
+                if (mx > 0.0) std::frexp(mx, &ex);
+                q.wexp = 10 - ex;
+                q.nout = 1;
+                q.dst_off[0] = ws_j0 + (int64_t)j * jslot;
+                b.p.cjobs.push_back(q);
+            }
+            b.push(st);
+        } else if (!col_only) {
             if (!box) {
                 // row launches of <= gmax directs, balanced (9 -> 5 + 4 with gmax 5)
                 static const int gmax = std::max(1, std::min(kMaxND, std::getenv("FGB_ROW_GROUP") ? std::atoi(std::getenv("FGB_ROW_GROUP")) : kMaxND));
@@ -998,6 +1035,14 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
             if (per_f[i].empty()) continue;
             const int h = std::max(1, (int)std::ceil(d.smoother.radius * d.sigmas[i]));
             if (umma_freq_used(h, (int)per_f[i].size(), H, W)) p.jbuf = std::max(p.jbuf, col_umma_jpad(h));
+        }
+    }
+    if (p.jbuf > 0) {
+        for (int i = 0; i < d.n_freq; ++i) {
+            if (per_f[i].empty()) continue;
+            const int h = std::max(1, (int)std::ceil(d.smoother.radius * d.sigmas[i]));
+            if (umma_freq_used(h, (int)per_f[i].size(), H, W) && rowu_used(h, W))
+                p.xbuf = std::max(p.xbuf, row_umma_jpad(h));
         }
     }
     const int64_t jslot = p.jbuf > 0 ? (int64_t)(H + 2 * p.jbuf) * W : HW;
@@ -1419,6 +1464,7 @@ struct Ctx {
     std::map<std::string, std::unique_ptr<DevBuf>> line_taps;  // fgb_smooth_lines tap tables (immutable)
     DevBuf ser_scratch;                                         // fgb_ser_sums partials
     DevBuf maxbits;                                             // max|f| bits per image (split-fp16 J scale)
+    DevBuf fprep;                                               // x-padded split-fp16 image planes (ST_ROWU)
     int sms = 0;                                                // SM count (persistent grids)
     DevBuf iir_cnt;                                             // iir32 arrival counters, zero between launches
     size_t iir_cnt_zeroed = 0;                                  // bytes of iir_cnt known to be zero
@@ -1511,6 +1557,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     FGB_TRY(ws_acquire(cx, s));
     if (p.jbuf > 0) {
         FGB_TRY(cx.maxbits.ensure(sizeof(unsigned) * (size_t)chunk));
+        if (p.xbuf > 0) FGB_TRY(cx.fprep.ensure(row_umma_fprep_bytes(p.H, p.W, p.xbuf, chunk)));
         if (cx.sms == 0) {
             int dev = 0;
             FGB_CUDA(cudaGetDevice(&dev));
@@ -1540,6 +1587,11 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
             if (p.jbuf > 0) {  // split-fp16 J scale per image, before the lanes fork
                 ++g_launches;
                 FGB_CUDA(launch_absmax(imgb, im.pitch, img_bs, p.H, p.W, nb, (unsigned*)cx.maxbits.p, cx.sms, s));
+                if (p.xbuf > 0) {
+                    ++g_launches;
+                    FGB_CUDA(launch_row_umma_prep(imgb, im.pitch, img_bs, p.H, p.W, p.xbuf, nb,
+                                                  (const unsigned*)cx.maxbits.p, cx.fprep.p, s));
+                }
             }
         }
         if (nl > 1) {
@@ -1609,6 +1661,25 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.j16_plane = p.hpw;
                     a.maxbits = (const unsigned*)cx.maxbits.p;
                     FGB_CUDA(launch_row_sym<T>(a, st.rg, knobs().row_smem_taps ? nullptr : p.wrow.data() + st.rg.wofs, s));
+                    break;
+                }
+                case ST_ROWU: {
+                    if constexpr (std::is_same<T, float>::value) {
+                        RowUArgs a{};
+                        a.jobs = p.d_cjobs() + st.job0;
+                        a.weights = p.d_wcol();
+                        a.dst_base = ws;
+                        a.dst_bstride = p.ws_img_c;
+                        a.hpw = p.hpw;
+                        a.H = st.H;
+                        a.W = st.W;
+                        a.h = st.h;
+                        a.njobs = st.njobs;
+                        a.batch = nb;
+                        a.jbuf = p.jbuf;
+                        a.xbuf = p.xbuf;
+                        FGB_CUDA(launch_row_umma(a, cx.fprep.p, cx.sms, s));
+                    }
                     break;
                 }
                 case ST_COLU: {

@@ -109,6 +109,26 @@ bool col_umma_supported(int h, int W);
 size_t col_umma_smem(int h);
 // ws / ws_bytes: the J region of the workspace (the tensor map spans it)
 cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cudaStream_t s);
+// ---- K1u: row pass on the tensor cores (row_umma.cu, fp32 build) ---------
+// Reads x-padded split-fp16 image planes (launch_row_umma_prep), writes the split-fp16
+// J slots of ColUArgs (rows + replicate pad rows).  jobs[j]: wofs = row taps (kr, ki)
+// for t = 0..h in `weights`, wexp, dst_off[0] = the J slot (complex elements from dst_base).
+struct RowUArgs {
+    const ColJob<float>* jobs;
+    const float2* weights;
+    float2* dst_base;
+    int64_t dst_bstride;        // complex elements between images (the workspace image stride)
+    int64_t hpw;                // complex elements per J slot = (H + 2 jbuf) * W
+    int H, W, h, njobs, batch, jbuf;
+    int xbuf;                   // replicate columns left / right of the image in the prep planes
+    int jpad, K, nstrips, nyb;  // set by the launcher
+};
+int row_umma_jpad(int h);
+bool row_umma_supported(int h, int W);
+size_t row_umma_fprep_bytes(int H, int W, int xbuf, int batch);
+cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstride, int H, int W, int xbuf, int batch,
+                                 const unsigned* maxbits, void* fprep, cudaStream_t s);
+cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t s);
 // max|f| bits per image (memset + atomicMax)
 cudaError_t launch_absmax(const float* img, int64_t pitch, int64_t bstride, int H, int W, int batch, unsigned* out,
                           int sms, cudaStream_t s);

@@ -1,0 +1,363 @@
+// K1u: fp32-build row stage of the Gabor bank on the tensor cores (tcgen05,
+// split-fp16), writing the split-fp16 J planes the column pass (col_umma.cu)
+// reads.
+//
+// Reference semantics: horizontal_stage (gabor.py:107-132).  With the
+// modulation folded into the taps, for one direct
+// orientation (row phase step omega_c = omega cos theta):
+//     J(y, x) = sum_{t=-h..h} w[t] e^{-i omega_c t} f[y, clamp(x+t)].
+// Over a tile of 64 output columns x 128 image rows this is a banded Toeplitz
+// product D (128 x 128) = Wt (128 x K) . Ft (K x 128):
+//   * M row 2 xl / 2 xl + 1 = Re / Im taps of output column xl (kr[|t|],
+//     sgn(t) ki[|t|]) at K column k = xl + jpad + t (zero outside the band),
+//   * K = 64 + 2 jpad input columns (jpad = h rounded up to 32, so the window
+//     is whole 64-column TMA boxes), read from x-padded split-fp16 image
+//     planes (replicate padding: clamp() costs nothing),
+//   * N = 128 image rows (the image rows are the K-major B operand).
+// Precision as in col_umma.cu: f 2^e = f_hi + f_lo (the image prep kernel),
+// taps 2^s = w_hi + w_lo, D = Wh Fh + Wh Fl + Wl Fh in fp32 (TMEM); the
+// epilogue multiplies by 2^-s, giving J 2^e, and splits it into the hi / lo
+// half2 planes.
+//
+// Persistent warp-specialised CTA (one per SM): warp 8 TMA producer (64-column
+// x 128-row boxes of the hi and lo image planes = one 32 KB ring stage per
+// 64 K columns), warp 9 TMEM allocator + MMA issuer (K/16 steps x 3 MMAs,
+// M = 128, N = 128, K-major B with 128-byte swizzle), warps 0-7 epilogue
+// (TMEM lane quadrant w % 4 = 16 output columns, column half w / 4 = 64 image
+// rows): TMEM -> shared transpose -> hi / lo split -> row-contiguous stores,
+// the first / last image row also into the jbuf replicate pad rows.  Work
+// unit = one tile (direct, image, 128-row block, 64-column strip), strips
+// fastest; the taps of a direct are (re)built in TMEM when it changes.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "kernels.h"
+#include "umma.cuh"
+
+namespace fgb {
+
+namespace {
+
+constexpr int kTX = 64;            // output columns per tile
+constexpr int kTY = 128;           // image rows per tile (MMA N)
+constexpr int kStageBytes = 32768; // 64 K columns: (hi, lo) x 128 rows x 128 B
+constexpr int kStages = 5;
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+constexpr int kThreads = 32 * (kEpiWarps + 2);
+constexpr uint32_t kAcc = 128;
+constexpr int kStgPitch = 136;     // floats per staged image row: 128 M rows + 8 (16-byte rows)
+constexpr int kStgBytes = 2 * 32 * kStgPitch * 4;  // one [32 image rows][128 M rows] block per column half
+
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
+
+// Each CTA runs a contiguous range of units (consecutive strips of one row block: the
+// column halo of a tile is the previous tile's, still in L2); the unit coordinates are
+// decoded once and then stepped (no integer division per tile).
+struct UnitIter {
+    int u, u1, job, b, yb, strip;
+    __device__ UnitIter(const RowUArgs& a, int nunits) {
+        u = (int)((int64_t)blockIdx.x * nunits / gridDim.x);
+        u1 = (int)((int64_t)(blockIdx.x + 1) * nunits / gridDim.x);
+        strip = u % a.nstrips;
+        int r = u / a.nstrips;
+        yb = r % a.nyb;
+        r /= a.nyb;
+        b = r % a.batch;
+        job = r / a.batch;
+    }
+    __device__ bool ok() const { return u < u1; }
+    __device__ void next(const RowUArgs& a) {
+        ++u;
+        if (++strip == a.nstrips) {
+            strip = 0;
+            if (++yb == a.nyb) {
+                yb = 0;
+                if (++b == a.batch) {
+                    b = 0;
+                    ++job;
+                }
+            }
+        }
+    }
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    row_umma_kernel(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ RowUArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], aready;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int K = a.K, ksteps = a.K / 16, kst = a.K / 64;  // ring stages per tile
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tfull[1], 1);
+        mbar_init(&tempty[0], kEpiThreads);
+        mbar_init(&tempty[1], kEpiThreads);
+        mbar_init(&aready, kEpiThreads);
+    }
+    if (warp == kMmaWarp) umma::tmem_alloc(&tmem_base, 512);
+    if (warp == kTmaWarp && lane == 0) umma::tma_prefetch_desc(&fmap);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tb = tmem_base;
+    const uint32_t a_hi = tb + 2 * kAcc, a_lo = a_hi + (uint32_t)(K / 2);
+    const int nunits = a.njobs * a.batch * a.nyb * a.nstrips;
+
+    if (warp == kTmaWarp) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (UnitIter it(a, nunits); it.ok(); it.next(a)) {
+                const int b = it.b, yb = it.yb, strip = it.strip;
+                const int xs = strip * kTX - a.jpad + a.xbuf;  // padded-plane column of K column 0
+                for (int q = 0; q < kst; ++q, ++g) {
+                    const uint32_t slot = g % (uint32_t)kStages, round = g / (uint32_t)kStages;
+                    mbar_wait(&empty[slot], (round & 1u) ^ 1u);
+                    uint8_t* sp = ring + slot * kStageBytes;
+                    mbar_arrive_expect_tx(&full[slot], kStageBytes);
+                    umma::tma_load_3d(sp, &fmap, xs + 64 * q, yb * kTY, 2 * b, &full[slot]);
+                    umma::tma_load_3d(sp + 16384, &fmap, xs + 64 * q, yb * kTY, 2 * b + 1, &full[slot]);
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t idesc = umma::idesc_f16_f32(128, kTY, false, false);
+            uint32_t g = 0, t = 0, nreload = 0;
+            int cur = -1;
+            for (UnitIter it(a, nunits); it.ok(); it.next(a), ++t) {
+                const int job = it.job;
+                if (job != cur) {
+                    mbar_wait(&aready, nreload & 1u);
+                    ++nreload;
+                    cur = job;
+                    umma::fence_after();
+                }
+                const uint32_t buf = t & 1u;
+                mbar_wait(&tempty[buf], ((t >> 1) & 1u) ^ 1u);
+                umma::fence_after();
+                const uint32_t d = tb + buf * kAcc;
+                for (int kk = 0; kk < ksteps; ++kk) {
+                    const uint32_t gs = g + (kk >> 2);
+                    const uint32_t slot = gs % (uint32_t)kStages;
+                    if ((kk & 3) == 0) {
+                        mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
+                        umma::fence_after();
+                    }
+                    // K-major, 128-byte swizzle: K step = 32 bytes inside the swizzle atom
+                    const uint32_t sb = smem_u32(ring + slot * kStageBytes) + 32u * (kk & 3);
+                    const uint64_t bh = umma::smem_desc(sb, 16, 1024, umma::kLayoutSw128);
+                    const uint64_t bl = umma::smem_desc(sb + 16384, 16, 1024, umma::kLayoutSw128);
+                    umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
+                    umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
+                    umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                    if ((kk & 3) == 3) umma::mma_commit(&empty[slot]);  // stage fully consumed
+                }
+                umma::mma_commit(&tfull[buf]);
+                g += kst;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue ----------------
+        const int quad = warp & 3, half = warp >> 2;
+        const int m = 32 * quad + lane;  // TMEM lane = M row = (output column xl = m / 2, Re / Im)
+        const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
+        const int xl = m >> 1, im = m & 1;
+        float* stg = reinterpret_cast<float*>(ring + kStages * kStageBytes) + half * 32 * kStgPitch;
+        int cur = -1;
+        uint32_t t = 0;
+        float inv_w = 1.f;
+        const int H = a.H, W = a.W, jbuf = a.jbuf;
+        const int64_t hpw = a.hpw;
+        for (UnitIter it(a, nunits); it.ok(); it.next(a), ++t) {
+            const int job = it.job, b = it.b, yb = it.yb, strip = it.strip;
+            const ColJob<float>& jb = a.jobs[job];
+            if (job != cur) {
+                // tap row m: K column k -> t = k - jpad - xl: (kr[|t|], sgn(t) ki[|t|]) * 2^wexp
+                const float2* w = a.weights + jb.wofs;
+                const float wsc = pow2f(jb.wexp);
+                inv_w = pow2f(-jb.wexp);
+                for (int c = 16 * half; c < K / 2; c += 32) {
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float v[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int tt = 2 * (c + i) + e - a.jpad - xl;
+                            const int at = tt < 0 ? -tt : tt;
+                            float x = 0.f;
+                            if (at <= a.h) {
+                                const float2 kk = w[at];
+                                x = (im ? (tt < 0 ? -kk.y : kk.y) : kk.x) * wsc;
+                            }
+                            v[e] = x;
+                        }
+                        umma::split_f16x2(v[0], v[1], hi[i], lo[i]);
+                    }
+                    umma::tmem_st16(a_hi + lane_addr + c, hi);
+                    umma::tmem_st16(a_lo + lane_addr + c, lo);
+                }
+                umma::tmem_st_wait();
+                umma::fence_before();
+                umma::mbar_arrive(&aready);
+                cur = job;
+            }
+            uint32_t* jh = reinterpret_cast<uint32_t*>(a.dst_base + jb.dst_off[0] + (int64_t)b * a.dst_bstride);
+            // write-out item of this lane: image row (2 rr2 + (lane >> 4)) of the warp's 8, columns 4 c4 .. 4 c4 + 3
+            const int c4 = lane & 15, ro = lane >> 4;
+            const int x = strip * kTX + 4 * c4;
+            const bool xok = x < W;
+            const uint32_t buf = t & 1u;
+            mbar_wait(&tfull[buf], (t >> 1) & 1u);
+            umma::fence_after();
+#pragma unroll 1
+            for (int qq = 0; qq < 2; ++qq) {  // 32 image rows per pass
+                const int n0 = 64 * half + 32 * qq;
+                float v[32];
+                umma::tmem_ld16(tb + lane_addr + buf * kAcc + n0, *reinterpret_cast<float(*)[16]>(v));
+                umma::tmem_ld16(tb + lane_addr + buf * kAcc + n0 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+                umma::tmem_ld_wait();
+                named_bar(1 + half, 128);  // the previous pass's reads of this half's staging are done
+                // staging [32 image rows][128 M rows (+pad)]: row-major by image row
+#pragma unroll
+                for (int j = 0; j < 32; ++j) stg[j * kStgPitch + m] = v[j];
+                named_bar(1 + half, 128);
+                // write-out: warp quad handles image rows 8 quad .. 8 quad + 7 of the 32, two per step
+                const int yq = yb * kTY + n0 + 8 * quad + ro;
+                const float* sq = stg + (8 * quad + ro) * kStgPitch + 8 * c4;
+                uint32_t* pq = jh + (int64_t)(yq + jbuf) * W + x;
+#pragma unroll
+                for (int rr2 = 0; rr2 < 4; ++rr2) {
+                    const int y = yq + 2 * rr2;
+                    const float4 p0 = *reinterpret_cast<const float4*>(sq + 2 * rr2 * kStgPitch);
+                    const float4 p1 = *reinterpret_cast<const float4*>(sq + 2 * rr2 * kStgPitch + 4);
+                    uint4 hw, lw;
+                    umma::split_f16x2(p0.x * inv_w, p0.y * inv_w, hw.x, lw.x);
+                    umma::split_f16x2(p0.z * inv_w, p0.w * inv_w, hw.y, lw.y);
+                    umma::split_f16x2(p1.x * inv_w, p1.y * inv_w, hw.z, lw.z);
+                    umma::split_f16x2(p1.z * inv_w, p1.w * inv_w, hw.w, lw.w);
+                    if (y < H && xok) {
+                        uint32_t* p = pq + (int64_t)(2 * rr2) * W;
+                        *reinterpret_cast<uint4*>(p) = hw;
+                        *reinterpret_cast<uint4*>(p + hpw) = lw;
+                        if (y == 0 || y == H - 1) {  // replicate rows of the column pass's padding
+                            const int r0 = y == 0 ? 0 : H + jbuf, r1 = y == 0 ? jbuf : H + 2 * jbuf;
+                            for (int r = r0; r < r1; ++r) {
+                                uint32_t* q = jh + (int64_t)r * W + x;
+                                *reinterpret_cast<uint4*>(q) = hw;
+                                *reinterpret_cast<uint4*>(q + hpw) = lw;
+                            }
+                        }
+                    }
+                }
+            }
+            umma::fence_before();
+            umma::mbar_arrive(&tempty[buf]);
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) umma::tmem_dealloc(tb, 512);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (EncodeFn)p;
+    }();
+    return fn;
+}
+
+// image -> x-padded split-fp16 planes: plane 2b = hi, 2b + 1 = lo of (f 2^e) (replicate padding)
+__global__ void fprep_kernel(const float* __restrict__ img, int64_t pitch, int64_t bstride, int H, int W, int xbuf,
+                             int Wp, const unsigned* __restrict__ maxbits, __half* __restrict__ out) {
+    const int b = blockIdx.z, y = blockIdx.y;
+    const float sc = pow2f(jscale_exp(maxbits[b]));
+    const float* row = img + (int64_t)b * bstride + (int64_t)y * pitch;
+    __half* hi = out + ((int64_t)(2 * b) * H + y) * Wp;
+    __half* lo = out + ((int64_t)(2 * b + 1) * H + y) * Wp;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < Wp; x += gridDim.x * blockDim.x) {
+        const float v = row[min(max(x - xbuf, 0), W - 1)] * sc;
+        const __half h = __float2half_rn(v);
+        hi[x] = h;
+        lo[x] = __float2half_rn(v - __half2float(h));
+    }
+}
+
+}  // namespace
+
+int row_umma_jpad(int h) { return (h + 31) / 32 * 32; }
+
+bool row_umma_supported(int h, int W) {
+    return h >= 1 && kTX + 2 * row_umma_jpad(h) <= 256 && W % 8 == 0 && W >= kTX && encode_fn() != nullptr;
+}
+
+size_t row_umma_fprep_bytes(int H, int W, int xbuf, int batch) {
+    return (size_t)batch * 2 * H * (size_t)(W + 2 * xbuf) * sizeof(__half);
+}
+
+cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstride, int H, int W, int xbuf, int batch,
+                                 const unsigned* maxbits, void* fprep, cudaStream_t s) {
+    const int Wp = W + 2 * xbuf;
+    dim3 grid((Wp + 255) / 256, H, batch);
+    fprep_kernel<<<grid, 256, 0, s>>>(img, pitch, bstride, H, W, xbuf, Wp, maxbits, (__half*)fprep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t s) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    a.jpad = row_umma_jpad(a.h);
+    a.K = kTX + 2 * a.jpad;
+    if (a.jpad > a.xbuf || a.K > 256) return cudaErrorInvalidValue;
+    const int Wp = a.W + 2 * a.xbuf;
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)Wp, (cuuint64_t)a.H, (cuuint64_t)2 * a.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)Wp * 2, (cuuint64_t)Wp * 2 * a.H};
+    cuuint32_t box[3] = {64, kTY, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(fprep), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        std::fprintf(stderr, "row_umma: tensor map encode failed (Wp %d H %d)\n", Wp, a.H);
+        return cudaErrorInvalidValue;
+    }
+    a.nstrips = (a.W + kTX - 1) / kTX;
+    a.nyb = (a.H + kTY - 1) / kTY;
+    const int64_t units = (int64_t)a.njobs * a.batch * a.nyb * a.nstrips;
+    const int grid = (int)std::min<int64_t>(units, sms);
+    const size_t smem = (size_t)kStages * kStageBytes + kStgBytes + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(row_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    row_umma_kernel<<<grid, kThreads, smem, s>>>(map, a);
+    return cudaGetLastError();
+}
+
+}  // namespace fgb
