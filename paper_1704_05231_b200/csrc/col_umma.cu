@@ -249,17 +249,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int q = i; q < rel_end; ++q) umma::mbar_arrive(&empty[(gst + q) % (uint32_t)kStages]);
                 }
                 const int ybase = y0 + i * kTile + 16 * quad;  // output row of M rows 0 / 1 of the quadrant
-#pragma unroll 1
+                float v[64];  // this warp's 64 accumulator columns, one TMEM wait
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + 64 * half + 16 * j, *reinterpret_cast<float(*)[16]>(v + 16 * j));
+                umma::tmem_ld_wait();
+                umma::fence_before();
+                umma::mbar_arrive(&tempty[buf]);  // accumulator drained: the MMA may reuse it
+#pragma unroll
                 for (int qq = 0; qq < 2; ++qq) {  // 32 accumulator columns = 16 complex per pass
                     const int col = 64 * half + 32 * qq;
-                    float v[32];
-                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + col, *reinterpret_cast<float(*)[16]>(v));
-                    umma::tmem_ld16(tb + lane_addr + buf * kAcc + col + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-                    umma::tmem_ld_wait();
                     // stage the raw accumulator row (A of output row r on even lanes, B on odd lanes)
                     float4* srow = reinterpret_cast<float4*>(stg + lane * kStgPitch);
+                    __syncwarp();
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) srow[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    for (int j = 0; j < 8; ++j)
+                        srow[j] = make_float4(v[32 * qq + 4 * j], v[32 * qq + 4 * j + 1], v[32 * qq + 4 * j + 2], v[32 * qq + 4 * j + 3]);
                     __syncwarp();
                     // combine + coalesced write-out: pass k covers output rows 4k .. 4k+3 of the 16
                     const int x = strip * 64 + col / 2 + 2 * seg;
@@ -278,10 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        -(A.w + B.z) * inv);
                         }
                     }
-                    __syncwarp();
                 }
-                umma::fence_before();
-                umma::mbar_arrive(&tempty[buf]);
             }
             gst += Gs;
         }

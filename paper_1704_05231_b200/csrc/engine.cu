@@ -1041,7 +1041,11 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
         for (int i = 0; i < d.n_freq; ++i) {
             if (per_f[i].empty()) continue;
             const int h = std::max(1, (int)std::ceil(d.smoother.radius * d.sigmas[i]));
-            if (umma_freq_used(h, (int)per_f[i].size(), H, W) && rowu_used(h, W))
+            // the persistent row kernel needs enough 128 x 64 tiles per SM to amortise its pipeline fill
+            // (config 2, 1024^2 x 5 directs: 4 tiles per SM, FFMA rows 21 us vs 32 us per launch)
+            const int64_t tiles = (int64_t)((H + 127) / 128) * ((W + 63) / 64) * (int64_t)per_f[i].size() *
+                                  std::min(d.img.batch, 16);
+            if (umma_freq_used(h, (int)per_f[i].size(), H, W) && rowu_used(h, W) && tiles >= 16 * 148)
                 p.xbuf = std::max(p.xbuf, row_umma_jpad(h));
         }
     }

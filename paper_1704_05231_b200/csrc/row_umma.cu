@@ -49,8 +49,8 @@ constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr uint32_t kAcc = 128;
-constexpr int kStgPitch = 136;     // floats per staged image row: 128 M rows + 8 (16-byte rows)
-constexpr int kStgBytes = 2 * 32 * kStgPitch * 4;  // one [32 image rows][128 M rows] block per column half
+constexpr int kStgPitch = 36;      // floats per staged image row: a warp's 32 M rows + 4 (conflict-free)
+constexpr int kStgBytes = kEpiWarps * 32 * kStgPitch * 4;  // one [32 image rows][32 M rows] block per warp
 
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
 
@@ -84,8 +84,6 @@ struct UnitIter {
         }
     }
 };
-
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
 __global__ void __launch_bounds__(kThreads, 1)
     row_umma_kernel(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ RowUArgs a) {
@@ -177,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m = 32 * quad + lane;  // TMEM lane = M row = (output column xl = m / 2, Re / Im)
         const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
         const int xl = m >> 1, im = m & 1;
-        float* stg = reinterpret_cast<float*>(ring + kStages * kStageBytes) + half * 32 * kStgPitch;
+        float* stg = reinterpret_cast<float*>(ring + kStages * kStageBytes) + warp * 32 * kStgPitch;
         int cur = -1;
         uint32_t t = 0;
         float inv_w = 1.f;
@@ -218,41 +216,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cur = job;
             }
             uint32_t* jh = reinterpret_cast<uint32_t*>(a.dst_base + jb.dst_off[0] + (int64_t)b * a.dst_bstride);
-            // write-out item of this lane: image row (2 rr2 + (lane >> 4)) of the warp's 8, columns 4 c4 .. 4 c4 + 3
-            const int c4 = lane & 15, ro = lane >> 4;
-            const int x = strip * kTX + 4 * c4;
+            // write-out item of this lane: image row 8 it + (lane >> 2) of a 32-row pass, output columns
+            // 16 quad + 4 cg .. + 3 (the warp's 16 columns: 64 bytes per row and plane)
+            const int cg = lane & 3, rl = lane >> 2;
+            const int x = strip * kTX + 16 * quad + 4 * cg;
             const bool xok = x < W;
             const uint32_t buf = t & 1u;
             mbar_wait(&tfull[buf], (t >> 1) & 1u);
             umma::fence_after();
-#pragma unroll 1
-            for (int qq = 0; qq < 2; ++qq) {  // 32 image rows per pass
-                const int n0 = 64 * half + 32 * qq;
-                float v[32];
-                umma::tmem_ld16(tb + lane_addr + buf * kAcc + n0, *reinterpret_cast<float(*)[16]>(v));
-                umma::tmem_ld16(tb + lane_addr + buf * kAcc + n0 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-                umma::tmem_ld_wait();
-                named_bar(1 + half, 128);  // the previous pass's reads of this half's staging are done
-                // staging [32 image rows][128 M rows (+pad)]: row-major by image row
+            float v[64];  // both 32-row passes of this warp's 64 image rows, one TMEM wait
 #pragma unroll
-                for (int j = 0; j < 32; ++j) stg[j * kStgPitch + m] = v[j];
-                named_bar(1 + half, 128);
-                // write-out: warp quad handles image rows 8 quad .. 8 quad + 7 of the 32, two per step
-                const int yq = yb * kTY + n0 + 8 * quad + ro;
-                const float* sq = stg + (8 * quad + ro) * kStgPitch + 8 * c4;
-                uint32_t* pq = jh + (int64_t)(yq + jbuf) * W + x;
+            for (int j = 0; j < 4; ++j)
+                umma::tmem_ld16(tb + lane_addr + buf * kAcc + 64 * half + 16 * j, *reinterpret_cast<float(*)[16]>(v + 16 * j));
+            umma::tmem_ld_wait();
+            umma::fence_before();
+            umma::mbar_arrive(&tempty[buf]);  // accumulator drained: the MMA may reuse it
 #pragma unroll
-                for (int rr2 = 0; rr2 < 4; ++rr2) {
-                    const int y = yq + 2 * rr2;
-                    const float4 p0 = *reinterpret_cast<const float4*>(sq + 2 * rr2 * kStgPitch);
-                    const float4 p1 = *reinterpret_cast<const float4*>(sq + 2 * rr2 * kStgPitch + 4);
+            for (int qq = 0; qq < 2; ++qq) {
+                // per-warp staging [32 image rows][32 M rows (+4)]: transposed through shared memory
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) stg[j * kStgPitch + lane] = v[32 * qq + j];
+                __syncwarp();
+                const int y0 = yb * kTY + 64 * half + 32 * qq + rl;
+                uint32_t* pq = jh + (int64_t)(y0 + jbuf) * W + x;
+#pragma unroll
+                for (int it = 0; it < 4; ++it) {
+                    const int y = y0 + 8 * it;
+                    const float* sr = stg + (rl + 8 * it) * kStgPitch + 8 * cg;
+                    const float4 p0 = *reinterpret_cast<const float4*>(sr);
+                    const float4 p1 = *reinterpret_cast<const float4*>(sr + 4);
                     uint4 hw, lw;
                     umma::split_f16x2(p0.x * inv_w, p0.y * inv_w, hw.x, lw.x);
                     umma::split_f16x2(p0.z * inv_w, p0.w * inv_w, hw.y, lw.y);
                     umma::split_f16x2(p1.x * inv_w, p1.y * inv_w, hw.z, lw.z);
                     umma::split_f16x2(p1.z * inv_w, p1.w * inv_w, hw.w, lw.w);
                     if (y < H && xok) {
-                        uint32_t* p = pq + (int64_t)(2 * rr2) * W;
+                        uint32_t* p = pq + (int64_t)(8 * it) * W;
                         *reinterpret_cast<uint4*>(p) = hw;
                         *reinterpret_cast<uint4*>(p + hpw) = lw;
                         if (y == 0 || y == H - 1) {  // replicate rows of the column pass's padding
@@ -266,8 +266,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            umma::fence_before();
-            umma::mbar_arrive(&tempty[buf]);
         }
     }
     umma::fence_before();
