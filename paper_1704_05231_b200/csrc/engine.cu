@@ -1045,7 +1045,8 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
             // (config 2, 1024^2 x 5 directs: 4 tiles per SM, FFMA rows 21 us vs 32 us per launch)
             const int64_t tiles = (int64_t)((H + 127) / 128) * ((W + 63) / 64) * (int64_t)per_f[i].size() *
                                   std::min(d.img.batch, 16);
-            if (umma_freq_used(h, (int)per_f[i].size(), H, W) && rowu_used(h, W) && tiles >= 16 * 148)
+            static const bool force = std::getenv("FGB_ROW_UMMA") != nullptr;  // tests: small images too
+            if (umma_freq_used(h, (int)per_f[i].size(), H, W) && rowu_used(h, W) && (force || tiles >= 16 * 148))
                 p.xbuf = std::max(p.xbuf, row_umma_jpad(h));
         }
     }

@@ -67,7 +67,7 @@ def test_tensor_core_kernels_are_the_ones_that_run(env):
     torch, fg, D = env
     from paper_1704_05231_b200 import _native as N
 
-    f = torch.rand((1, 256, 256), device="cuda")
+    f = torch.rand((4, 1024, 1024), device="cuda")  # >= 16 row tiles per SM: the row pass runs on the tensor cores too
     spec = fg.BankSpec((math.pi / 8, math.pi / 32), 8, (8.0, 32.0))
     N.lib.fgb_profile_enable(1)
     try:
@@ -99,6 +99,25 @@ def test_zero_and_constant_images(env):
     assert int((D.compute_bank(z, spec, fg.ExactFIR(3.0)).abs() != 0).sum()) == 0
     c = np.full((128, 192), 3.25)
     assert bank_err(fg, c, 8, spec.frequencies, spec.sigmas) <= TOL
+
+
+def test_tensor_core_rows_on_small_images():
+    """FGB_ROW_UMMA forces the tensor-core row pass below its size threshold (read once per process:
+    a subprocess) -- the parity cases above again, through row_umma's tile edges."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import math, sys; sys.path.insert(0, '.');"
+        "from tests.test_gpu_umma import bank_err; import paper_1704_05231_b200 as fg;"
+        "from tests.conftest import random_image;"
+        "cases = [(64, 64, 4, [math.pi / 4], [4.0]), (131, 200, 8, [math.pi / 4, math.pi / 8], [4.0, 8.0]),"
+        " (333, 320, 8, [math.pi / 8, math.pi / 16], [8.0, 16.0]), (97, 136, 6, [1.3, 0.4], [5.0, 11.0]),"
+        " (260, 264, 16, [math.pi / 16, math.pi / 32], [16.0, 32.0])];"
+        "errs = [bank_err(fg, random_image(H * 7 + W, H, 0.0, 1.0, width=W), N, fr, sg) for H, W, N, fr, sg in cases];"
+        "print(errs); assert max(errs) <= 1e-5"
+    )
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, FGB_ROW_UMMA="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout, r.stderr[-2000:])
 
 
 def test_ffma_kernels_behind_the_knobs():
