@@ -59,8 +59,7 @@ constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr uint32_t kAcc = 128;     // TMEM columns per accumulator
-constexpr int kStgPitch = 36;      // floats per staged row: 128 B of accumulators + 16 B (conflict-free 16-B access)
-constexpr int kStgBytes = kEpiWarps * 32 * kStgPitch * 4;
+constexpr int kStgBytes = kEpiWarps * 8192;  // output staging: 2 buffers x 2 planes x 16 rows x 128 B per warp
 
 
 // 2^e as a float for |e| <= 126 (exact)
@@ -80,11 +79,12 @@ __device__ __forceinline__ void st_cs4(float2* p, float a, float b, float c, flo
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    col_umma_kernel(const __grid_constant__ CUtensorMap jmap, const __grid_constant__ ColUArgs a) {
+    col_umma_kernel(const __grid_constant__ CUtensorMap jmap, const __grid_constant__ CUtensorMap omap,
+                    const __grid_constant__ ColUArgs a) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte aligned ring (128-byte swizzle atoms); offsets from smem_raw keep the shared state space
     uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], aready;
+    __shared__ uint64_t full[kStages], empty[kStages], tfull[3], tempty[3], aready;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = a.K, ksteps = a.K / 16, wst = (ksteps + 3) / 4;  // stages spanned by a tile's window
@@ -93,10 +93,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(&tfull[0], 1);
-        mbar_init(&tfull[1], 1);
-        mbar_init(&tempty[0], kEpiThreads);
-        mbar_init(&tempty[1], kEpiThreads);
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kEpiThreads);
+        }
         mbar_init(&aready, kEpiThreads);
     }
     if (warp == kMmaWarp) umma::tmem_alloc(&tmem_base, 512);
@@ -105,7 +105,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     umma::fence_after();
     const uint32_t tb = tmem_base;
-    const uint32_t a_hi = tb + 2 * kAcc, a_lo = a_hi + (uint32_t)(K / 2);
+    // accumulators: 3 buffers when the taps (K columns) leave room in the 512 TMEM columns, else 2
+    const uint32_t nacc = (512 - K) >= 3 * (int)kAcc ? 3u : 2u;
+    const uint32_t a_hi = tb + nacc * kAcc, a_lo = a_hi + (uint32_t)(K / 2);
     const int nunits = a.njobs * a.batch * a.nchunks * a.nstrips;
     const int chunk_rows = a.ch_tiles * kTile;
 
@@ -120,10 +122,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
                 const int Gs = nt + wst - 1;
                 const int plane = (int)(2 * (((int64_t)b * a.ws_img_c + a.jobs[job].src_off) / a.hpw));
-                const int c0 = strip * 128;
+
                 for (int q = 0; q < Gs; ++q, ++g) {
                     const uint32_t slot = g % (uint32_t)kStages, round = g / (uint32_t)kStages;
-                    mbar_wait(&empty[slot], (round & 1u) ^ 1u);
+                    if (a.spin & 1) umma::mbar_wait_spin(&empty[slot], (round & 1u) ^ 1u);
+                    else mbar_wait(&empty[slot], (round & 1u) ^ 1u);
                     uint8_t* sp = ring + slot * kStageBytes;
                     if (a.dbg & 4) {  // A/B knob: no J loads
                         umma::mbar_arrive(&full[slot]);
@@ -131,10 +134,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     mbar_arrive_expect_tx(&full[slot], kStageBytes);
                     const int rr = y0 + a.jbuf - a.jpad + kTile * q;  // buffer row (input row + jbuf)
-                    umma::tma_load_3d(sp, &jmap, c0, rr, plane, &full[slot]);
-                    umma::tma_load_3d(sp + 8192, &jmap, c0 + 64, rr, plane, &full[slot]);
-                    umma::tma_load_3d(sp + 16384, &jmap, c0, rr, plane + 1, &full[slot]);
-                    umma::tma_load_3d(sp + 24576, &jmap, c0 + 64, rr, plane + 1, &full[slot]);
+                    // strip-major planes: each 64-row stage block of a strip is 16 KB contiguous
+                    umma::tma_load_4d(sp, &jmap, 0, rr, strip, plane, &full[slot]);
+                    umma::tma_load_4d(sp + 8192, &jmap, 64, rr, strip, plane, &full[slot]);
+                    umma::tma_load_4d(sp + 16384, &jmap, 0, rr, strip, plane + 1, &full[slot]);
+                    umma::tma_load_4d(sp + 24576, &jmap, 64, rr, strip, plane + 1, &full[slot]);
                 }
             }
         }
@@ -157,8 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma::fence_after();
                 }
                 for (int i = 0; i < nt; ++i, ++t) {
-                    const uint32_t buf = t & 1u;
-                    mbar_wait(&tempty[buf], ((t >> 1) & 1u) ^ 1u);
+                    const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
+                    if (a.spin & 2) umma::mbar_wait_spin(&tempty[buf], ph ^ 1u);
+                    else mbar_wait(&tempty[buf], ph ^ 1u);
                     umma::fence_after();
                     const uint32_t d = tb + buf * kAcc;
                     // K step kk = group kk of the window: stage i + kk / 4, 16-row group kk % 4
@@ -166,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t gs = g + i + (kk >> 2);
                         const uint32_t slot = gs % (uint32_t)kStages;
                         if ((kk & 3) == 0) {
-                            mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
+                            if (a.spin & 2) umma::mbar_wait_spin(&full[slot], (gs / (uint32_t)kStages) & 1u);
+                            else mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
                             umma::fence_after();
                         }
                         const uint32_t sb = smem_u32(ring + slot * kStageBytes) + 2048u * (kk & 3);
@@ -192,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m = 32 * quad + lane;  // TMEM lane = M row
         const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
         const int r = m >> 1, odd = m & 1;
-        float* stg = reinterpret_cast<float*>(ring + kStages * kStageBytes) + warp * 32 * kStgPitch;  // [32][kStgPitch]
+        // output staging: per warp 2 buffers x (F_theta, F_pi-theta) x [16 rows][128 B] (128-byte swizzle, TMA stores)
+        uint8_t* ostg = ring + kStages * kStageBytes + warp * 8192;
         int cur = -1;
         uint32_t t = 0, gst = 0;  // tiles; the producer's ring-stage counter at the start of the unit
         int wexp = 0;
@@ -237,12 +244,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             float2* dst1 = a.dst_base + (nout > 1 ? jb.dst_off[1] : jb.dst_off[0]) + (int64_t)b * a.dst_bstride;
             const int y0 = chunk * chunk_rows;
             const int nt = min(a.ch_tiles, (a.H - y0 + kTile - 1) / kTile);
-            // read-back item of this lane: output row rloc (of the warp's 16) and 16-byte segment seg
-            const int seg = lane & 7;
             const int Gs = nt + wst - 1;
+            const int plane0 = (int)((jb.dst_off[0] + (int64_t)b * a.dst_bstride) / a.hw);
+            const int plane1 = (int)((jb.dst_off[nout > 1 ? 1 : 0] + (int64_t)b * a.dst_bstride) / a.hw);
+            const int r = lane >> 1;  // output row (of the warp's 16) of this lane's M row
             for (int i = 0; i < nt; ++i, ++t) {
-                const uint32_t buf = t & 1u;
-                mbar_wait(&tfull[buf], (t >> 1) & 1u);
+                const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
+                if (a.spin & 4) umma::mbar_wait_spin(&tfull[buf], ph);
+                else mbar_wait(&tfull[buf], ph);
                 umma::fence_after();
                 if (threadIdx.x == 0) {  // the MMAs of this tile are done: its first stage is free
                     const int rel_end = (i == nt - 1) ? Gs : i + 1;
@@ -257,36 +266,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma::fence_before();
                 umma::mbar_arrive(&tempty[buf]);  // accumulator drained: the MMA may reuse it
 #pragma unroll
-                for (int qq = 0; qq < 2; ++qq) {  // 32 accumulator columns = 16 complex per pass
-                    const int col = 64 * half + 32 * qq;
-                    // stage the raw accumulator row (A of output row r on even lanes, B on odd lanes)
-                    float4* srow = reinterpret_cast<float4*>(stg + lane * kStgPitch);
+                for (int qq = 0; qq < 2; ++qq) {  // 16 complex columns per pass
+                    uint8_t* sb = ostg + 4096 * qq;  // pass qq -> buffer qq (two TMA store groups in flight)
+                    if (lane == 0) umma::bulk_wait_read<1>();  // the store group that last read this buffer is done
                     __syncwarp();
+                    // even lane: F_theta row r = A - iB (A own, B partner); odd lane: conj(A + iB) row r
+                    uint8_t* rowp = sb + (odd ? 2048 : 0) + r * 128;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        srow[j] = make_float4(v[32 * qq + 4 * j], v[32 * qq + 4 * j + 1], v[32 * qq + 4 * j + 2], v[32 * qq + 4 * j + 3]);
-                    __syncwarp();
-                    // combine + coalesced write-out: pass k covers output rows 4k .. 4k+3 of the 16
-                    const int x = strip * 64 + col / 2 + 2 * seg;
+                    for (int c = 0; c < 8; ++c) {  // 16-byte chunk c = complex columns 2c, 2c + 1
+                        float o[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int rl = 4 * k + (lane >> 3);
-                        const float4 A = *reinterpret_cast<const float4*>(stg + (2 * rl) * kStgPitch + 4 * seg);
-                        const float4 B = *reinterpret_cast<const float4*>(stg + (2 * rl + 1) * kStgPitch + 4 * seg);
-                        const int orow = ybase + rl;
-                        if (orow < a.H && x < a.W && !(a.dbg & 1)) {
-                            const int64_t o = (int64_t)orow * a.W + x;
-                            // F_theta = A - iB; F_{pi - theta} = conj(A + iB)
-                            st_cs4(dst0 + o, (A.x + B.y) * inv, (A.y - B.x) * inv, (A.z + B.w) * inv, (A.w - B.z) * inv);
-                            if (nout > 1)
-                                st_cs4(dst1 + o, (A.x - B.y) * inv, -(A.y + B.x) * inv, (A.z - B.w) * inv,
-                                       -(A.w + B.z) * inv);
+                        for (int e = 0; e < 2; ++e) {
+                            const int k = 32 * qq + 4 * c + 2 * e;
+                            const float pr = __shfl_xor_sync(0xffffffffu, v[k], 1);
+                            const float pi = __shfl_xor_sync(0xffffffffu, v[k + 1], 1);
+                            if (!odd) {
+                                o[2 * e] = (v[k] + pi) * inv;
+                                o[2 * e + 1] = (v[k + 1] - pr) * inv;
+                            } else {
+                                o[2 * e] = (pr - v[k + 1]) * inv;
+                                o[2 * e + 1] = -(pi + v[k]) * inv;
+                            }
                         }
+                        *reinterpret_cast<float4*>(rowp + ((c ^ (r & 7)) << 4)) = make_float4(o[0], o[1], o[2], o[3]);
                     }
+                    umma::fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && !(a.dbg & 1)) {
+                        const int xf = 2 * (strip * 64 + 32 * half + 16 * qq);  // float column
+                        umma::tma_store_3d(&omap, xf, ybase, plane0, sb);
+                        if (nout > 1) umma::tma_store_3d(&omap, xf, ybase, plane1, sb + 2048);
+                    }
+                    if (lane == 0) umma::bulk_commit();
                 }
             }
             gst += Gs;
         }
+        if (lane == 0) umma::bulk_wait_read<0>();  // staging reads done before the CTA exits
     }
     umma::fence_before();
     __syncthreads();
@@ -327,29 +343,48 @@ cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cud
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     static const int dbg = std::getenv("FGB_UMMA_DBG") ? std::atoi(std::getenv("FGB_UMMA_DBG")) : 0;
-    a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no J loads); results are wrong when set
+    a.dbg = dbg;
+    static const int spin = std::getenv("FGB_UMMA_SPIN") ? std::atoi(std::getenv("FGB_UMMA_SPIN")) : 0;
+    a.spin = spin;  // A/B: spinning mbarrier waits (1 producer, 2 MMA issuer, 4 epilogue)  // A/B ablation (1 no stores, 2 no MMAs, 4 no J loads); results are wrong when set
     a.jpad = col_umma_jpad(a.h);
     a.K = kTile + 2 * a.jpad;
-    if (a.jpad > a.jbuf || a.hpw != (a.H + 2 * (int64_t)a.jbuf) * a.W) {
+    const int W64 = (a.W + 63) / 64 * 64;
+    if (a.jpad > a.jbuf || a.hpw != (a.H + 2 * (int64_t)a.jbuf) * W64) {
         std::fprintf(stderr, "col_umma: J slot layout mismatch (jpad %d jbuf %d hpw %lld)\n", a.jpad, a.jbuf,
                      (long long)a.hpw);
         return cudaErrorInvalidValue;
     }
     const int64_t Hp = a.H + 2 * (int64_t)a.jbuf;
-    // J planes: [nplanes][Hp][W] of half2 (hi plane, lo plane per job slot)
+    // J planes: [nplanes][W64 / 64 strips][Hp][128 halfs] (hi plane, lo plane per job slot)
     const int64_t plane_bytes = a.hpw * 4;
     const int64_t nplanes = ws_bytes / plane_bytes;
     CUtensorMap map;
-    cuuint64_t dims[3] = {(cuuint64_t)2 * a.W, (cuuint64_t)Hp, (cuuint64_t)nplanes};
-    cuuint64_t strides[2] = {(cuuint64_t)a.W * 4, (cuuint64_t)plane_bytes};
-    cuuint32_t box[3] = {64, kTile, 1};  // one 64-row stage block per load
-    cuuint32_t estr[3] = {1, 1, 1};
-    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint64_t dims[4] = {128, (cuuint64_t)Hp, (cuuint64_t)(W64 / 64), (cuuint64_t)nplanes};
+    cuuint64_t strides[3] = {256, (cuuint64_t)Hp * 256, (cuuint64_t)plane_bytes};
+    cuuint32_t box[4] = {64, kTile, 1, 1};  // one 64-row stage block (one of the two column blocks) per load
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, ws, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
         CUDA_SUCCESS) {
         std::fprintf(stderr, "col_umma: tensor map encode failed (W %d Hp %lld planes %lld)\n", a.W, (long long)Hp,
                      (long long)nplanes);
         return cudaErrorInvalidValue;
+    }
+    // outputs: [plane][H][W] complex64 from dst_base, stored by TMA from the swizzled staging
+    a.hw = (int64_t)a.H * a.W;
+    CUtensorMap omap;
+    {
+        cuuint64_t od[3] = {(cuuint64_t)2 * a.W, (cuuint64_t)a.H, (cuuint64_t)a.dst_planes};
+        cuuint64_t os[2] = {(cuuint64_t)a.W * 8, (cuuint64_t)a.hw * 8};
+        cuuint32_t ob[3] = {32, 16, 1};
+        if (a.dst_planes < 1 || (reinterpret_cast<uintptr_t>(a.dst_base) & 15) ||
+            enc(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.dst_base, od, os, ob, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+                CUDA_SUCCESS) {
+            std::fprintf(stderr, "col_umma: output tensor map encode failed (W %d H %d planes %lld)\n", a.W, a.H,
+                         (long long)a.dst_planes);
+            return cudaErrorInvalidValue;
+        }
     }
     // work units: strips x row chunks x images x jobs; enough units for an even last wave
     a.nstrips = (a.W + 63) / 64;
@@ -369,7 +404,7 @@ cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cud
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    col_umma_kernel<<<grid, kThreads, smem, s>>>(map, a);
+    col_umma_kernel<<<grid, kThreads, smem, s>>>(map, omap, a);
     return cudaGetLastError();
 }
 

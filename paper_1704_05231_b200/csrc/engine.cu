@@ -357,7 +357,7 @@ template <typename T> struct Plan : PlanBase {
     int H = 0, W = 0;
     int jbuf = 0;                 // > 0: J slots are split-fp16 planes with jbuf replicate rows (ST_COLU)
     int xbuf = 0;                 // > 0: some row stages run on the tensor cores (ST_ROWU) from x-padded prep planes
-    int64_t hpw = 0;              // (H + 2 jbuf) * W: complex elements per J slot (= u32 per fp16 plane)
+    int64_t hpw = 0;              // (H + 2 jbuf) * W64: complex elements per J slot (= u32 per fp16 plane)
     int chunk = 1;
     int nlanes = 1;               // concurrent stream lanes used by the steps
 
@@ -1050,7 +1050,8 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
                 p.xbuf = std::max(p.xbuf, row_umma_jpad(h));
         }
     }
-    const int64_t jslot = p.jbuf > 0 ? (int64_t)(H + 2 * p.jbuf) * W : HW;
+    // split-fp16 J slot: per plane [strip of 64 columns][H + 2 jbuf rows][64 half2] (a column strip is contiguous)
+    const int64_t jslot = p.jbuf > 0 ? (int64_t)(H + 2 * p.jbuf) * ((W + 63) / 64 * 64) : HW;
     p.hpw = jslot;
     const int64_t lane_stride = plain_fir ? max_nj * jslot : (2 * max_nj + 1) * HW;
     int64_t need = 0;
@@ -1703,6 +1704,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                         a.jbuf = p.jbuf;
                         a.njobs = st.njobs;
                         a.batch = nb;
+                        a.dst_planes = (int64_t)nb * bsC(st.dst) / ((int64_t)st.H * st.W);
                         FGB_CUDA(launch_col_umma(a, cx.ws.p, ws_img_bytes * chunk, cx.sms, s));
                     }
                     break;

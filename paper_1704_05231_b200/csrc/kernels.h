@@ -103,6 +103,9 @@ struct ColUArgs {
     int jpad, K;                // set by the launcher (jpad = h rounded up to 16 <= jbuf)
     int nstrips, nchunks, ch_tiles;
     int dbg;                    // set by the launcher from FGB_UMMA_DBG (ablation only)
+    int spin;                   // set by the launcher from FGB_UMMA_SPIN (A/B)
+    int64_t hw;                 // H * W (set by the launcher): output planes are [plane][H][W] complex
+    int64_t dst_planes;         // planes reachable from dst_base (the TMA store map spans them)
 };
 int col_umma_jpad(int h);
 bool col_umma_supported(int h, int W);
@@ -122,6 +125,7 @@ struct RowUArgs {
     int H, W, h, njobs, batch, jbuf;
     int xbuf;                   // replicate columns left / right of the image in the prep planes
     int jpad, K, nstrips, nyb;  // set by the launcher
+    int dbg;                    // FGB_UMMA_DBG (ablation only)
 };
 int row_umma_jpad(int h);
 bool row_umma_supported(int h, int W);

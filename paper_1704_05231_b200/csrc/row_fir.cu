@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
     if constexpr (sizeof(T) == 4) {
         if (a.j16) {
             // split-fp16 J for the tensor-core column pass (col_umma.cu): J 2^e = hi + lo per
-            // component, half2 (re, im) per element; the edge rows also fill the jpad pad rows
+            // component, half2 (re, im) per element, strip-major planes; the edge rows also fill the
+            // jpad pad rows
             if (xb >= a.W) return;
             const float sc = ldexpf(1.f, jscale_exp(a.maxbits[b]));
             const int r0 = y == 0 ? 0 : y + a.jpad;
@@ -219,9 +220,11 @@ __global__ void __launch_bounds__(kRowTX * kRowTY) row_sym_kernel(const __grid_c
                 uint32_t hw[R], lw[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) umma::split_f16x2(acc[k][r].x * sc, acc[k][r].y * sc, hw[r], lw[r]);
-                uint32_t* hp0 = reinterpret_cast<uint32_t*>(a.dst_base + g.dst_off[k] + (size_t)b * a.out_bstride) + xb;
+                // strip-major plane: [W / 64 strips][H + 2 jpad rows][64]
+                uint32_t* hp0 = reinterpret_cast<uint32_t*>(a.dst_base + g.dst_off[k] + (size_t)b * a.out_bstride) +
+                                (size_t)(xb >> 6) * (a.H + 2 * a.jpad) * 64 + (xb & 63);
                 for (int rr = r0; rr <= r1; ++rr) {
-                    uint32_t* ph = hp0 + (size_t)rr * a.W;
+                    uint32_t* ph = hp0 + (size_t)rr * 64;
                     *reinterpret_cast<uint4*>(ph) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                     *reinterpret_cast<uint4*>(ph + a.j16_plane) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
                 }

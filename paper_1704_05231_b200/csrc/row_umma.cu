@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     row_umma_kernel(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ RowUArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], aready;
+    __shared__ uint64_t full[kStages], empty[kStages], tfull[3], tempty[3], aready;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = a.K, ksteps = a.K / 16, kst = a.K / 64;  // ring stages per tile
@@ -98,10 +98,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(&tfull[0], 1);
-        mbar_init(&tfull[1], 1);
-        mbar_init(&tempty[0], kEpiThreads);
-        mbar_init(&tempty[1], kEpiThreads);
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kEpiThreads);
+        }
         mbar_init(&aready, kEpiThreads);
     }
     if (warp == kMmaWarp) umma::tmem_alloc(&tmem_base, 512);
@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     umma::fence_after();
     const uint32_t tb = tmem_base;
-    const uint32_t a_hi = tb + 2 * kAcc, a_lo = a_hi + (uint32_t)(K / 2);
+    // accumulators: 3 buffers when the taps (K columns) leave room in the 512 TMEM columns, else 2
+    const uint32_t nacc = (512 - K) >= 3 * (int)kAcc ? 3u : 2u;
+    const uint32_t a_hi = tb + nacc * kAcc, a_lo = a_hi + (uint32_t)(K / 2);
     const int nunits = a.njobs * a.batch * a.nyb * a.nstrips;
 
     if (warp == kTmaWarp) {
@@ -124,6 +126,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t slot = g % (uint32_t)kStages, round = g / (uint32_t)kStages;
                     mbar_wait(&empty[slot], (round & 1u) ^ 1u);
                     uint8_t* sp = ring + slot * kStageBytes;
+                    if (a.dbg & 4) {  // A/B knob: no image loads
+                        umma::mbar_arrive(&full[slot]);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[slot], kStageBytes);
                     umma::tma_load_3d(sp, &fmap, xs + 64 * q, yb * kTY, 2 * b, &full[slot]);
                     umma::tma_load_3d(sp + 16384, &fmap, xs + 64 * q, yb * kTY, 2 * b + 1, &full[slot]);
@@ -144,8 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     cur = job;
                     umma::fence_after();
                 }
-                const uint32_t buf = t & 1u;
-                mbar_wait(&tempty[buf], ((t >> 1) & 1u) ^ 1u);
+                const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
+                mbar_wait(&tempty[buf], ph ^ 1u);
                 umma::fence_after();
                 const uint32_t d = tb + buf * kAcc;
                 for (int kk = 0; kk < ksteps; ++kk) {
@@ -159,9 +165,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t sb = smem_u32(ring + slot * kStageBytes) + 32u * (kk & 3);
                     const uint64_t bh = umma::smem_desc(sb, 16, 1024, umma::kLayoutSw128);
                     const uint64_t bl = umma::smem_desc(sb + 16384, 16, 1024, umma::kLayoutSw128);
-                    umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
-                    umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
-                    umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                    if (!(a.dbg & 2)) {
+                        umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
+                        umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
+                        umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                    }
                     if ((kk & 3) == 3) umma::mma_commit(&empty[slot]);  // stage fully consumed
                 }
                 umma::mma_commit(&tfull[buf]);
@@ -219,10 +227,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             // write-out item of this lane: image row 8 it + (lane >> 2) of a 32-row pass, output columns
             // 16 quad + 4 cg .. + 3 (the warp's 16 columns: 64 bytes per row and plane)
             const int cg = lane & 3, rl = lane >> 2;
-            const int x = strip * kTX + 16 * quad + 4 * cg;
-            const bool xok = x < W;
-            const uint32_t buf = t & 1u;
-            mbar_wait(&tfull[buf], (t >> 1) & 1u);
+            const int xs = 16 * quad + 4 * cg;  // column within the strip
+            const bool xok = strip * kTX + xs < W;
+            const int Hp = H + 2 * jbuf;
+            uint32_t* js = jh + (int64_t)strip * Hp * 64 + xs;  // strip-major plane: [strip][Hp][64]
+            const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
+            mbar_wait(&tfull[buf], ph);
             umma::fence_after();
             float v[64];  // both 32-row passes of this warp's 64 image rows, one TMEM wait
 #pragma unroll
@@ -239,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = 0; j < 32; ++j) stg[j * kStgPitch + lane] = v[32 * qq + j];
                 __syncwarp();
                 const int y0 = yb * kTY + 64 * half + 32 * qq + rl;
-                uint32_t* pq = jh + (int64_t)(y0 + jbuf) * W + x;
+                uint32_t* pq = js + (int64_t)(y0 + jbuf) * 64;
 #pragma unroll
                 for (int it = 0; it < 4; ++it) {
                     const int y = y0 + 8 * it;
@@ -251,14 +261,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma::split_f16x2(p0.z * inv_w, p0.w * inv_w, hw.y, lw.y);
                     umma::split_f16x2(p1.x * inv_w, p1.y * inv_w, hw.z, lw.z);
                     umma::split_f16x2(p1.z * inv_w, p1.w * inv_w, hw.w, lw.w);
-                    if (y < H && xok) {
-                        uint32_t* p = pq + (int64_t)(8 * it) * W;
+                    if (y < H && xok && !(a.dbg & 1)) {
+                        uint32_t* p = pq + 8 * it * 64;
                         *reinterpret_cast<uint4*>(p) = hw;
                         *reinterpret_cast<uint4*>(p + hpw) = lw;
                         if (y == 0 || y == H - 1) {  // replicate rows of the column pass's padding
                             const int r0 = y == 0 ? 0 : H + jbuf, r1 = y == 0 ? jbuf : H + 2 * jbuf;
                             for (int r = r0; r < r1; ++r) {
-                                uint32_t* q = jh + (int64_t)r * W + x;
+                                uint32_t* q = js + (int64_t)r * 64;
                                 *reinterpret_cast<uint4*>(q) = hw;
                                 *reinterpret_cast<uint4*>(q + hpw) = lw;
                             }
@@ -328,6 +338,8 @@ cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstrid
 cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t s) {
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
+    static const int dbg = std::getenv("FGB_UMMA_DBG") ? std::atoi(std::getenv("FGB_UMMA_DBG")) : 0;
+    a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no image loads); results are wrong when set
     a.jpad = row_umma_jpad(a.h);
     a.K = kTX + 2 * a.jpad;
     if (a.jpad > a.xbuf || a.K > 256) return cudaErrorInvalidValue;
