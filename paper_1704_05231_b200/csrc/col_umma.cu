@@ -125,8 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
                 for (int q = 0; q < Gs; ++q, ++g) {
                     const uint32_t slot = g % (uint32_t)kStages, round = g / (uint32_t)kStages;
-                    if (a.spin & 1) umma::mbar_wait_spin(&empty[slot], (round & 1u) ^ 1u);
-                    else mbar_wait(&empty[slot], (round & 1u) ^ 1u);
+                    mbar_wait(&empty[slot], (round & 1u) ^ 1u);
                     uint8_t* sp = ring + slot * kStageBytes;
                     if (a.dbg & 4) {  // A/B knob: no J loads
                         umma::mbar_arrive(&full[slot]);
@@ -162,8 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 for (int i = 0; i < nt; ++i, ++t) {
                     const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
-                    if (a.spin & 2) umma::mbar_wait_spin(&tempty[buf], ph ^ 1u);
-                    else mbar_wait(&tempty[buf], ph ^ 1u);
+                    mbar_wait(&tempty[buf], ph ^ 1u);
                     umma::fence_after();
                     const uint32_t d = tb + buf * kAcc;
                     // K step kk = group kk of the window: stage i + kk / 4, 16-row group kk % 4
@@ -171,8 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t gs = g + i + (kk >> 2);
                         const uint32_t slot = gs % (uint32_t)kStages;
                         if ((kk & 3) == 0) {
-                            if (a.spin & 2) umma::mbar_wait_spin(&full[slot], (gs / (uint32_t)kStages) & 1u);
-                            else mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
+                            mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
                             umma::fence_after();
                         }
                         const uint32_t sb = smem_u32(ring + slot * kStageBytes) + 2048u * (kk & 3);
@@ -250,8 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int r = lane >> 1;  // output row (of the warp's 16) of this lane's M row
             for (int i = 0; i < nt; ++i, ++t) {
                 const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
-                if (a.spin & 4) umma::mbar_wait_spin(&tfull[buf], ph);
-                else mbar_wait(&tfull[buf], ph);
+                mbar_wait(&tfull[buf], ph);
                 umma::fence_after();
                 if (threadIdx.x == 0) {  // the MMAs of this tile are done: its first stage is free
                     const int rel_end = (i == nt - 1) ? Gs : i + 1;
@@ -343,9 +339,7 @@ cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cud
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     static const int dbg = std::getenv("FGB_UMMA_DBG") ? std::atoi(std::getenv("FGB_UMMA_DBG")) : 0;
-    a.dbg = dbg;
-    static const int spin = std::getenv("FGB_UMMA_SPIN") ? std::atoi(std::getenv("FGB_UMMA_SPIN")) : 0;
-    a.spin = spin;  // A/B: spinning mbarrier waits (1 producer, 2 MMA issuer, 4 epilogue)  // A/B ablation (1 no stores, 2 no MMAs, 4 no J loads); results are wrong when set
+    a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no J loads); results are wrong when set
     a.jpad = col_umma_jpad(a.h);
     a.K = kTile + 2 * a.jpad;
     const int W64 = (a.W + 63) / 64 * 64;

@@ -103,7 +103,6 @@ struct ColUArgs {
     int jpad, K;                // set by the launcher (jpad = h rounded up to 16 <= jbuf)
     int nstrips, nchunks, ch_tiles;
     int dbg;                    // set by the launcher from FGB_UMMA_DBG (ablation only)
-    int spin;                   // set by the launcher from FGB_UMMA_SPIN (A/B)
     int64_t hw;                 // H * W (set by the launcher): output planes are [plane][H][W] complex
     int64_t dst_planes;         // planes reachable from dst_base (the TMA store map spans them)
 };
