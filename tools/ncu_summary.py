@@ -7,7 +7,8 @@ WANT = ['gpu__time_duration.sum', 'sm__inst_executed_pipe_fma.avg.pct_of_peak_su
         'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'launch__grid_size', 'launch__registers_per_thread',
         'launch__occupancy_limit_registers', 'launch__occupancy_limit_shared_mem', 'sm__cycles_active.avg',
         'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 'lts__t_sectors_srcunit_tex_op_write.sum',
-        'l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum', 'lts__t_bytes.sum']
+        'l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum', 'lts__t_bytes.sum',
+        'sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed', 'lts__throughput.avg.pct_of_peak_sustained_elapsed']
 
 
 def main(path):
