@@ -268,23 +268,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     // even lane: F_theta row r = A - iB (A own, B partner); odd lane: conj(A + iB) row r
                     uint8_t* rowp = sb + (odd ? 2048 : 0) + r * 128;
+                    // step c: even lanes write chunk c, odd lanes chunk c ^ 4, so the two rows of a lane pair
+                    // (same swizzled slot, planes 2 KB apart) land in different banks
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {  // 16-byte chunk c = complex columns 2c, 2c + 1
+                    for (int c = 0; c < 8; ++c) {  // 16-byte chunk = complex columns 2 ch, 2 ch + 1
+                        const int ch = odd ? (c ^ 4) : c;
                         float o[4];
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
-                            const int k = 32 * qq + 4 * c + 2 * e;
-                            const float pr = __shfl_xor_sync(0xffffffffu, v[k], 1);
-                            const float pi = __shfl_xor_sync(0xffffffffu, v[k + 1], 1);
+                            const int ko = 32 * qq + 4 * c + 2 * e, kx = 32 * qq + 4 * (c ^ 4) + 2 * e;
+                            const float own_r = odd ? v[kx] : v[ko], own_i = odd ? v[kx + 1] : v[ko + 1];
+                            // the partner's chunk is the other one of (c, c ^ 4)
+                            const float pr = __shfl_xor_sync(0xffffffffu, odd ? v[ko] : v[kx], 1);
+                            const float pi = __shfl_xor_sync(0xffffffffu, odd ? v[ko + 1] : v[kx + 1], 1);
                             if (!odd) {
-                                o[2 * e] = (v[k] + pi) * inv;
-                                o[2 * e + 1] = (v[k + 1] - pr) * inv;
+                                o[2 * e] = (own_r + pi) * inv;
+                                o[2 * e + 1] = (own_i - pr) * inv;
                             } else {
-                                o[2 * e] = (pr - v[k + 1]) * inv;
-                                o[2 * e + 1] = -(pi + v[k]) * inv;
+                                o[2 * e] = (pr - own_i) * inv;
+                                o[2 * e + 1] = -(pi + own_r) * inv;
                             }
                         }
-                        *reinterpret_cast<float4*>(rowp + ((c ^ (r & 7)) << 4)) = make_float4(o[0], o[1], o[2], o[3]);
+                        *reinterpret_cast<float4*>(rowp + ((ch ^ (r & 7)) << 4)) = make_float4(o[0], o[1], o[2], o[3]);
                     }
                     umma::fence_async_smem();
                     __syncwarp();
