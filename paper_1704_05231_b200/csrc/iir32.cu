@@ -67,6 +67,9 @@ struct Iir32Par {
     float ccr, cci;          // complex residue
     float gr, gcr, gci;      // steady state per unit constant input: c / (1 - q)
     float wr[kM], wcr[kM], wci[kM];  // backward-start weights c q^i
+    // pass 1 of a full segment as dot products with the segment's modulated input (no recursion
+    // chain): end states e = sum_k E[k] z_k, backward-start sums b = sum_k B[k] z_k
+    float ER[kM], ECR[kM], ECI[kM], BR[kM], BCR[kM], BCI[kM];
     float Q[2][3];           // q^kM, q^mlast: (real, complex re, complex im)
     float Mb[2][9];          // b contribution of a forward carry-in (s_r, s_cr, s_ci) -> (b_r, b_cr, b_ci)
     float QS[2][3];          // the same for super-segments (the kSY segments of a CTA): q^(kSY kM), q^mlastS
@@ -439,10 +442,40 @@ __global__ void __launch_bounds__(kTX * kSY, STREAM ? 8 : 1) iir32_sum(const Iir
         float2 br = dup(0.f), bcr = dup(0.f), bci = dup(0.f);
         Sec s;
         auto run = [&](const auto& in) {
-            if (seg == 0) sec_steady(s, in.z(0), q);
-            else s.r = s.cr = s.ci = dup(0.f);
-            if (m == kM) sum_body<true>(in, i0, m, s, br, bcr, bci, q);
-            else sum_body<false>(in, i0, m, s, br, bcr, bci, q);
+            if (m == kM) {
+                // full segment: six independent dot products (FFMA2 with uniform weights)
+                float2 er = dup(0.f), ecr = dup(0.f), eci = dup(0.f);
+#pragma unroll
+                for (int i = 0; i < kM; ++i) {
+                    const float2 z = in.z(i0 + i);
+                    er = __ffma2_rn(dup(q.ER[i]), z, er);
+                    ecr = __ffma2_rn(dup(q.ECR[i]), z, ecr);
+                    eci = __ffma2_rn(dup(q.ECI[i]), z, eci);
+                    br = __ffma2_rn(dup(q.BR[i]), z, br);
+                    bcr = __ffma2_rn(dup(q.BCR[i]), z, bcr);
+                    bci = __ffma2_rn(dup(q.BCI[i]), z, bci);
+                }
+                if (seg == 0) {
+                    // the reference's steady-state init: its free response over the segment
+                    Sec s0;
+                    sec_steady(s0, in.z(0), q);
+                    const float* Q = q.Q[0];
+                    const float* M = q.Mb[0];
+                    er = __ffma2_rn(dup(Q[0]), s0.r, er);
+                    ecr = __ffma2_rn(dup(Q[1]), s0.cr, __ffma2_rn(dup(-Q[2]), s0.ci, ecr));
+                    eci = __ffma2_rn(dup(Q[1]), s0.ci, __ffma2_rn(dup(Q[2]), s0.cr, eci));
+                    br = __ffma2_rn(dup(M[0]), s0.r, __ffma2_rn(dup(M[1]), s0.cr, __ffma2_rn(dup(M[2]), s0.ci, br)));
+                    bcr = __ffma2_rn(dup(M[3]), s0.r, __ffma2_rn(dup(M[4]), s0.cr, __ffma2_rn(dup(M[5]), s0.ci, bcr)));
+                    bci = __ffma2_rn(dup(M[6]), s0.r, __ffma2_rn(dup(M[7]), s0.cr, __ffma2_rn(dup(M[8]), s0.ci, bci)));
+                }
+                s.r = er;
+                s.cr = ecr;
+                s.ci = eci;
+            } else {  // the short last segment: the recursion (rolled)
+                if (seg == 0) sec_steady(s, in.z(0), q);
+                else s.r = s.cr = s.ci = dup(0.f);
+                sum_body<false>(in, i0, m, s, br, bcr, bci, q);
+            }
         };
         if constexpr (STREAM) {
             InS<CPLX> in;
@@ -771,6 +804,27 @@ void iir32_params(const IirCoef& c, int L, Iir32Par* out) {
         p.wr[i] = (float)wr.real();
         p.wcr[i] = (float)wc.real();
         p.wci[i] = (float)wc.imag();
+    }
+    // full-segment pass-1 weights: forward impulse response g_n = c_r q_r^n + 2 Re(c_c q_c^n);
+    // E[k] = c q^(kM-1-k); B[k] = sum_{i >= k} (c q^i) g_(i-k)  (fp64, rounded once)
+    {
+        double g[kM];
+        for (int n = 0; n < kM; ++n) g[n] = (cr * std::pow(qr, n)).real() + 2.0 * (cc * std::pow(qc, n)).real();
+        for (int k = 0; k < kM; ++k) {
+            const cd er = cr * std::pow(qr, kM - 1 - k), ec = cc * std::pow(qc, kM - 1 - k);
+            p.ER[k] = (float)er.real();
+            p.ECR[k] = (float)ec.real();
+            p.ECI[k] = (float)ec.imag();
+            double br = 0.0;
+            cd bc = 0.0;
+            for (int i = k; i < kM; ++i) {
+                br += (cr * std::pow(qr, i)).real() * g[i - k];
+                bc += cc * std::pow(qc, i) * g[i - k];
+            }
+            p.BR[k] = (float)br;
+            p.BCR[k] = (float)bc.real();
+            p.BCI[k] = (float)bc.imag();
+        }
     }
     // transfer q^m and Mb of a run of m samples: segments (kM, mlast) and super-segments (kSW, mlastS)
     auto run = [&](int m, float* Q, float* Mb) {
