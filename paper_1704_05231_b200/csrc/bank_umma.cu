@@ -1,0 +1,445 @@
+// K5u: one frequency of the fp32 Gabor bank -- row AND column passes -- in one
+// tensor-core kernel, J kept in shared memory (half-widths h <= 32).
+//
+// Reference semantics: horizontal_stage -> vertical_stage(_conjugate)
+// (gabor.py:107-169, bank.py:68-74) for every direct orientation of one
+// frequency, exactly as row_umma.cu + col_umma.cu compute them (DESIGN.md
+// §4.1: banded Toeplitz products, split fp16, fp32 accumulation in TMEM), but
+// the split-fp16 J never goes to HBM: the row pass writes each 64-row J block
+// of a 64-column strip straight into a shared-memory ring in the layout the
+// column MMAs read (MN-major, 128-byte swizzle), and the column pass consumes
+// it.  HBM traffic per frequency: the image planes in, the outputs out.
+//
+// Per CTA (persistent, one per SM, 448 threads, 512 TMEM columns):
+//   warp 12  TMA producer: 64-column x 64-row boxes of the x- and y-padded
+//            split-fp16 image planes (2 per J block: K_r = 128 input columns)
+//   warp 13  TMEM allocator + MMA issuer, per unit in dependency order:
+//            row block j (8 K steps x 3 MMAs, M 128 x N 64), then column tile
+//            j - 2 (K_c / 16 steps x 3 MMAs, M 128 x N 128) once blocks
+//            j - 2 .. j are in the ring
+//   warps 8-11  row epilogue: D_row (TMEM) -> J 2^e -> fp16 hi / lo -> the
+//            ring block (the padded image rows make the column pass's
+//            replicate rows for free)
+//   warps 0-7  column epilogue (as col_umma.cu): F_theta / F_pi-theta, staged
+//            row-contiguous streaming stores
+// TMEM: D_col [0, 128), D_row x 2 [128, 256), row taps hi / lo [256, 384),
+// column taps hi / lo [384, 384 + K_c).  Work unit = (direct, image, row
+// chunk, 64-column strip), strips fastest; taps rebuilt when the direct changes.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "kernels.h"
+#include "umma.cuh"
+
+namespace fgb {
+
+namespace {
+
+constexpr int kT = 64;              // output columns per strip, rows per J block / column tile
+constexpr int kJBytes = 32768;      // J block: (hi, lo) x 2 column blocks x 64 rows x 128 B
+constexpr int kJSlots = 4;
+constexpr int kIBytes = 16384;      // image chunk: (hi, lo) x 64 rows x 128 B (64 input columns)
+constexpr int kISlots = 3;
+constexpr int kStgPitch = 36;
+constexpr int kColWarps = 8, kRowWarps = 4;
+constexpr int kRowW0 = kColWarps, kTmaWarp = kColWarps + kRowWarps, kMmaWarp = kTmaWarp + 1;
+constexpr int kThreads = 32 * (kMmaWarp + 1);
+constexpr int kColThreads = 32 * kColWarps, kRowThreads = 32 * kRowWarps;
+constexpr int kKr = 128;            // row K: 64 + 2 x 32
+constexpr int kJr = 32;             // row tap padding (h <= 32)
+constexpr uint32_t kDcol = 0, kDrow = 128, kRtap = 256, kCtap = 384;
+constexpr int kSmem = kJSlots * kJBytes + kISlots * kIBytes + kColWarps * 32 * kStgPitch * 4 + 1024;
+
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
+
+__device__ __forceinline__ void st_cs4(float2* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+struct UnitIt {
+    int u, job, b, chunk, strip;
+    __device__ void decode(const BankUArgs& a) {
+        strip = u % a.nstrips;
+        int r = u / a.nstrips;
+        chunk = r % a.nchunks;
+        r /= a.nchunks;
+        b = r % a.batch;
+        job = r / a.batch;
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    bank_umma_kernel(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ BankUArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* jring = base;
+    uint8_t* iring = base + kJSlots * kJBytes;
+    float* stg_all = reinterpret_cast<float*>(iring + kISlots * kIBytes);
+    __shared__ uint64_t ifull[kISlots], iempty[kISlots], jfull[kJSlots], jempty[kJSlots];
+    __shared__ uint64_t rfull[2], rempty[2], cfull, cempty, aready;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Kc = a.Kc, ksc = Kc / 16, jpc = a.jpc, g0 = (kT - jpc) / 16;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kISlots; ++s) {
+            mbar_init(&ifull[s], 1);
+            mbar_init(&iempty[s], 1);
+        }
+        for (int s = 0; s < kJSlots; ++s) {
+            mbar_init(&jfull[s], kRowThreads);
+            mbar_init(&jempty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&rfull[s], 1);
+            mbar_init(&rempty[s], kRowThreads);
+        }
+        mbar_init(&cfull, 1);
+        mbar_init(&cempty, kColThreads);
+        mbar_init(&aready, kColThreads + kRowThreads);
+    }
+    if (warp == kMmaWarp) umma::tmem_alloc(&tmem_base, 512);
+    if (warp == kTmaWarp && lane == 0) umma::tma_prefetch_desc(&fmap);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tb = tmem_base;
+    const int nunits = a.njobs * a.batch * a.nchunks * a.nstrips;
+    const int chunk_rows = a.ch_tiles * kT;
+    auto tiles_of = [&](int chunk) { return min(a.ch_tiles, (a.H - chunk * chunk_rows + kT - 1) / kT); };
+
+    if (warp == kTmaWarp) {
+        // ---------------- TMA producer: image chunks (64 columns x 64 rows, hi + lo) ----------------
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
+                it.decode(a);
+                const int y0 = it.chunk * chunk_rows, nb = tiles_of(it.chunk) + 2;
+                const int xs = it.strip * kT - kJr + a.xbuf;
+                for (int j = 0; j < nb; ++j)
+                    for (int kc = 0; kc < 2; ++kc, ++g) {
+                        const uint32_t slot = g % kISlots;
+                        mbar_wait(&iempty[slot], ((g / kISlots) & 1u) ^ 1u);
+                        uint8_t* sp = iring + slot * kIBytes;
+                        if (a.dbg & 4) {  // A/B knob: no image loads
+                            umma::mbar_arrive(&ifull[slot]);
+                            continue;
+                        }
+                        mbar_arrive_expect_tx(&ifull[slot], kIBytes);
+                        // J block j = J rows y0 + 64 (j - 1) .. + 63: padded-plane rows + kPadR
+                        const int row = y0 + kT * (j - 1) + kBankUPadRows;
+                        umma::tma_load_3d(sp, &fmap, xs + 64 * kc, row, 2 * it.b, &ifull[slot]);
+                        umma::tma_load_3d(sp + kIBytes / 2, &fmap, xs + 64 * kc, row, 2 * it.b + 1, &ifull[slot]);
+                    }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t idr = umma::idesc_f16_f32(128, kT, false, false);   // row: B K-major (image rows)
+            const uint32_t idc = umma::idesc_f16_f32(128, 128, false, true);   // column: B MN-major (J rows)
+            uint32_t gi = 0, gb = 0, gt = 0, nreload = 0;
+            int cur = -1;
+            for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
+                it.decode(a);
+                const int nt = tiles_of(it.chunk), nb = nt + 2;
+                if (it.job != cur) {
+                    mbar_wait(&aready, nreload & 1u);
+                    ++nreload;
+                    cur = it.job;
+                    umma::fence_after();
+                }
+                const uint32_t gbase = gb;
+                // column tile i = J blocks i .. i + 2 (window rows 64 i - jpc .. 64 i + 63 + jpc); issued three
+                // row blocks behind so the row epilogue has converted its last block by then
+                auto column = [&](int i) {
+                    mbar_wait(&cempty, (gt & 1u) ^ 1u);
+                    umma::fence_after();
+                    int seen = -1;
+                    for (int kk = 0; kk < ksc; ++kk) {
+                        const int G = g0 + kk;
+                        const uint32_t blk = gbase + i + (G >> 2);
+                        const uint32_t slot = blk % kJSlots;
+                        if ((int)blk != seen) {
+                            mbar_wait(&jfull[slot], (blk / kJSlots) & 1u);
+                            umma::fence_after();
+                            seen = (int)blk;
+                        }
+                        const uint32_t sb = smem_u32(jring + slot * kJBytes) + 2048u * (G & 3);
+                        const uint64_t bh = umma::smem_desc(sb, 8192, 1024, umma::kLayoutSw128);
+                        const uint64_t bl = umma::smem_desc(sb + kJBytes / 2, 8192, 1024, umma::kLayoutSw128);
+                        if (a.dbg & 2) continue;  // A/B knob: no MMAs
+                        umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bh, idc, kk > 0 ? 1u : 0u);
+                        umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bl, idc, 1u);
+                        umma::mma_f16_ts(tb + kDcol, tb + kCtap + Kc / 2 + 8 * kk, bh, idc, 1u);
+                    }
+                    umma::mma_commit(&cfull);  // the column epilogue also frees the J blocks this tile was the last to read
+                    ++gt;
+                };
+                for (int j = 0; j < nb; ++j) {
+                    // row block j -> D_row[gb % 2]
+                    const uint32_t rb = gb & 1u;
+                    mbar_wait(&rempty[rb], ((gb >> 1) & 1u) ^ 1u);
+                    umma::fence_after();
+                    const uint32_t d = tb + kDrow + rb * kT;
+                    for (int kc = 0; kc < 2; ++kc, ++gi) {
+                        const uint32_t slot = gi % kISlots;
+                        mbar_wait(&ifull[slot], (gi / kISlots) & 1u);
+                        umma::fence_after();
+                        const uint32_t sb = smem_u32(iring + slot * kIBytes);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int kk = 4 * kc + q;
+                            const uint64_t bh = umma::smem_desc(sb + 32u * q, 16, 1024, umma::kLayoutSw128);
+                            const uint64_t bl = umma::smem_desc(sb + kIBytes / 2 + 32u * q, 16, 1024, umma::kLayoutSw128);
+                            if (a.dbg & 2) continue;
+                            umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bh, idr, kk > 0 ? 1u : 0u);
+                            umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bl, idr, 1u);
+                            umma::mma_f16_ts(d, tb + kRtap + kKr / 2 + 8 * kk, bh, idr, 1u);
+                        }
+                    }
+                    umma::mma_commit(&rfull[rb]);  // the row epilogue also frees the block's image chunks
+                    ++gb;
+                    if (j >= 3) column(j - 3);
+                }
+                column(nt - 1);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= kRowW0) {
+        // ---------------- row epilogue (warps 8-11): D_row -> split-fp16 J block in the ring ----------------
+        const int quad = warp - kRowW0;
+        const int m = 32 * quad + lane;  // TMEM lane = M row = J half index (2 xl + re/im) of the strip
+        const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
+        const int xl = m >> 1, im = m & 1;
+        const int nblk = m >> 6, hb = (m & 63) * 2;  // column block, byte within the 128-byte row
+        uint32_t gb = 0;
+        int cur = -1;
+        float inv_r = 1.f;
+        for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
+            it.decode(a);
+            const BankUJob& jb = a.jobs[it.job];
+            if (it.job != cur) {
+                // row taps: M row m, K column k -> t = k - 32 - xl: (kr[|t|], sgn(t) ki[|t|]) 2^rexp
+                const float2* w = a.weights + jb.rofs;
+                const float wsc = pow2f(jb.rexp);
+                inv_r = pow2f(-jb.rexp);
+                for (int c = 0; c < kKr / 2; c += 16) {
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        float v[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int tt = 2 * (c + q) + e - kJr - xl;
+                            const int at = tt < 0 ? -tt : tt;
+                            float x = 0.f;
+                            if (at <= a.h) {
+                                const float2 kk = w[at];
+                                x = (im ? (tt < 0 ? -kk.y : kk.y) : kk.x) * wsc;
+                            }
+                            v[e] = x;
+                        }
+                        umma::split_f16x2(v[0], v[1], hi[q], lo[q]);
+                    }
+                    umma::tmem_st16(tb + kRtap + lane_addr + c, hi);
+                    umma::tmem_st16(tb + kRtap + kKr / 2 + lane_addr + c, lo);
+                }
+                umma::tmem_st_wait();
+                umma::fence_before();
+                umma::mbar_arrive(&aready);
+                cur = it.job;
+            }
+            const int nb = tiles_of(it.chunk) + 2;
+            for (int j = 0; j < nb; ++j, ++gb) {
+                const uint32_t rb = gb & 1u;
+                mbar_wait(&rfull[rb], (gb >> 1) & 1u);
+                umma::fence_after();
+                if (threadIdx.x == 32 * kRowW0) {  // block gb's row MMAs are done: its two image chunks are free
+                    umma::mbar_arrive(&iempty[(2 * gb) % kISlots]);
+                    umma::mbar_arrive(&iempty[(2 * gb + 1) % kISlots]);
+                }
+                float v[64];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    umma::tmem_ld16(tb + kDrow + rb * kT + lane_addr + 16 * q, *reinterpret_cast<float(*)[16]>(v + 16 * q));
+                umma::tmem_ld_wait();
+                umma::fence_before();
+                umma::mbar_arrive(&rempty[rb]);
+                const uint32_t slot = gb % kJSlots;
+                mbar_wait(&jempty[slot], ((gb / kJSlots) & 1u) ^ 1u);
+                uint8_t* jb0 = jring + slot * kJBytes + nblk * 8192;
+#pragma unroll
+                for (int r = 0; r < ((a.dbg & 8) ? 0 : kT); ++r) {
+                    const float x = v[r] * inv_r;
+                    const __half h = __float2half_rn(x);
+                    const __half l = __float2half_rn(x - __half2float(h));
+                    const int off = r * 128 + ((((hb >> 4) ^ (r & 7)) << 4) | (hb & 15));
+                    *reinterpret_cast<__half*>(jb0 + off) = h;
+                    *reinterpret_cast<__half*>(jb0 + kJBytes / 2 + off) = l;
+                }
+                umma::fence_async_smem();
+                umma::mbar_arrive(&jfull[slot]);
+            }
+        }
+    } else {
+        // ---------------- column epilogue (warps 0-7) ----------------
+        const int quad = warp & 3, half = warp >> 2;
+        const int m = 32 * quad + lane;
+        const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
+        const int r = m >> 1, odd = m & 1;
+        float* stg = stg_all + warp * 32 * kStgPitch;
+        const int seg = lane & 7;
+        uint32_t gt = 0, gbl = 0;  // tiles; J blocks before this unit
+        int cur = -1, cexp = 0;
+        for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
+            it.decode(a);
+            const BankUJob& jb = a.jobs[it.job];
+            if (it.job != cur) {
+                // column taps: M row m, K column k -> t = k - jpc - r: (odd ? kb : ka)[t] 2^cexp
+                const float2* w = a.weights + jb.cofs;
+                cexp = jb.cexp;
+                const float wsc = pow2f(cexp);
+                for (int c = 16 * half; c < Kc / 2; c += 32) {
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        float v[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int tt = 2 * (c + q) + e - jpc - r;
+                            float x = 0.f;
+                            if (tt >= -a.h && tt <= a.h) {
+                                const float2 kk = w[tt + a.h];
+                                x = (odd ? kk.y : kk.x) * wsc;
+                            }
+                            v[e] = x;
+                        }
+                        umma::split_f16x2(v[0], v[1], hi[q], lo[q]);
+                    }
+                    umma::tmem_st16(tb + kCtap + lane_addr + c, hi);
+                    umma::tmem_st16(tb + kCtap + Kc / 2 + lane_addr + c, lo);
+                }
+                umma::tmem_st_wait();
+                umma::fence_before();
+                umma::mbar_arrive(&aready);
+                cur = it.job;
+            }
+            const float inv = pow2f(-(jscale_exp(a.maxbits[it.b]) + cexp));
+            const int nout = jb.nout;
+            float2* dst0 = a.dst_base + jb.dst_off[0] + (int64_t)it.b * a.dst_bstride;
+            float2* dst1 = a.dst_base + (nout > 1 ? jb.dst_off[1] : jb.dst_off[0]) + (int64_t)it.b * a.dst_bstride;
+            const int y0 = it.chunk * chunk_rows, nt = tiles_of(it.chunk);
+            for (int i = 0; i < nt; ++i, ++gt) {
+                mbar_wait(&cfull, gt & 1u);
+                umma::fence_after();
+                if (threadIdx.x == 0) {
+                    // block i is not in tile i + 1's window; after the unit's last tile, neither are i + 1, i + 2
+                    const int rel_end = (i == nt - 1) ? i + 3 : i + 1;
+                    for (int q = i; q < rel_end; ++q) umma::mbar_arrive(&jempty[(gbl + q) % kJSlots]);
+                }
+                float v[64];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    umma::tmem_ld16(tb + kDcol + lane_addr + 64 * half + 16 * q, *reinterpret_cast<float(*)[16]>(v + 16 * q));
+                umma::tmem_ld_wait();
+                umma::fence_before();
+                umma::mbar_arrive(&cempty);
+                const int ybase = y0 + i * kT + 16 * quad;
+#pragma unroll
+                for (int qq = 0; qq < 2; ++qq) {
+                    const int col = 64 * half + 32 * qq;
+                    float4* srow = reinterpret_cast<float4*>(stg + lane * kStgPitch);
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        srow[q] = make_float4(v[32 * qq + 4 * q], v[32 * qq + 4 * q + 1], v[32 * qq + 4 * q + 2], v[32 * qq + 4 * q + 3]);
+                    __syncwarp();
+                    const int x = it.strip * kT + col / 2 + 2 * seg;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int rl = 4 * k + (lane >> 3);
+                        const float4 A = *reinterpret_cast<const float4*>(stg + (2 * rl) * kStgPitch + 4 * seg);
+                        const float4 B = *reinterpret_cast<const float4*>(stg + (2 * rl + 1) * kStgPitch + 4 * seg);
+                        const int orow = ybase + rl;
+                        if (orow < a.H && x < a.W && !(a.dbg & 1)) {
+                            const int64_t o = (int64_t)orow * a.W + x;
+                            st_cs4(dst0 + o, (A.x + B.y) * inv, (A.y - B.x) * inv, (A.z + B.w) * inv, (A.w - B.z) * inv);
+                            if (nout > 1)
+                                st_cs4(dst1 + o, (A.x - B.y) * inv, -(A.y + B.x) * inv, (A.z - B.w) * inv,
+                                       -(A.w + B.z) * inv);
+                        }
+                    }
+                }
+            }
+            gbl += nt + 2;
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) umma::tmem_dealloc(tb, 512);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (EncodeFn)p;
+    }();
+    return fn;
+}
+
+}  // namespace
+
+bool bank_umma_supported(int h, int W) {
+    return h >= 1 && h <= kJr && W % 8 == 0 && W >= kT && encode_fn() != nullptr;
+}
+
+cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream_t s) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    static const int dbg = std::getenv("FGB_UMMA_DBG") ? std::atoi(std::getenv("FGB_UMMA_DBG")) : 0;
+    a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no image loads, 8 no J conversion)
+    a.jpc = (a.h + 15) / 16 * 16;
+    a.Kc = kT + 2 * a.jpc;
+    if (a.h > kJr || a.xbuf < kJr || a.Kc > 128) return cudaErrorInvalidValue;
+    const int Wp = a.W + 2 * a.xbuf, Hq = a.H + 2 * kBankUPadRows;
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)Wp, (cuuint64_t)Hq, (cuuint64_t)2 * a.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)Wp * 2, (cuuint64_t)Wp * 2 * Hq};
+    cuuint32_t box[3] = {64, kT, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(fprep), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        std::fprintf(stderr, "bank_umma: tensor map encode failed (Wp %d Hq %d)\n", Wp, Hq);
+        return cudaErrorInvalidValue;
+    }
+    a.nstrips = (a.W + kT - 1) / kT;
+    const int ntiles = (a.H + kT - 1) / kT;
+    const int64_t basen = (int64_t)a.nstrips * a.batch * a.njobs;
+    // chunks: >= 8 tiles each (2 halo J blocks per chunk), enough units for an even last wave
+    const int nch = (int)std::min<int64_t>(std::max<int64_t>(1, (20LL * sms + basen - 1) / basen), std::max(1, ntiles / 8));
+    a.ch_tiles = (ntiles + nch - 1) / nch;
+    a.nchunks = (ntiles + a.ch_tiles - 1) / a.ch_tiles;
+    const int64_t units = basen * a.nchunks;
+    const int grid = (int)std::min<int64_t>(units, sms);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(bank_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    bank_umma_kernel<<<grid, kThreads, kSmem, s>>>(map, a);
+    return cudaGetLastError();
+}
+
+}  // namespace fgb

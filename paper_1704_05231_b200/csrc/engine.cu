@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <sstream>
@@ -296,7 +297,7 @@ struct Ref {
     int64_t off = 0;  // elements of the referenced type (T for real, C for complex)
 };
 
-enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF, ST_BANKF, ST_COLU, ST_ROWU };
+enum StepKind { ST_ROW = 0, ST_COL, ST_IIR, ST_TR_RC, ST_TR_CC, ST_TR_RR, ST_SDFTF, ST_BANKF, ST_COLU, ST_ROWU, ST_BANKU };
 
 template <typename T> struct Step {
     int kind = 0;
@@ -343,12 +344,13 @@ template <typename T> struct Plan : PlanBase {
     std::vector<T> wrow;          // row tap tables
     std::vector<C> wcol;          // column tap pairs
     std::vector<ColJob<T>> cjobs;
+    std::vector<BankUJob> bjobs;  // ST_BANKU (fp32)
     std::vector<IirJob<T>> ijobs;
     std::vector<double2> tabs;
     std::vector<int32_t> ints;
     std::vector<double> dbls;
     DevBuf blob;
-    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_ijobs = 0, off_tabs = 0, off_tabs32 = 0, off_ints = 0, off_dbls = 0;
+    size_t off_wrow = 0, off_wcol = 0, off_cjobs = 0, off_bjobs = 0, off_ijobs = 0, off_tabs = 0, off_tabs32 = 0, off_ints = 0, off_dbls = 0;
     // workspace per image (bytes), scratch (T elements per image-chunk) and chunking
     int64_t ws_img_c = 0;         // complex elements per image
     int64_t scratch_img_t = 0;    // T elements per image (IIR scratch)
@@ -356,7 +358,9 @@ template <typename T> struct Plan : PlanBase {
     int64_t out_img_c = 0;        // complex elements per output image
     int H = 0, W = 0;
     int jbuf = 0;                 // > 0: J slots are split-fp16 planes with jbuf replicate rows (ST_COLU)
-    int xbuf = 0;                 // > 0: some row stages run on the tensor cores (ST_ROWU) from x-padded prep planes
+    int xbuf = 0;                 // > 0: some row stages run on the tensor cores (ST_ROWU / ST_BANKU) from the prep planes
+    bool banku = false;           // fp32 FIR bank plan: some frequencies run as ST_BANKU (J in shared memory)
+    std::set<int> banku_h;        // their half-widths
     int64_t hpw = 0;              // (H + 2 jbuf) * W64: complex elements per J slot (= u32 per fp16 plane)
     int chunk = 1;
     int nlanes = 1;               // concurrent stream lanes used by the steps
@@ -367,6 +371,7 @@ template <typename T> struct Plan : PlanBase {
         off_wrow = o; o = al(o + wrow.size() * sizeof(T));
         off_wcol = o; o = al(o + wcol.size() * sizeof(C));
         off_cjobs = o; o = al(o + cjobs.size() * sizeof(ColJob<T>));
+        off_bjobs = o; o = al(o + bjobs.size() * sizeof(BankUJob));
         off_ijobs = o; o = al(o + ijobs.size() * sizeof(IirJob<T>));
         off_tabs = o; o = al(o + tabs.size() * sizeof(double2));
         off_tabs32 = o; o = al(o + tabs.size() * sizeof(float2));
@@ -377,6 +382,7 @@ template <typename T> struct Plan : PlanBase {
         if (!wrow.empty()) std::memcpy(h.data() + off_wrow, wrow.data(), wrow.size() * sizeof(T));
         if (!wcol.empty()) std::memcpy(h.data() + off_wcol, wcol.data(), wcol.size() * sizeof(C));
         if (!cjobs.empty()) std::memcpy(h.data() + off_cjobs, cjobs.data(), cjobs.size() * sizeof(ColJob<T>));
+        if (!bjobs.empty()) std::memcpy(h.data() + off_bjobs, bjobs.data(), bjobs.size() * sizeof(BankUJob));
         if (!ijobs.empty()) std::memcpy(h.data() + off_ijobs, ijobs.data(), ijobs.size() * sizeof(IirJob<T>));
         if (!tabs.empty()) std::memcpy(h.data() + off_tabs, tabs.data(), tabs.size() * sizeof(double2));
         for (size_t i = 0; i < tabs.size(); ++i) {  // fp32 copy (each value rounded once from the fp64 table)
@@ -391,6 +397,7 @@ template <typename T> struct Plan : PlanBase {
     const T* d_wrow() const { return (const T*)((char*)blob.p + off_wrow); }
     const C* d_wcol() const { return (const C*)((char*)blob.p + off_wcol); }
     const ColJob<T>* d_cjobs() const { return (const ColJob<T>*)((char*)blob.p + off_cjobs); }
+    const BankUJob* d_bjobs() const { return (const BankUJob*)((char*)blob.p + off_bjobs); }
     const IirJob<T>* d_ijobs() const { return (const IirJob<T>*)((char*)blob.p + off_ijobs); }
     const double2* d_tabs() const { return (const double2*)((char*)blob.p + off_tabs); }
     const float2* d_tabs32() const { return (const float2*)((char*)blob.p + off_tabs32); }
@@ -701,6 +708,14 @@ static bool umma_freq_used(int h, int nj, int H, int W) {
     return !off && h >= min_h && H >= 16 && col_umma_supported(h, W) && !fused_bank_used(h, nj, H, W);
 }
 
+// Row + column passes of one frequency in one tensor-core kernel, J in shared memory
+// (bank_umma.cu; h <= 32).  FGB_BANK_UMMA=0 keeps the separate passes.
+static bool banku_used(int h, int nj, int H, int W) {
+    static const bool off = std::getenv("FGB_BANK_UMMA") && std::atoi(std::getenv("FGB_BANK_UMMA")) == 0;
+    static const bool coloff = std::getenv("FGB_COL_FFMA") != nullptr;
+    return !off && !coloff && h >= 7 && H >= 16 && bank_umma_supported(h, W) && !fused_bank_used(h, nj, H, W);
+}
+
 // One frequency worth of Gabor work: row stage for `jobs`, column stage with
 // direct / mirrored outputs.  J planes live in ws at [ws_j0 + j*H*W].
 template <typename T>
@@ -780,6 +795,52 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
                     st.bytes = (double)H * W * sizeof(T) + (double)counted * H * W * sizeof(cx_t<T>);
                     b.push(st);
                 }
+                *ws_need = std::max(*ws_need, need - (int64_t)nj * jslot);
+                return FGB_OK;
+            }
+        }
+        // row + column passes in one tensor-core kernel (no J planes)
+        if constexpr (std::is_same<T, float>::value) {
+            if (!box && !row_only && !col_only && b.p.banku_h.count(h) && b.p.xbuf >= 32) {
+                Step<T> st;
+                st.kind = ST_BANKU;
+                st.name = "bank_umma";
+                st.H = H;
+                st.W = W;
+                st.h = h;
+                st.src = img;
+                st.dst = out;
+                st.job0 = (int)b.p.bjobs.size();
+                st.njobs = nj;
+                int counted = 0;
+                for (int j = 0; j < nj; ++j) {
+                    BankUJob q{};
+                    q.rofs = (int32_t)b.p.wcol.size();
+                    double mr = 0.0, mc = 0.0;
+                    for (int t = 0; t <= h; ++t) {
+                        const double kr = w[h + t] * std::cos(jobs[j].wc * t), ki = -w[h + t] * std::sin(jobs[j].wc * t);
+                        b.p.wcol.push_back(mk<T>((T)kr, (T)ki));
+                        mr = std::max(mr, std::max(std::fabs(kr), std::fabs(ki)));
+                    }
+                    q.cofs = b.col_weights(w, t0, jobs[j].ws);
+                    for (int qq = 0; qq < nt; ++qq)
+                        mc = std::max(mc, std::max(std::fabs((double)b.p.wcol[q.cofs + qq].x), std::fabs((double)b.p.wcol[q.cofs + qq].y)));
+                    int ex = 0;
+                    if (mr > 0.0) std::frexp(mr, &ex);
+                    q.rexp = 10 - ex;
+                    ex = 0;
+                    if (mc > 0.0) std::frexp(mc, &ex);
+                    q.cexp = 10 - ex;
+                    q.dst_off[0] = jobs[j].out_direct;
+                    q.dst_off[1] = jobs[j].out_mirror >= 0 ? jobs[j].out_mirror : jobs[j].out_direct;
+                    q.nout = jobs[j].out_mirror >= 0 ? 2 : 1;
+                    counted += q.nout;
+                    b.p.bjobs.push_back(q);
+                }
+                const double sfl = 4.0 * h + 1;
+                st.flops = ((double)nj * (2.0 * sfl + 8.0) + (double)counted * (2.0 * sfl + 12.0)) * H * W;
+                st.bytes = (double)H * W * sizeof(T) + (double)counted * H * W * sizeof(cx_t<T>);
+                b.push(st);
                 *ws_need = std::max(*ws_need, need - (int64_t)nj * jslot);
                 return FGB_OK;
             }
@@ -1034,7 +1095,18 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
         for (int i = 0; i < d.n_freq; ++i) {
             if (per_f[i].empty()) continue;
             const int h = std::max(1, (int)std::ceil(d.smoother.radius * d.sigmas[i]));
-            if (umma_freq_used(h, (int)per_f[i].size(), H, W)) p.jbuf = std::max(p.jbuf, col_umma_jpad(h));
+            // the persistent fused kernel needs >= 16 tiles (64 x 64 outputs of one direct) per SM
+            // (config 2, 1024^2 x 5 directs: 9 per SM, 168 vs 195 G px*filters/s with the separate passes)
+            const int64_t tiles = (int64_t)((H + 63) / 64) * ((W + 63) / 64) * (int64_t)per_f[i].size() *
+                                  std::min(d.img.batch, 16);
+            static const bool force = std::getenv("FGB_BANK_UMMA") && std::atoi(std::getenv("FGB_BANK_UMMA")) == 2;
+            if (banku_used(h, (int)per_f[i].size(), H, W) && (force || tiles >= 16 * 148)) {
+                p.banku = true;
+                p.banku_h.insert(h);
+                p.xbuf = std::max(p.xbuf, 32);
+            } else if (umma_freq_used(h, (int)per_f[i].size(), H, W)) {
+                p.jbuf = std::max(p.jbuf, col_umma_jpad(h));
+            }
         }
     }
     if (p.jbuf > 0) {
@@ -1046,7 +1118,8 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
             const int64_t tiles = (int64_t)((H + 127) / 128) * ((W + 63) / 64) * (int64_t)per_f[i].size() *
                                   std::min(d.img.batch, 16);
             static const bool force = std::getenv("FGB_ROW_UMMA") != nullptr;  // tests: small images too
-            if (umma_freq_used(h, (int)per_f[i].size(), H, W) && rowu_used(h, W) && (force || tiles >= 16 * 148))
+            if (!p.banku_h.count(h) && umma_freq_used(h, (int)per_f[i].size(), H, W) &&
+                rowu_used(h, W) && (force || tiles >= 16 * 148))
                 p.xbuf = std::max(p.xbuf, row_umma_jpad(h));
         }
     }
@@ -1561,7 +1634,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
     }
     if (!cx.fork_ev) FGB_CUDA(cudaEventCreateWithFlags(&cx.fork_ev, cudaEventDisableTiming));
     FGB_TRY(ws_acquire(cx, s));
-    if (p.jbuf > 0) {
+    if (p.jbuf > 0 || p.xbuf > 0) {
         FGB_TRY(cx.maxbits.ensure(sizeof(unsigned) * (size_t)chunk));
         if (p.xbuf > 0) FGB_TRY(cx.fprep.ensure(row_umma_fprep_bytes(p.H, p.W, p.xbuf, chunk)));
         if (cx.sms == 0) {
@@ -1590,7 +1663,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
         const int nb = std::min(chunk, batch - b0);
         const T* imgb = (const T*)img + (size_t)b0 * img_bs;
         if constexpr (std::is_same<T, float>::value) {
-            if (p.jbuf > 0) {  // split-fp16 J scale per image, before the lanes fork
+            if (p.jbuf > 0 || p.xbuf > 0) {  // split-fp16 J scale per image, before the lanes fork
                 ++g_launches;
                 FGB_CUDA(launch_absmax(imgb, im.pitch, img_bs, p.H, p.W, nb, (unsigned*)cx.maxbits.p, cx.sms, s));
                 if (p.xbuf > 0) {
@@ -1667,6 +1740,24 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                     a.j16_plane = p.hpw;
                     a.maxbits = (const unsigned*)cx.maxbits.p;
                     FGB_CUDA(launch_row_sym<T>(a, st.rg, knobs().row_smem_taps ? nullptr : p.wrow.data() + st.rg.wofs, s));
+                    break;
+                }
+                case ST_BANKU: {
+                    if constexpr (std::is_same<T, float>::value) {
+                        BankUArgs a{};
+                        a.jobs = p.d_bjobs() + st.job0;
+                        a.weights = p.d_wcol();
+                        a.dst_base = baseC(st.dst);
+                        a.dst_bstride = bsC(st.dst);
+                        a.maxbits = (const unsigned*)cx.maxbits.p;
+                        a.H = st.H;
+                        a.W = st.W;
+                        a.h = st.h;
+                        a.njobs = st.njobs;
+                        a.batch = nb;
+                        a.xbuf = p.xbuf;
+                        FGB_CUDA(launch_bank_umma(a, cx.fprep.p, cx.sms, s));
+                    }
                     break;
                 }
                 case ST_ROWU: {

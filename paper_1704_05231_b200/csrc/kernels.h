@@ -132,6 +132,28 @@ size_t row_umma_fprep_bytes(int H, int W, int xbuf, int batch);
 cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstride, int H, int W, int xbuf, int batch,
                                  const unsigned* maxbits, void* fprep, cudaStream_t s);
 cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t s);
+// ---- K5u: row + column passes of one frequency in one tensor-core kernel (bank_umma.cu) ----
+// J stays in shared memory.  Reads the prep planes of launch_row_umma_prep (x-padded by xbuf
+// >= 32 columns, y-padded by kBankUPadRows replicate rows); h <= 32.
+constexpr int kBankUPadRows = 64;
+struct BankUJob {
+    int32_t rofs, cofs;         // row taps (kr, ki) t = 0..h / column taps (ka, kb) t = -h..h in `weights`
+    int32_t rexp, cexp;         // tap scales 2^rexp, 2^cexp
+    int64_t dst_off[2];         // F_theta, F_pi-theta (complex elements from dst_base)
+    int32_t nout, pad_;
+};
+struct BankUArgs {
+    const BankUJob* jobs;
+    const float2* weights;
+    float2* dst_base;
+    int64_t dst_bstride;
+    const unsigned* maxbits;
+    int H, W, h, njobs, batch, xbuf;
+    int jpc, Kc, nstrips, nchunks, ch_tiles;  // set by the launcher
+    int dbg;                                  // FGB_UMMA_DBG (ablation only)
+};
+bool bank_umma_supported(int h, int W);
+cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream_t s);
 // max|f| bits per image (memset + atomicMax)
 cudaError_t launch_absmax(const float* img, int64_t pitch, int64_t bstride, int H, int W, int batch, unsigned* out,
                           int sms, cudaStream_t s);

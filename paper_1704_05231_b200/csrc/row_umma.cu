@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         continue;
                     }
                     mbar_arrive_expect_tx(&full[slot], kStageBytes);
-                    umma::tma_load_3d(sp, &fmap, xs + 64 * q, yb * kTY, 2 * b, &full[slot]);
-                    umma::tma_load_3d(sp + 16384, &fmap, xs + 64 * q, yb * kTY, 2 * b + 1, &full[slot]);
+                    const int yr = yb * kTY + kBankUPadRows;  // padded-plane row of image row yb * kTY
+                    umma::tma_load_3d(sp, &fmap, xs + 64 * q, yr, 2 * b, &full[slot]);
+                    umma::tma_load_3d(sp + 16384, &fmap, xs + 64 * q, yr, 2 * b + 1, &full[slot]);
                 }
             }
         }
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
                         umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
                     }
-                    if ((kk & 3) == 3) umma::mma_commit(&empty[slot]);  // stage fully consumed
+
                 }
                 umma::mma_commit(&tfull[buf]);
                 g += kst;
@@ -234,6 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
             mbar_wait(&tfull[buf], ph);
             umma::fence_after();
+            if (threadIdx.x == 0)  // the tile's MMAs are done: its ring stages are free (no per-stage commits)
+                for (int q = 0; q < kst; ++q) umma::mbar_arrive(&empty[(t * kst + q) % (uint32_t)kStages]);
             float v[64];  // both 32-row passes of this warp's 64 image rows, one TMEM wait
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -299,14 +302,16 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-// image -> x-padded split-fp16 planes: plane 2b = hi, 2b + 1 = lo of (f 2^e) (replicate padding)
+// image -> x- and y-padded split-fp16 planes: plane 2b = hi, 2b + 1 = lo of (f 2^e), replicate
+// padding (xbuf columns, kBankUPadRows rows on each side: plane row yp = image row yp - kBankUPadRows)
 __global__ void fprep_kernel(const float* __restrict__ img, int64_t pitch, int64_t bstride, int H, int W, int xbuf,
                              int Wp, const unsigned* __restrict__ maxbits, __half* __restrict__ out) {
-    const int b = blockIdx.z, y = blockIdx.y;
+    const int b = blockIdx.z, yp = blockIdx.y, Hq = H + 2 * kBankUPadRows;
+    const int y = min(max(yp - kBankUPadRows, 0), H - 1);
     const float sc = pow2f(jscale_exp(maxbits[b]));
     const float* row = img + (int64_t)b * bstride + (int64_t)y * pitch;
-    __half* hi = out + ((int64_t)(2 * b) * H + y) * Wp;
-    __half* lo = out + ((int64_t)(2 * b + 1) * H + y) * Wp;
+    __half* hi = out + ((int64_t)(2 * b) * Hq + yp) * Wp;
+    __half* lo = out + ((int64_t)(2 * b + 1) * Hq + yp) * Wp;
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < Wp; x += gridDim.x * blockDim.x) {
         const float v = row[min(max(x - xbuf, 0), W - 1)] * sc;
         const __half h = __float2half_rn(v);
@@ -324,13 +329,13 @@ bool row_umma_supported(int h, int W) {
 }
 
 size_t row_umma_fprep_bytes(int H, int W, int xbuf, int batch) {
-    return (size_t)batch * 2 * H * (size_t)(W + 2 * xbuf) * sizeof(__half);
+    return (size_t)batch * 2 * (H + 2 * kBankUPadRows) * (size_t)(W + 2 * xbuf) * sizeof(__half);
 }
 
 cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstride, int H, int W, int xbuf, int batch,
                                  const unsigned* maxbits, void* fprep, cudaStream_t s) {
     const int Wp = W + 2 * xbuf;
-    dim3 grid((Wp + 255) / 256, H, batch);
+    dim3 grid((Wp + 255) / 256, H + 2 * kBankUPadRows, batch);
     fprep_kernel<<<grid, 256, 0, s>>>(img, pitch, bstride, H, W, xbuf, Wp, maxbits, (__half*)fprep);
     return cudaGetLastError();
 }
@@ -345,8 +350,9 @@ cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t
     if (a.jpad > a.xbuf || a.K > 256) return cudaErrorInvalidValue;
     const int Wp = a.W + 2 * a.xbuf;
     CUtensorMap map;
-    cuuint64_t dims[3] = {(cuuint64_t)Wp, (cuuint64_t)a.H, (cuuint64_t)2 * a.batch};
-    cuuint64_t strides[2] = {(cuuint64_t)Wp * 2, (cuuint64_t)Wp * 2 * a.H};
+    const int Hq = a.H + 2 * kBankUPadRows;
+    cuuint64_t dims[3] = {(cuuint64_t)Wp, (cuuint64_t)Hq, (cuuint64_t)2 * a.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)Wp * 2, (cuuint64_t)Wp * 2 * Hq};
     cuuint32_t box[3] = {64, kTY, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(fprep), dims, strides, box, estr,

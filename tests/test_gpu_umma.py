@@ -76,7 +76,7 @@ def test_tensor_core_kernels_are_the_ones_that_run(env):
         names = {e["name"] for e in N.profile_read()}
     finally:
         N.lib.fgb_profile_enable(0)
-    assert {"row_umma", "col_umma"} <= names, names
+    assert {"row_umma", "col_umma", "bank_umma"} <= names, names  # sigma 32: two passes; sigma 8: fused
 
 
 def test_per_image_scale_in_a_batch(env):
@@ -116,6 +116,25 @@ def test_tensor_core_rows_on_small_images():
         "print(errs); assert max(errs) <= 1e-5"
     )
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, FGB_ROW_UMMA="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout, r.stderr[-2000:])
+
+
+def test_fused_tensor_core_bank_on_small_images():
+    """FGB_BANK_UMMA=2 forces the fused row + column kernel (bank_umma.cu, J in shared memory) below its
+    size threshold: tile edges, partial strips, the replicate rows of the padded image planes."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import math, sys; sys.path.insert(0, '.');"
+        "from tests.test_gpu_umma import bank_err; import paper_1704_05231_b200 as fg;"
+        "from tests.conftest import random_image;"
+        "cases = [(64, 64, 4, [math.pi / 4], [4.0]), (131, 200, 8, [math.pi / 4, math.pi / 8], [4.0, 8.0]),"
+        " (333, 320, 8, [math.pi / 8, math.pi / 3], [8.0, 10.0]), (97, 136, 6, [1.3, 0.4], [5.0, 7.0]),"
+        " (260, 264, 16, [math.pi / 16], [3.0])];"
+        "errs = [bank_err(fg, random_image(H * 7 + W, H, 0.0, 1.0, width=W), N, fr, sg) for H, W, N, fr, sg in cases];"
+        "print(errs); assert max(errs) <= 1e-5"
+    )
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, FGB_BANK_UMMA="2"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout, r.stderr[-2000:])
 
