@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == kMmaWarp) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        // ---------------- MMA issuer (the whole warp runs the loop; one elected lane issues) ----------------
+        {
             const uint32_t idr = umma::idesc_f16_f32(128, kT, false, false);   // row: B K-major (image rows)
             const uint32_t idc = umma::idesc_f16_f32(128, 128, false, true);   // column: B MN-major (J rows)
             uint32_t gi = 0, gb = 0, gt = 0, nreload = 0;
@@ -170,11 +170,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t bh = umma::smem_desc(sb, 8192, 1024, umma::kLayoutSw128);
                         const uint64_t bl = umma::smem_desc(sb + kJBytes / 2, 8192, 1024, umma::kLayoutSw128);
                         if (a.dbg & 2) continue;  // A/B knob: no MMAs
-                        umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bh, idc, kk > 0 ? 1u : 0u);
-                        umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bl, idc, 1u);
-                        umma::mma_f16_ts(tb + kDcol, tb + kCtap + Kc / 2 + 8 * kk, bh, idc, 1u);
+                        if (umma::elect_one()) {
+                            umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bh, idc, kk > 0 ? 1u : 0u);
+                            umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bl, idc, 1u);
+                            umma::mma_f16_ts(tb + kDcol, tb + kCtap + Kc / 2 + 8 * kk, bh, idc, 1u);
+                        }
+                        __syncwarp();
                     }
-                    umma::mma_commit(&cfull);  // the column epilogue also frees the J blocks this tile was the last to read
+                    if (umma::elect_one()) umma::mma_commit(&cfull);
+                    __syncwarp();  // the column epilogue also frees the J blocks this tile was the last to read
                     ++gt;
                 };
                 for (int j = 0; j < nb; ++j) {
@@ -194,12 +198,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint64_t bh = umma::smem_desc(sb + 32u * q, 16, 1024, umma::kLayoutSw128);
                             const uint64_t bl = umma::smem_desc(sb + kIBytes / 2 + 32u * q, 16, 1024, umma::kLayoutSw128);
                             if (a.dbg & 2) continue;
-                            umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bh, idr, kk > 0 ? 1u : 0u);
-                            umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bl, idr, 1u);
-                            umma::mma_f16_ts(d, tb + kRtap + kKr / 2 + 8 * kk, bh, idr, 1u);
+                            if (umma::elect_one()) {
+                                umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bh, idr, kk > 0 ? 1u : 0u);
+                                umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bl, idr, 1u);
+                                umma::mma_f16_ts(d, tb + kRtap + kKr / 2 + 8 * kk, bh, idr, 1u);
+                            }
+                            __syncwarp();
                         }
                     }
-                    umma::mma_commit(&rfull[rb]);  // the row epilogue also frees the block's image chunks
+                    if (umma::elect_one()) umma::mma_commit(&rfull[rb]);
+                    __syncwarp();  // the row epilogue also frees the block's image chunks
                     ++gb;
                     if (j >= 3) column(j - 3);
                 }

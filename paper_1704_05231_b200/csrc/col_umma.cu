@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == kMmaWarp) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        // ---------------- MMA issuer (the whole warp runs the loop; one elected lane issues) ----------------
+        {
             const uint32_t idesc = umma::idesc_f16_f32(128, 128, false, true);
             uint32_t g = 0, t = 0, nreload = 0;
             int cur = -1;
@@ -176,14 +176,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t bh = umma::smem_desc(sb, 8192, 1024, umma::kLayoutSw128);
                         const uint64_t bl = umma::smem_desc(sb + 16384, 8192, 1024, umma::kLayoutSw128);
                         if (a.dbg & 2) continue;  // A/B knob: no MMAs
-                        umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
-                        umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
-                        umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                        if (umma::elect_one()) {
+                            umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
+                            umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
+                            umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                        }
+                        __syncwarp();
                     }
                     // one commit per tile: the epilogue's first thread releases the ring stages
                     // (stage i; all the unit's remaining stages after its last tile) once it has
                     // seen this tile's accumulator complete
-                    umma::mma_commit(&tfull[buf]);
+                    if (umma::elect_one()) umma::mma_commit(&tfull[buf]);
+                    __syncwarp();
                 }
                 g += Gs;
             }

@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == kMmaWarp) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        // ---------------- MMA issuer (the whole warp runs the loop; one elected lane issues) ----------------
+        {
             const uint32_t idesc = umma::idesc_f16_f32(128, kTY, false, false);
             uint32_t g = 0, t = 0, nreload = 0;
             int cur = -1;
@@ -167,13 +167,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t bh = umma::smem_desc(sb, 16, 1024, umma::kLayoutSw128);
                     const uint64_t bl = umma::smem_desc(sb + 16384, 16, 1024, umma::kLayoutSw128);
                     if (!(a.dbg & 2)) {
-                        umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
-                        umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
-                        umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                        if (umma::elect_one()) {
+                            umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
+                            umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
+                            umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                        }
+                        __syncwarp();
                     }
 
                 }
-                umma::mma_commit(&tfull[buf]);
+                if (umma::elect_one()) umma::mma_commit(&tfull[buf]);
+                __syncwarp();
                 g += kst;
             }
         }
