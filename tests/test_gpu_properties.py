@@ -76,15 +76,23 @@ def test_config4_conjugate_symmetry_and_batch(fg):
 
 
 def test_config3_batch_equals_single_images(fg):
+    """An image's outputs do not depend on its position in a batch (bit-exact, same plan), and equal
+    the single-image call's to rounding: the kernel choice may differ with the batch size (the
+    persistent tensor-core kernels need enough tiles per SM), never the arithmetic semantics."""
     import torch
 
     cfg = bench.CONFIGS[3]
     ims = (0, 17, 63)
     imgs = torch.from_numpy(np.stack([bench.make_image(cfg, i) for i in ims])).cuda()
-    batched = _plan(fg, tuple(imgs.shape), cfg, fg.ExactFIR(3.0))(imgs)
+    plan = _plan(fg, tuple(imgs.shape), cfg, fg.ExactFIR(3.0))
+    batched = plan(imgs)
+    perm = plan(imgs[[2, 0, 1]].contiguous())
+    for j, pj in ((0, 1), (1, 2), (2, 0)):
+        assert torch.equal(batched[j], perm[pj]), j
     for j in range(len(ims)):
-        one = _plan(fg, (1, 1024, 1024), cfg, fg.ExactFIR(3.0))(imgs[j:j + 1].contiguous())
-        assert torch.equal(batched[j], one[0]), j
+        one = _plan(fg, (1, 1024, 1024), cfg, fg.ExactFIR(3.0))(imgs[j:j + 1].contiguous())[0]
+        scale = one.abs().amax()
+        assert float((batched[j] - one).abs().amax() / scale) <= 2e-6, j
 
 
 def test_constant_image_gives_the_dc_response(fg):
