@@ -12,7 +12,7 @@ import json
 import os
 import sys
 
-NAMES = {"row_umma_kernel": "row_umma", "col_umma_kernel": "col_umma", "row_sym_kernel": "row_fir", "col_kernel": "col_fir", "bank_fused_kernel": "bank_fused",
+NAMES = {"bank_umma_kernel": "bank_umma", "row_umma_kernel": "row_umma", "col_umma_kernel": "col_umma", "row_sym_kernel": "row_fir", "col_kernel": "col_fir", "bank_fused_kernel": "bank_fused",
          "sdft_fused_kernel": "sdft_fused", "iir32_": "iir", "iir_": "iir"}
 out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02", "fma_pipe.json")
 res = json.load(open(out_path)) if os.path.exists(out_path) else {}

@@ -27,4 +27,4 @@ for c in 2 4; do
     timeout 900 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/${T}_fma_c${c}i.csv python tools/run_case.py --config $c --smoother iir --iters 1 > /dev/null 2>&1; echo "fma c$c iir rc=$?"
 done
 python tools/run_case.py --config 5 --iters 1 > /dev/null 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"col_umma|row_umma" -s 2 -c 2 -o gpurun_out/${T}_full_umma_c5 python tools/run_case.py --config 5 --iters 1 > /dev/null 2>&1; echo "full umma rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"col_umma|row_umma|bank_umma" -s 2 -c 3 -o gpurun_out/${T}_full_umma_c5 python tools/run_case.py --config 5 --iters 1 > /dev/null 2>&1; echo "full umma rc=$?"

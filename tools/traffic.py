@@ -12,7 +12,7 @@ import json
 import os
 import sys
 
-NAMES = {"row_umma_kernel": "row_umma", "col_umma_kernel": "col_umma", "row_sym_kernel": "row_fir", "col_kernel": "col_fir", "bank_fused_kernel": "bank_fused",
+NAMES = {"bank_umma_kernel": "bank_umma", "row_umma_kernel": "row_umma", "col_umma_kernel": "col_umma", "row_sym_kernel": "row_fir", "col_kernel": "col_fir", "bank_fused_kernel": "bank_fused",
          "sdft_fused_kernel": "sdft_fused", "iir_": "iir", "iir32_": "iir"}
 # an IIR "launch" in bench.py is one stage (iir32_sum + iir32_fin, or the five fp64-state kernels)
 STAGE_HEADS = ("iir32_sum", "iir_fwd")
