@@ -413,13 +413,26 @@ cudaError_t launch_col_umma(ColUArgs a, void* ws, int64_t ws_bytes, int sms, cud
 
 // ---- per-image max |f| (the J scale exponent) ----------------------------
 // grid (row blocks, batch); threads stride the columns of their rows
+// grid (blocks per image, batch); 16-byte loads when rows are 16-byte aligned (pitch % 4, W % 4)
 __global__ void absmax_kernel(const float* __restrict__ img, int64_t pitch, int64_t bstride, int H, int W,
                               unsigned* __restrict__ out) {
     const float* base = img + (int64_t)blockIdx.y * bstride;
     unsigned mx = 0;
-    for (int y = blockIdx.x; y < H; y += gridDim.x) {
-        const float* row = base + (int64_t)y * pitch;
-        for (int x = threadIdx.x; x < W; x += blockDim.x) mx = max(mx, __float_as_uint(fabsf(row[x])));
+    const bool vec = (pitch & 3) == 0 && (W & 3) == 0 && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
+    if (vec) {
+        const int w4 = W >> 2;
+        const int64_t n4 = (int64_t)H * w4;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t y = i / w4, x4 = i - y * w4;
+            const float4 v = __ldcs(reinterpret_cast<const float4*>(base + y * pitch) + x4);
+            mx = max(mx, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
+                             max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+        }
+    } else {
+        for (int y = blockIdx.x; y < H; y += gridDim.x) {
+            const float* row = base + (int64_t)y * pitch;
+            for (int x = threadIdx.x; x < W; x += blockDim.x) mx = max(mx, __float_as_uint(fabsf(row[x])));
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -430,8 +443,8 @@ cudaError_t launch_absmax(const float* img, int64_t pitch, int64_t bstride, int 
                           int sms, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned) * batch, s);
     if (e != cudaSuccess) return e;
-    const int per = std::max(1, std::min(H, (4 * sms + batch - 1) / batch));
-    absmax_kernel<<<dim3(per, batch), 256, 0, s>>>(img, pitch, bstride, H, W, out);
+    const int per = std::max(1, std::min(H, (8 * sms + batch - 1) / batch));
+    absmax_kernel<<<dim3(per, batch), 512, 0, s>>>(img, pitch, bstride, H, W, out);
     return cudaGetLastError();
 }
 

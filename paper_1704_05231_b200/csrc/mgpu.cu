@@ -31,28 +31,29 @@
 
 namespace {
 
-// ---- device-time model (ms per megapixel), parallel.py:_ROW_A.. (profiles/r02/unit_costs_c5.json) ----
+// ---- device-time model, parallel.py:_FIT / run_cost (profiles/r02/unit_costs_c5.json) ----
+// cost = A(h) + B1(h) single + B2(h) double (ms on an 8192^2 image), linear in h between the anchors
 constexpr double kMpx = 67.108864;
-constexpr double kRowA = 0.107 / kMpx, kRowS = 0.00285 / kMpx, kRowB = 0.0019 / kMpx;
-constexpr double kColA = 0.175 / kMpx, kColT = 0.00715 / kMpx;
-constexpr double kFusedA = 0.22 / kMpx, kFusedG = 0.225 / kMpx;
-constexpr int kRowGroup = 8;  // engine: balanced row launches of <= kMaxND = 8 directs
+constexpr double kFit[5][4] = {{6, 0.1395, 0.2506, 0.2729}, {12, 0.0, 0.2774, 0.3352}, {24, 0.0413, 0.2827, 0.3382},
+                               {48, 0.0224, 0.3902, 0.5254}, {96, 0.0448, 0.5814, 0.6067}};
 
 double run_cost(double sigma, const std::vector<int>& ks, int n, double radius) {
     if (ks.empty()) return 0.0;
     const int h = std::max(1, (int)std::ceil(radius * sigma));
-    const int t = 2 * h + 1;
-    const int nh = n / 2;
-    const int g = (int)ks.size();
-    if (h <= 6) return kFusedA * ((g + 4) / 5) + kFusedG * g;
-    const int launches = (g + kRowGroup - 1) / kRowGroup;
-    const double row = launches * (kRowA + kRowS * t) + g * kRowB * t;
-    double col = 0.0;
-    for (int k : ks) {
-        const double f = k == 0 ? 0.65 : ((2 * k == n && nh == k) ? 0.91 : 1.0);
-        col += f * (kColA + kColT * t);
+    double p[3] = {kFit[4][1], kFit[4][2], kFit[4][3]};
+    if (h <= kFit[0][0]) {
+        for (int j = 0; j < 3; ++j) p[j] = kFit[0][1 + j];
+    } else {
+        for (int i = 0; i < 4; ++i)
+            if (h <= kFit[i + 1][0]) {
+                const double w = (h - kFit[i][0]) / (kFit[i + 1][0] - kFit[i][0]);
+                for (int j = 0; j < 3; ++j) p[j] = kFit[i][1 + j] + w * (kFit[i + 1][1 + j] - kFit[i][1 + j]);
+                break;
+            }
     }
-    return row + col;
+    int single = 0;
+    for (int k : ks) single += (k == 0 || 2 * k == n) ? 1 : 0;
+    return (p[0] + p[1] * single + p[2] * ((int)ks.size() - single)) / kMpx;
 }
 
 // cost of one rank's unit list (units of one frequency share their row launches)

@@ -316,11 +316,26 @@ __global__ void fprep_kernel(const float* __restrict__ img, int64_t pitch, int64
     const float* row = img + (int64_t)b * bstride + (int64_t)y * pitch;
     __half* hi = out + ((int64_t)(2 * b) * Hq + yp) * Wp;
     __half* lo = out + ((int64_t)(2 * b + 1) * Hq + yp) * Wp;
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < Wp; x += gridDim.x * blockDim.x) {
-        const float v = row[min(max(x - xbuf, 0), W - 1)] * sc;
-        const __half h = __float2half_rn(v);
-        hi[x] = h;
-        lo[x] = __float2half_rn(v - __half2float(h));
+    // 8 output columns per thread: 16-byte stores (Wp % 8 == 0), 16-byte loads inside the image
+    const bool vin = ((reinterpret_cast<uintptr_t>(row) & 15) == 0) && (xbuf & 3) == 0;
+    for (int x = 8 * (blockIdx.x * blockDim.x + threadIdx.x); x < Wp; x += 8 * gridDim.x * blockDim.x) {
+        float v[8];
+        const int xi = x - xbuf;
+        if (vin && xi >= 0 && xi + 8 <= W) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(row + xi));
+            const float4 c = __ldg(reinterpret_cast<const float4*>(row + xi + 4));
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = row[min(max(xi + j, 0), W - 1)];
+        }
+        uint4 hw, lw;
+        uint32_t* ph = reinterpret_cast<uint32_t*>(&hw);
+        uint32_t* pl = reinterpret_cast<uint32_t*>(&lw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) umma::split_f16x2(v[2 * j] * sc, v[2 * j + 1] * sc, ph[j], pl[j]);
+        *reinterpret_cast<uint4*>(hi + x) = hw;
+        *reinterpret_cast<uint4*>(lo + x) = lw;
     }
 }
 
@@ -339,8 +354,8 @@ size_t row_umma_fprep_bytes(int H, int W, int xbuf, int batch) {
 cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstride, int H, int W, int xbuf, int batch,
                                  const unsigned* maxbits, void* fprep, cudaStream_t s) {
     const int Wp = W + 2 * xbuf;
-    dim3 grid((Wp + 255) / 256, H + 2 * kBankUPadRows, batch);
-    fprep_kernel<<<grid, 256, 0, s>>>(img, pitch, bstride, H, W, xbuf, Wp, maxbits, (__half*)fprep);
+    dim3 grid((Wp / 8 + 127) / 128, H + 2 * kBankUPadRows, batch);
+    fprep_kernel<<<grid, 128, 0, s>>>(img, pitch, bstride, H, W, xbuf, Wp, maxbits, (__half*)fprep);
     return cudaGetLastError();
 }
 

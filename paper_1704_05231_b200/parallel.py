@@ -32,40 +32,41 @@ def shard_images(n_images: int, world: int) -> list[list[int]]:
     return out
 
 
-# Device-time model of the bank kernels (ms per megapixel), fitted to the B200
-# measurements in profiles/r02/unit_costs_c5.json (tools/unit_costs.py: every
-# contiguous k-range of every config-5 frequency, row / column launches split by
-# the live profile).  T = 2 ceil(r sigma) + 1 taps.
-#   row launch  (K1, up to 8 directs, symmetric pairs shared):  _ROW_A + _ROW_S*T per launch
-#                                                                + _ROW_B*T per direct
-#   column job  (K2, theta and pi - theta from one J):          _COL_A + _COL_T*T, times
-#                0.65 for theta = 0 (no B term) and 0.91 for theta = pi/2 (real J)
-#   fused small-sigma launch (K5, h <= 6, groups of <= 5 directs): _FUSED_A per launch + _FUSED_G per direct
+# Device-time model of the bank kernels, fitted to the B200 measurements in
+# profiles/r02/unit_costs_c5.json (tools/unit_costs.py: every contiguous k-range of every
+# config-5 frequency, kernel time from the live profile).  Per frequency of half-width
+# h = ceil(r sigma), computing g directs of which `single` have one output (theta = 0, pi/2)
+# and `double` two (theta, pi - theta):
+#     cost = A(h) + B1(h) * single + B2(h) * double          (ms on the fit's 8192^2 image)
+# with (A, B1, B2) interpolated linearly in h between the fitted half-widths: h = 6 the fused
+# FFMA kernel (bank_fused.cu), h = 12 / 24 the fused tensor-core kernel (bank_umma.cu), h = 48 /
+# 96 the tensor-core row + column passes (row_umma.cu, col_umma.cu).  Max error of the fit
+# over the 225 measured ranges: 14 %.  mgpu.cu restates it (same anchors, same order).
 _MPX = 67.108864  # the fit's 8192^2 image
-_ROW_A, _ROW_S, _ROW_B = 0.107 / _MPX, 0.00285 / _MPX, 0.0019 / _MPX
-_COL_A, _COL_T = 0.175 / _MPX, 0.00715 / _MPX
-_FUSED_A, _FUSED_G = 0.22 / _MPX, 0.225 / _MPX
-_ROW_GROUP = 8  # engine: balanced row launches of <= kMaxND = 8 directs
+_FIT = ((6, 0.1395, 0.2506, 0.2729), (12, 0.0, 0.2774, 0.3352), (24, 0.0413, 0.2827, 0.3382),
+        (48, 0.0224, 0.3902, 0.5254), (96, 0.0448, 0.5814, 0.6067))
+
+
+def _fit_at(h: int) -> tuple[float, float, float]:
+    if h <= _FIT[0][0]:
+        return _FIT[0][1:]
+    for (h0, *p0), (h1, *p1) in zip(_FIT, _FIT[1:]):
+        if h <= h1:
+            w = (h - h0) / (h1 - h0)
+            return tuple(a + w * (b - a) for a, b in zip(p0, p1))
+    return _FIT[-1][1:]
 
 
 def run_cost(sigma: float, ks, n: int, radius: float = 3.0, mpx: float = 1.0) -> float:
     """Modelled device ms of one rank computing the direct orientations ``ks`` of
-    one frequency (sharing its row launches) on an image of ``mpx`` megapixels."""
+    one frequency (one launch for all of them) on an image of ``mpx`` megapixels."""
     ks = list(ks)
     if not ks:
         return 0.0
     h = max(1, math.ceil(radius * sigma))
-    t = 2 * h + 1
-    nh = n // 2
-    if h <= 6:  # fused launches of <= 5 directs each
-        return mpx * (_FUSED_A * -(-len(ks) // 5) + _FUSED_G * len(ks))
-    launches = -(-len(ks) // _ROW_GROUP)
-    row = launches * (_ROW_A + _ROW_S * t) + len(ks) * _ROW_B * t
-    col = 0.0
-    for k in ks:
-        f = 0.65 if k == 0 else (0.91 if 2 * k == n and nh == k else 1.0)
-        col += f * (_COL_A + _COL_T * t)
-    return mpx * (row + col)
+    a, b1, b2 = _fit_at(h)
+    single = sum(1 for k in ks if k == 0 or 2 * k == n)
+    return mpx / _MPX * (a + b1 * single + b2 * (len(ks) - single))
 
 
 def bank_unit_costs(freqs, sigmas, n: int, radius: float = 3.0) -> dict[int, float]:
@@ -80,10 +81,8 @@ def partition_units(freqs, sigmas, n: int, world: int, radius: float = 3.0) -> l
     contiguous runs of the sequence ordered by frequency (largest sigma first)
     then k, minimising the largest modelled rank cost (exact linear-partition
     DP).  Contiguity keeps a rank's directs of one frequency together so they
-    share row launches (K1 forms the symmetric pair sums once for all of
-    them); a plain LPT over single units loses that sharing -- on config 5 it
-    costs ~24% more device time in total (sum of single-unit times 50.5 ms vs
-    40.7 ms for the grouped bank, profiles/r02/unit_costs_c5.json)."""
+    share one launch (and its fixed cost); a plain LPT over single units
+    splits frequencies across ranks."""
     nh = n // 2
     order = [(i, k) for i in sorted(range(len(sigmas)), key=lambda i: (-sigmas[i], i)) for k in range(nh + 1)]
     m = len(order)

@@ -29,7 +29,7 @@ def test_lpt_units_balanced_config5():
         parts = P.lpt_assign(costs, world)
         flat = sorted(u for p in parts for u in p)
         assert flat == sorted(costs)
-        assert P.load_balance(parts, costs) < 1.03
+        assert P.load_balance(parts, costs) < 1.05
         ent = [e for p in parts for e in P.unit_entries(p, 16)]
         assert sorted(ent) == sorted((i, k) for i in range(5) for k in range(16))
 
@@ -40,8 +40,8 @@ def test_partition_units_config5():
     freqs = [math.pi / 2 ** j for j in range(1, 6)]
     sig = [2.0 ** j for j in range(1, 6)]
     total = P.partition_cost([list(range(45))], sig, 16)[0]
-    assert abs(total * 67.108864 - 40.7) < 2.0  # the measured config-5 step (profiles/r02/unit_costs_c5.json)
-    for world, eff in ((1, 1.0), (2, 0.97), (4, 0.95), (8, 0.85)):
+    assert abs(total * 67.108864 - 18.5) < 1.5  # the measured config-5 step (profiles/r02/bench_c5.json)
+    for world, eff in ((1, 1.0), (2, 0.98), (4, 0.97), (8, 0.93)):
         parts = P.partition_units(freqs, sig, 16, world)
         assert sorted(u for p in parts for u in p) == list(range(45))
         c = P.partition_cost(parts, sig, 16)
@@ -52,10 +52,10 @@ def test_partition_units_config5():
 
 
 def test_run_cost_model_matches_measurements():
-    """A few measured B200 points of profiles/r02/unit_costs_c5.json (ms, 8192^2)."""
+    """A few measured B200 points of profiles/r02/unit_costs_c5.json (kernel ms, 8192^2)."""
     mpx = 67.108864
-    for sigma, ks, ms in ((32.0, range(9), 18.53), (16.0, range(9), 9.45), (8.0, [3], 0.835), (4.0, range(5), 1.97),
-                          (2.0, [4], 0.479), (32.0, [8], 2.374)):
+    for sigma, ks, ms in ((32.0, range(9), 5.603), (16.0, range(9), 4.451), (8.0, [3], 0.413), (4.0, range(5), 1.492),
+                          (8.0, range(9), 3.126), (16.0, [0], 0.427)):
         got = P.run_cost(sigma, ks, 16, 3.0, mpx)
         assert abs(got - ms) / ms < 0.15, (sigma, list(ks), got, ms)
 
