@@ -177,8 +177,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         __syncwarp();
                     }
-                    if (umma::elect_one()) umma::mma_commit(&cfull);
-                    __syncwarp();  // the column epilogue also frees the J blocks this tile was the last to read
+                    if (umma::elect_one()) {
+                        umma::mma_commit(&cfull);
+                        // J block i is not in tile i + 1's window; after the unit's last tile, neither are
+                        // i + 1, i + 2: their slots free when these MMAs complete
+                        const int rel_end = (i == nt - 1) ? i + 3 : i + 1;
+                        for (int q = i; q < rel_end; ++q) umma::mma_commit(&jempty[(gbase + q) % kJSlots]);
+                    }
+                    __syncwarp();
                     ++gt;
                 };
                 for (int j = 0; j < nb; ++j) {
@@ -205,9 +211,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             __syncwarp();
                         }
+                        // the image chunk is free once these MMAs complete
+                        if (umma::elect_one()) umma::mma_commit(&iempty[slot]);
+                        __syncwarp();
                     }
                     if (umma::elect_one()) umma::mma_commit(&rfull[rb]);
-                    __syncwarp();  // the row epilogue also frees the block's image chunks
+                    __syncwarp();
                     ++gb;
                     if (j >= 3) column(j - 3);
                 }
@@ -217,11 +226,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
     } else if (warp >= kRowW0) {
         // ---------------- row epilogue (warps 8-11): D_row -> split-fp16 J block in the ring ----------------
+        // The accumulator is read as m8n8 fragments (16x256b: thread t holds TMEM lanes t/4 and t/4 + 8,
+        // columns 2 (t%4) + {0,1} + 8k) and written with stmatrix.trans: memory row = J row (TMEM
+        // column), 16 bytes = 8 consecutive J halves (TMEM lanes) -- one instruction stores 4 swizzled
+        // 8-row matrices (hi / lo x two lane octets), conflict-free.
         const int quad = warp - kRowW0;
-        const int m = 32 * quad + lane;  // TMEM lane = M row = J half index (2 xl + re/im) of the strip
+        const int m = 32 * quad + lane;  // tap rebuild: TMEM lane = M row = J half index (2 xl + re/im)
         const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
         const int xl = m >> 1, im = m & 1;
-        const int nblk = m >> 6, hb = (m & 63) * 2;  // column block, byte within the 128-byte row
+        // stmatrix address of this thread: matrix q = lane / 8 (bit 0: lane octet +8, bit 1: lo plane),
+        // row j = lane % 8 of the 8-row group; the J half index of the matrix's first column is mq
+        const int sq = lane >> 3, sj = lane & 7;
+        uint32_t soff[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int mq = 32 * quad + 16 * hh + 8 * (sq & 1);
+            soff[hh] = (uint32_t)((sq >> 1) * (kJBytes / 2) + (mq >> 6) * 8192 + sj * 128 +
+                                  ((((mq & 63) >> 3) ^ sj) << 4));
+        }
+        const uint32_t jring_s = smem_u32(jring);
         uint32_t gb = 0;
         int cur = -1;
         float inv_r = 1.f;
@@ -264,28 +287,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t rb = gb & 1u;
                 mbar_wait(&rfull[rb], (gb >> 1) & 1u);
                 umma::fence_after();
-                if (threadIdx.x == 32 * kRowW0) {  // block gb's row MMAs are done: its two image chunks are free
-                    umma::mbar_arrive(&iempty[(2 * gb) % kISlots]);
-                    umma::mbar_arrive(&iempty[(2 * gb + 1) % kISlots]);
-                }
-                float v[64];
+                uint32_t v[2][32];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    umma::tmem_ld16(tb + kDrow + rb * kT + lane_addr + 16 * q, *reinterpret_cast<float(*)[16]>(v + 16 * q));
+                for (int hh = 0; hh < 2; ++hh)
+                    umma::tmem_ld16x256b_x8(tb + kDrow + rb * kT + ((uint32_t)(32 * quad + 16 * hh) << 16), v[hh]);
                 umma::tmem_ld_wait();
                 umma::fence_before();
                 umma::mbar_arrive(&rempty[rb]);
                 const uint32_t slot = gb % kJSlots;
                 mbar_wait(&jempty[slot], ((gb / kJSlots) & 1u) ^ 1u);
-                uint8_t* jb0 = jring + slot * kJBytes + nblk * 8192;
+                if (!(a.dbg & 8)) {
+                    const uint32_t sbase = jring_s + slot * kJBytes;
 #pragma unroll
-                for (int r = 0; r < ((a.dbg & 8) ? 0 : kT); ++r) {
-                    const float x = v[r] * inv_r;
-                    const __half h = __float2half_rn(x);
-                    const __half l = __float2half_rn(x - __half2float(h));
-                    const int off = r * 128 + ((((hb >> 4) ^ (r & 7)) << 4) | (hb & 15));
-                    *reinterpret_cast<__half*>(jb0 + off) = h;
-                    *reinterpret_cast<__half*>(jb0 + kJBytes / 2 + off) = l;
+                    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            uint32_t h0, l0, h1, l1;  // (J rows 8k + 2 (t%4) + {0,1}) of lanes t/4 and t/4 + 8
+                            umma::split_f16x2(__uint_as_float(v[hh][4 * k]) * inv_r,
+                                              __uint_as_float(v[hh][4 * k + 1]) * inv_r, h0, l0);
+                            umma::split_f16x2(__uint_as_float(v[hh][4 * k + 2]) * inv_r,
+                                              __uint_as_float(v[hh][4 * k + 3]) * inv_r, h1, l1);
+                            umma::stmatrix_x4_trans(sbase + soff[hh] + 1024u * k, h0, h1, l0, l1);
+                        }
                 }
                 umma::fence_async_smem();
                 umma::mbar_arrive(&jfull[slot]);
@@ -299,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = m >> 1, odd = m & 1;
         float* stg = stg_all + warp * 32 * kStgPitch;
         const int seg = lane & 7;
-        uint32_t gt = 0, gbl = 0;  // tiles; J blocks before this unit
+        uint32_t gt = 0;  // tiles
         int cur = -1, cexp = 0;
         for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
             it.decode(a);
@@ -342,11 +365,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < nt; ++i, ++gt) {
                 mbar_wait(&cfull, gt & 1u);
                 umma::fence_after();
-                if (threadIdx.x == 0) {
-                    // block i is not in tile i + 1's window; after the unit's last tile, neither are i + 1, i + 2
-                    const int rel_end = (i == nt - 1) ? i + 3 : i + 1;
-                    for (int q = i; q < rel_end; ++q) umma::mbar_arrive(&jempty[(gbl + q) % kJSlots]);
-                }
                 float v[64];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
@@ -381,7 +399,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            gbl += nt + 2;
         }
     }
     umma::fence_before();
