@@ -17,11 +17,14 @@
 //            row block j (8 K steps x 3 MMAs, M 128 x N 64), then column tile
 //            j - 2 (K_c / 16 steps x 3 MMAs, M 128 x N 128) once blocks
 //            j - 2 .. j are in the ring
-//   warps 8-11  row epilogue: D_row (TMEM) -> J 2^e -> fp16 hi / lo -> the
-//            ring block (the padded image rows make the column pass's
-//            replicate rows for free)
+//   warps 8-11  row epilogue: D_row (TMEM, read as m8n8 fragments) -> J 2^e ->
+//            fp16 hi / lo -> the ring block with stmatrix.trans (the padded
+//            image rows make the column pass's replicate rows for free)
 //   warps 0-7  column epilogue (as col_umma.cu): F_theta / F_pi-theta, staged
-//            row-contiguous streaming stores
+//            (XOR-swizzled) row-contiguous streaming stores
+// Image chunks and J blocks are released by tcgen05.commit from the MMA warp
+// (arrive when the MMAs that read them complete), so neither release waits on
+// an epilogue.
 // TMEM: D_col [0, 128), D_row x 2 [128, 256), row taps hi / lo [256, 384),
 // column taps hi / lo [384, 384 + K_c).  Work unit = (direct, image, row
 // chunk, 64-column strip), strips fastest; taps rebuilt when the direct changes.
@@ -41,8 +44,8 @@ constexpr int kT = 64;              // output columns per strip, rows per J bloc
 constexpr int kJBytes = 32768;      // J block: (hi, lo) x 2 column blocks x 64 rows x 128 B
 constexpr int kJSlots = 4;
 constexpr int kIBytes = 16384;      // image chunk: (hi, lo) x 64 rows x 128 B (64 input columns)
-constexpr int kISlots = 3;
-constexpr int kStgPitch = 36;
+constexpr int kISlots = 4;
+constexpr int kStgPitch = 32;     // staging rows of 8 16-byte chunks, chunk c of row r at c ^ (r & 7)
 constexpr int kColWarps = 8, kRowWarps = 4;
 constexpr int kRowW0 = kColWarps, kTmaWarp = kColWarps + kRowWarps, kMmaWarp = kTmaWarp + 1;
 constexpr int kThreads = 32 * (kMmaWarp + 1);
@@ -380,14 +383,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
-                        srow[q] = make_float4(v[32 * qq + 4 * q], v[32 * qq + 4 * q + 1], v[32 * qq + 4 * q + 2], v[32 * qq + 4 * q + 3]);
+                        srow[q ^ (lane & 7)] = make_float4(v[32 * qq + 4 * q], v[32 * qq + 4 * q + 1], v[32 * qq + 4 * q + 2], v[32 * qq + 4 * q + 3]);
                     __syncwarp();
                     const int x = it.strip * kT + col / 2 + 2 * seg;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int rl = 4 * k + (lane >> 3);
-                        const float4 A = *reinterpret_cast<const float4*>(stg + (2 * rl) * kStgPitch + 4 * seg);
-                        const float4 B = *reinterpret_cast<const float4*>(stg + (2 * rl + 1) * kStgPitch + 4 * seg);
+                        const float4 A = *reinterpret_cast<const float4*>(stg + (2 * rl) * kStgPitch + 4 * (seg ^ ((2 * rl) & 7)));
+                        const float4 B =
+                            *reinterpret_cast<const float4*>(stg + (2 * rl + 1) * kStgPitch + 4 * (seg ^ ((2 * rl + 1) & 7)));
                         const int orow = ybase + rl;
                         if (orow < a.H && x < a.W && !(a.dbg & 1)) {
                             const int64_t o = (int64_t)orow * a.W + x;

@@ -713,7 +713,7 @@ static bool umma_freq_used(int h, int nj, int H, int W) {
 static bool banku_used(int h, int nj, int H, int W) {
     static const bool off = std::getenv("FGB_BANK_UMMA") && std::atoi(std::getenv("FGB_BANK_UMMA")) == 0;
     static const bool coloff = std::getenv("FGB_COL_FFMA") != nullptr;
-    return !off && !coloff && h >= 7 && H >= 16 && bank_umma_supported(h, W) && !fused_bank_used(h, nj, H, W);
+    return !off && !coloff && H >= 16 && bank_umma_supported(h, W) && !fused_bank_used(h, nj, H, W);
 }
 
 // One frequency worth of Gabor work: row stage for `jobs`, column stage with
