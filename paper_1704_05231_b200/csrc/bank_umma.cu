@@ -20,8 +20,10 @@
 //   warps 8-11  row epilogue: D_row (TMEM, read as m8n8 fragments) -> J 2^e ->
 //            fp16 hi / lo -> the ring block with stmatrix.trans (the padded
 //            image rows make the column pass's replicate rows for free)
-//   warps 0-7  column epilogue (as col_umma.cu): F_theta / F_pi-theta, staged
-//            (XOR-swizzled) row-contiguous streaming stores
+//   warps 0-7  column epilogue: D_col read as m8n8 fragments (the ka / kb rows
+//            of an output row sit 8 TMEM lanes apart, so one thread holds both),
+//            F_theta / F_pi-theta formed in registers, streaming stores of
+//            whole 32-byte sectors per thread quad (no staging, no shuffles)
 // Image chunks and J blocks are released by tcgen05.commit from the MMA warp
 // (arrive when the MMAs that read them complete), so neither release waits on
 // an epilogue.
@@ -44,8 +46,7 @@ constexpr int kT = 64;              // output columns per strip, rows per J bloc
 constexpr int kJBytes = 32768;      // J block: (hi, lo) x 2 column blocks x 64 rows x 128 B
 constexpr int kJSlots = 4;
 constexpr int kIBytes = 16384;      // image chunk: (hi, lo) x 64 rows x 128 B (64 input columns)
-constexpr int kISlots = 4;
-constexpr int kStgPitch = 32;     // staging rows of 8 16-byte chunks, chunk c of row r at c ^ (r & 7)
+constexpr int kISlots = 6;
 constexpr int kColWarps = 8, kRowWarps = 4;
 constexpr int kRowW0 = kColWarps, kTmaWarp = kColWarps + kRowWarps, kMmaWarp = kTmaWarp + 1;
 constexpr int kThreads = 32 * (kMmaWarp + 1);
@@ -53,12 +54,12 @@ constexpr int kColThreads = 32 * kColWarps, kRowThreads = 32 * kRowWarps;
 constexpr int kKr = 128;            // row K: 64 + 2 x 32
 constexpr int kJr = 32;             // row tap padding (h <= 32)
 constexpr uint32_t kDcol = 0, kDrow = 128, kRtap = 256, kCtap = 384;
-constexpr int kSmem = kJSlots * kJBytes + kISlots * kIBytes + kColWarps * 32 * kStgPitch * 4 + 1024;
+constexpr int kSmem = kJSlots * kJBytes + kISlots * kIBytes + 1024;
 
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
 
-__device__ __forceinline__ void st_cs4(float2* p, float a, float b, float c, float d) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+__device__ __forceinline__ void st_cs2(float2* p, float a, float b) {
+    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};\n" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
 struct UnitIt {
@@ -73,18 +74,18 @@ struct UnitIt {
     }
 };
 
+template <int JPC>
 __global__ void __launch_bounds__(kThreads, 1)
     bank_umma_kernel(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ BankUArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* jring = base;
     uint8_t* iring = base + kJSlots * kJBytes;
-    float* stg_all = reinterpret_cast<float*>(iring + kISlots * kIBytes);
     __shared__ uint64_t ifull[kISlots], iempty[kISlots], jfull[kJSlots], jempty[kJSlots];
     __shared__ uint64_t rfull[2], rempty[2], cfull, cempty, aready;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int Kc = a.Kc, ksc = Kc / 16, jpc = a.jpc, g0 = (kT - jpc) / 16;
+    constexpr int Kc = kT + 2 * JPC, jpc = JPC;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kISlots; ++s) {
             mbar_init(&ifull[s], 1);
@@ -138,11 +139,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == kMmaWarp) {
-        // ---------------- MMA issuer (the whole warp runs the loop; one elected lane issues) ----------------
+        // ---------------- MMA issuer ----------------
+        // The whole warp runs the loops converged; one elect.sync lane issues a block of MMAs (the 12 of an
+        // image chunk / of a J block's 16-row groups) per elect region.  JPC is a template parameter and
+        // the shared-memory descriptors advance by constants, so a K step costs its 3 tcgen05.mma plus a
+        // few uniform adds: the issuing warp must stay well under the ~60-78 cycles an MMA executes
+        // (ncu: with ~60 instructions per K step this warp was the kernel's critical path).
         {
             const uint32_t idr = umma::idesc_f16_f32(128, kT, false, false);   // row: B K-major (image rows)
             const uint32_t idc = umma::idesc_f16_f32(128, 128, false, true);   // column: B MN-major (J rows)
-            uint32_t gi = 0, gb = 0, gt = 0, nreload = 0;
+            const uint64_t jdesc0 = umma::smem_desc(smem_u32(jring), 8192, 1024, umma::kLayoutSw128);
+            const uint64_t idesc0 = umma::smem_desc(smem_u32(iring), 16, 1024, umma::kLayoutSw128);
+            const bool do_mma = !(a.dbg & 2);  // A/B knob: no MMAs
+            uint32_t gb = 0, gt = 0, nreload = 0;
+            uint32_t islot = 0, iphase = 0;
             int cur = -1;
             for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
                 it.decode(a);
@@ -154,40 +164,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma::fence_after();
                 }
                 const uint32_t gbase = gb;
-                // column tile i = J blocks i .. i + 2 (window rows 64 i - jpc .. 64 i + 63 + jpc); issued three
-                // row blocks behind so the row epilogue has converted its last block by then
+                // column tile i = J blocks i .. i + 2 (window rows 64 i - jpc .. 64 i + 63 + jpc: 16-row groups
+                // G = g0 .. g0 + ksc - 1 of the three blocks); issued three row blocks behind so the row
+                // epilogue has converted its last block by then
                 auto column = [&](int i) {
-                    mbar_wait(&cempty, (gt & 1u) ^ 1u);
+                    if (!(a.dbg & 16)) mbar_wait(&cempty, (gt & 1u) ^ 1u);  // 16: A/B knob, as if D_col were double-buffered
                     umma::fence_after();
-                    int seen = -1;
-                    for (int kk = 0; kk < ksc; ++kk) {
-                        const int G = g0 + kk;
-                        const uint32_t blk = gbase + i + (G >> 2);
+#pragma unroll
+                    for (int bq = 0; bq < 3; ++bq) {
+                        constexpr int g0c = (kT - JPC) / 16, kscc = (kT + 2 * JPC) / 16;
+                        const int q_lo = bq == 0 ? g0c : 0;
+                        const int q_hi = g0c + kscc - 4 * bq < 4 ? g0c + kscc - 4 * bq : 4;
+                        const uint32_t blk = gbase + i + bq;
                         const uint32_t slot = blk % kJSlots;
-                        if ((int)blk != seen) {
-                            mbar_wait(&jfull[slot], (blk / kJSlots) & 1u);
-                            umma::fence_after();
-                            seen = (int)blk;
-                        }
-                        const uint32_t sb = smem_u32(jring + slot * kJBytes) + 2048u * (G & 3);
-                        const uint64_t bh = umma::smem_desc(sb, 8192, 1024, umma::kLayoutSw128);
-                        const uint64_t bl = umma::smem_desc(sb + kJBytes / 2, 8192, 1024, umma::kLayoutSw128);
-                        if (a.dbg & 2) continue;  // A/B knob: no MMAs
+                        mbar_wait(&jfull[slot], (blk / kJSlots) & 1u);
+                        umma::fence_after();
+                        const uint64_t bh0 = jdesc0 + (uint64_t)(slot * (kJBytes >> 4));
                         if (umma::elect_one()) {
-                            umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bh, idc, kk > 0 ? 1u : 0u);
-                            umma::mma_f16_ts(tb + kDcol, tb + kCtap + 8 * kk, bl, idc, 1u);
-                            umma::mma_f16_ts(tb + kDcol, tb + kCtap + Kc / 2 + 8 * kk, bh, idc, 1u);
+                            if (do_mma) {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    if (q < q_lo || q >= q_hi) continue;
+                                    const int kk = 4 * bq + q - g0c;
+                                    const uint64_t bh = bh0 + (uint64_t)(128 * q), bl = bh + (uint64_t)(kJBytes >> 5);
+                                    const uint32_t ah = tb + kCtap + 8 * kk, al = ah + (kT + 2 * JPC) / 2;
+                                    umma::mma_f16_ts(tb + kDcol, ah, bh, idc, kk > 0 ? 1u : 0u);
+                                    umma::mma_f16_ts(tb + kDcol, ah, bl, idc, 1u);
+                                    umma::mma_f16_ts(tb + kDcol, al, bh, idc, 1u);
+                                }
+                            }
+                            if (bq == 2) {
+                                umma::mma_commit(&cfull);
+                                // J block i is not in tile i + 1's window; after the unit's last tile, neither are
+                                // i + 1, i + 2: their slots free when these MMAs complete
+                                umma::mma_commit(&jempty[(gbase + i) % kJSlots]);
+                                if (i == nt - 1) {
+                                    umma::mma_commit(&jempty[(gbase + i + 1) % kJSlots]);
+                                    umma::mma_commit(&jempty[(gbase + i + 2) % kJSlots]);
+                                }
+                            }
                         }
                         __syncwarp();
                     }
-                    if (umma::elect_one()) {
-                        umma::mma_commit(&cfull);
-                        // J block i is not in tile i + 1's window; after the unit's last tile, neither are
-                        // i + 1, i + 2: their slots free when these MMAs complete
-                        const int rel_end = (i == nt - 1) ? i + 3 : i + 1;
-                        for (int q = i; q < rel_end; ++q) umma::mma_commit(&jempty[(gbase + q) % kJSlots]);
-                    }
-                    __syncwarp();
                     ++gt;
                 };
                 for (int j = 0; j < nb; ++j) {
@@ -196,30 +214,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&rempty[rb], ((gb >> 1) & 1u) ^ 1u);
                     umma::fence_after();
                     const uint32_t d = tb + kDrow + rb * kT;
-                    for (int kc = 0; kc < 2; ++kc, ++gi) {
-                        const uint32_t slot = gi % kISlots;
-                        mbar_wait(&ifull[slot], (gi / kISlots) & 1u);
-                        umma::fence_after();
-                        const uint32_t sb = smem_u32(iring + slot * kIBytes);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int kk = 4 * kc + q;
-                            const uint64_t bh = umma::smem_desc(sb + 32u * q, 16, 1024, umma::kLayoutSw128);
-                            const uint64_t bl = umma::smem_desc(sb + kIBytes / 2 + 32u * q, 16, 1024, umma::kLayoutSw128);
-                            if (a.dbg & 2) continue;
-                            if (umma::elect_one()) {
-                                umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bh, idr, kk > 0 ? 1u : 0u);
-                                umma::mma_f16_ts(d, tb + kRtap + 8 * kk, bl, idr, 1u);
-                                umma::mma_f16_ts(d, tb + kRtap + kKr / 2 + 8 * kk, bh, idr, 1u);
+                    for (int kc = 0; kc < 2; ++kc) {
+                        mbar_wait(&ifull[islot], iphase);
+                        umma::fence_after();
+                        const uint64_t bh0 = idesc0 + (uint64_t)(islot * (kIBytes >> 4));
+                        if (umma::elect_one()) {
+                            if (do_mma) {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    const int kk = 4 * kc + q;
+                                    // K-major, 128-byte swizzle: K step = 32 bytes inside the swizzle atom
+                                    const uint64_t bh = bh0 + (uint64_t)(2 * q), bl = bh + (uint64_t)(kIBytes >> 5);
+                                    const uint32_t ah = tb + kRtap + 8 * kk, al = ah + kKr / 2;
+                                    umma::mma_f16_ts(d, ah, bh, idr, kk > 0 ? 1u : 0u);
+                                    umma::mma_f16_ts(d, ah, bl, idr, 1u);
+                                    umma::mma_f16_ts(d, al, bh, idr, 1u);
+                                }
                             }
-                            __syncwarp();
+                            umma::mma_commit(&iempty[islot]);  // the image chunk is free once these MMAs complete
+                            if (kc == 1) umma::mma_commit(&rfull[rb]);
                         }
-                        // the image chunk is free once these MMAs complete
-                        if (umma::elect_one()) umma::mma_commit(&iempty[slot]);
                         __syncwarp();
+                        if (++islot == kISlots) {
+                            islot = 0;
+                            iphase ^= 1u;
+                        }
                     }
-                    if (umma::elect_one()) umma::mma_commit(&rfull[rb]);
-                    __syncwarp();
                     ++gb;
                     if (j >= 3) column(j - 3);
                 }
@@ -319,12 +340,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ---------------- column epilogue (warps 0-7) ----------------
+        // M rows are ordered so that the ka and kb rows of an output row sit 8 TMEM lanes apart: row m =
+        // 16 g + 8 odd + j holds the (odd ? kb : ka) taps of output row 8 g + j.  Read as m8n8 fragments
+        // (16x256b), thread t then holds A = (lane t / 4) and B = (lane t / 4 + 8) of the SAME output row and
+        // complex column (t % 4) + 4 k: F_theta = A - iB and F_pi-theta = conj(A + iB) are formed in
+        // registers (no shuffles, no staging) and a thread quad stores one whole 32-byte sector per row.
         const int quad = warp & 3, half = warp >> 2;
-        const int m = 32 * quad + lane;
+        const int m = 32 * quad + lane;  // tap rebuild: TMEM lane = M row
         const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
-        const int r = m >> 1, odd = m & 1;
-        float* stg = stg_all + warp * 32 * kStgPitch;
-        const int seg = lane & 7;
+        const int r = 8 * (m >> 4) + (m & 7), odd = (m >> 3) & 1;
+        const int fr = lane >> 2, fc = lane & 3;
         uint32_t gt = 0;  // tiles
         int cur = -1, cexp = 0;
         for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
@@ -362,44 +387,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const float inv = pow2f(-(jscale_exp(a.maxbits[it.b]) + cexp));
             const int nout = jb.nout;
-            float2* dst0 = a.dst_base + jb.dst_off[0] + (int64_t)it.b * a.dst_bstride;
-            float2* dst1 = a.dst_base + (nout > 1 ? jb.dst_off[1] : jb.dst_off[0]) + (int64_t)it.b * a.dst_bstride;
+            const int xb = it.strip * kT + 32 * half;  // first complex column of this warp's half
+            float2* dst0 = a.dst_base + jb.dst_off[0] + (int64_t)it.b * a.dst_bstride + xb + fc;
+            float2* dst1 = a.dst_base + (nout > 1 ? jb.dst_off[1] : jb.dst_off[0]) + (int64_t)it.b * a.dst_bstride + xb + fc;
             const int y0 = it.chunk * chunk_rows, nt = tiles_of(it.chunk);
+            const int kmax = a.dbg & 1 ? 0 : min(8, (a.W - xb + 3) >> 2);  // 4-column groups inside the image
             for (int i = 0; i < nt; ++i, ++gt) {
                 mbar_wait(&cfull, gt & 1u);
                 umma::fence_after();
-                float v[64];
+                uint32_t v[2][32];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    umma::tmem_ld16(tb + kDcol + lane_addr + 64 * half + 16 * q, *reinterpret_cast<float(*)[16]>(v + 16 * q));
+                for (int hh = 0; hh < 2; ++hh)
+                    umma::tmem_ld16x256b_x8(tb + kDcol + ((uint32_t)(32 * quad + 16 * hh) << 16) + 64 * half, v[hh]);
                 umma::tmem_ld_wait();
                 umma::fence_before();
                 umma::mbar_arrive(&cempty);
-                const int ybase = y0 + i * kT + 16 * quad;
 #pragma unroll
-                for (int qq = 0; qq < 2; ++qq) {
-                    const int col = 64 * half + 32 * qq;
-                    float4* srow = reinterpret_cast<float4*>(stg + lane * kStgPitch);
-                    __syncwarp();
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int orow = y0 + i * kT + 16 * quad + 8 * hh + fr;
+                    if (orow >= a.H) continue;
+                    const int64_t o = (int64_t)orow * a.W;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        srow[q ^ (lane & 7)] = make_float4(v[32 * qq + 4 * q], v[32 * qq + 4 * q + 1], v[32 * qq + 4 * q + 2], v[32 * qq + 4 * q + 3]);
-                    __syncwarp();
-                    const int x = it.strip * kT + col / 2 + 2 * seg;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int rl = 4 * k + (lane >> 3);
-                        const float4 A = *reinterpret_cast<const float4*>(stg + (2 * rl) * kStgPitch + 4 * (seg ^ ((2 * rl) & 7)));
-                        const float4 B =
-                            *reinterpret_cast<const float4*>(stg + (2 * rl + 1) * kStgPitch + 4 * (seg ^ ((2 * rl + 1) & 7)));
-                        const int orow = ybase + rl;
-                        if (orow < a.H && x < a.W && !(a.dbg & 1)) {
-                            const int64_t o = (int64_t)orow * a.W + x;
-                            st_cs4(dst0 + o, (A.x + B.y) * inv, (A.y - B.x) * inv, (A.z + B.w) * inv, (A.w - B.z) * inv);
-                            if (nout > 1)
-                                st_cs4(dst1 + o, (A.x - B.y) * inv, -(A.y + B.x) * inv, (A.z - B.w) * inv,
-                                       -(A.w + B.z) * inv);
-                        }
+                    for (int k = 0; k < 8; ++k) {
+                        if (k >= kmax) break;
+                        const float ar = __uint_as_float(v[hh][4 * k]), ai = __uint_as_float(v[hh][4 * k + 1]);
+                        const float br = __uint_as_float(v[hh][4 * k + 2]), bi = __uint_as_float(v[hh][4 * k + 3]);
+                        st_cs2(dst0 + o + 4 * k, (ar + bi) * inv, (ai - br) * inv);
+                        if (nout > 1) st_cs2(dst1 + o + 4 * k, (ar - bi) * inv, -(ai + br) * inv);
                     }
                 }
             }
@@ -463,11 +477,16 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
     const int grid = (int)std::min<int64_t>(units, sms);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(bank_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaError_t e = cudaFuncSetAttribute(bank_umma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(bank_umma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    bank_umma_kernel<<<grid, kThreads, kSmem, s>>>(map, a);
+    if (a.jpc == 16)
+        bank_umma_kernel<16><<<grid, kThreads, kSmem, s>>>(map, a);
+    else
+        bank_umma_kernel<32><<<grid, kThreads, kSmem, s>>>(map, a);
     return cudaGetLastError();
 }
 
