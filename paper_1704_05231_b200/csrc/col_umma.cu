@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- MMA issuer (the whole warp runs the loop; one elected lane issues) ----------------
         {
             const uint32_t idesc = umma::idesc_f16_f32(128, 128, false, true);
+            const uint64_t rdesc0 = umma::smem_desc(smem_u32(ring), 8192, 1024, umma::kLayoutSw128);
+            const bool do_mma = !(a.dbg & 2);  // A/B knob: no MMAs
             uint32_t g = 0, t = 0, nreload = 0;
             int cur = -1;
             for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -164,22 +166,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&tempty[buf], ph ^ 1u);
                     umma::fence_after();
                     const uint32_t d = tb + buf * kAcc;
-                    // K step kk = group kk of the window: stage i + kk / 4, 16-row group kk % 4
-                    for (int kk = 0; kk < ksteps; ++kk) {
-                        const uint32_t gs = g + i + (kk >> 2);
+                    // K step kk = group kk of the window: stage i + kk / 4, 16-row group kk % 4.  One elect
+                    // region per stage (<= 12 MMAs), descriptors advance by constants: the issuing warp must
+                    // stay well under the MMAs' execution time (it was the critical path at ~60
+                    // instructions per K step)
+                    for (int st = 0; st < wst; ++st) {
+                        const uint32_t gs = g + i + st;
                         const uint32_t slot = gs % (uint32_t)kStages;
-                        if ((kk & 3) == 0) {
-                            mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
-                            umma::fence_after();
-                        }
-                        const uint32_t sb = smem_u32(ring + slot * kStageBytes) + 2048u * (kk & 3);
-                        const uint64_t bh = umma::smem_desc(sb, 8192, 1024, umma::kLayoutSw128);
-                        const uint64_t bl = umma::smem_desc(sb + 16384, 8192, 1024, umma::kLayoutSw128);
-                        if (a.dbg & 2) continue;  // A/B knob: no MMAs
-                        if (umma::elect_one()) {
-                            umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
-                            umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
-                            umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                        mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
+                        umma::fence_after();
+                        const uint64_t bh0 = rdesc0 + (uint64_t)(slot * (kStageBytes >> 4));
+                        const int nq = ksteps - 4 * st;
+                        if (do_mma && umma::elect_one()) {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (q < nq) {
+                                    const uint64_t bh = bh0 + (uint64_t)(128 * q), bl = bh + (uint64_t)(16384 >> 4);
+                                    const uint32_t ah = a_hi + 8 * (4 * st + q), al = ah + (uint32_t)(K / 2);
+                                    umma::mma_f16_ts(d, ah, bh, idesc, (st | q) ? 1u : 0u);
+                                    umma::mma_f16_ts(d, ah, bl, idesc, 1u);
+                                    umma::mma_f16_ts(d, al, bh, idesc, 1u);
+                                }
+                            }
                         }
                         __syncwarp();
                     }

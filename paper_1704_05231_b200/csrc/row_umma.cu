@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ uint64_t full[kStages], empty[kStages], tfull[3], tempty[3], aready;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int K = a.K, ksteps = a.K / 16, kst = a.K / 64;  // ring stages per tile
+    const int K = a.K, kst = a.K / 64;  // ring stages per tile (K = 64 + 2 jpad, jpad a multiple of 32)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- MMA issuer (the whole warp runs the loop; one elected lane issues) ----------------
         {
             const uint32_t idesc = umma::idesc_f16_f32(128, kTY, false, false);
+            const uint64_t rdesc0 = umma::smem_desc(smem_u32(ring), 16, 1024, umma::kLayoutSw128);
+            const bool do_mma = !(a.dbg & 2);  // A/B knob: no MMAs
             uint32_t g = 0, t = 0, nreload = 0;
             int cur = -1;
             for (UnitIter it(a, nunits); it.ok(); it.next(a), ++t) {
@@ -155,26 +157,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&tempty[buf], ph ^ 1u);
                 umma::fence_after();
                 const uint32_t d = tb + buf * kAcc;
-                for (int kk = 0; kk < ksteps; ++kk) {
-                    const uint32_t gs = g + (kk >> 2);
+                // one elect region per ring stage (12 MMAs), descriptors advance by constants (K is a
+                // multiple of 64): the issuing warp stays well under the MMAs' execution time
+                for (int st = 0; st < kst; ++st) {
+                    const uint32_t gs = g + st;
                     const uint32_t slot = gs % (uint32_t)kStages;
-                    if ((kk & 3) == 0) {
-                        mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
-                        umma::fence_after();
-                    }
-                    // K-major, 128-byte swizzle: K step = 32 bytes inside the swizzle atom
-                    const uint32_t sb = smem_u32(ring + slot * kStageBytes) + 32u * (kk & 3);
-                    const uint64_t bh = umma::smem_desc(sb, 16, 1024, umma::kLayoutSw128);
-                    const uint64_t bl = umma::smem_desc(sb + 16384, 16, 1024, umma::kLayoutSw128);
-                    if (!(a.dbg & 2)) {
-                        if (umma::elect_one()) {
-                            umma::mma_f16_ts(d, a_hi + 8 * kk, bh, idesc, kk > 0 ? 1u : 0u);
-                            umma::mma_f16_ts(d, a_hi + 8 * kk, bl, idesc, 1u);
-                            umma::mma_f16_ts(d, a_lo + 8 * kk, bh, idesc, 1u);
+                    mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
+                    umma::fence_after();
+                    const uint64_t bh0 = rdesc0 + (uint64_t)(slot * (kStageBytes >> 4));
+                    if (do_mma && umma::elect_one()) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            // K-major, 128-byte swizzle: K step = 32 bytes inside the swizzle atom
+                            const uint64_t bh = bh0 + (uint64_t)(2 * q), bl = bh + (uint64_t)(16384 >> 4);
+                            const uint32_t ah = a_hi + 8 * (4 * st + q), al = ah + (uint32_t)(K / 2);
+                            umma::mma_f16_ts(d, ah, bh, idesc, (st | q) ? 1u : 0u);
+                            umma::mma_f16_ts(d, ah, bl, idesc, 1u);
+                            umma::mma_f16_ts(d, al, bh, idesc, 1u);
                         }
-                        __syncwarp();
                     }
-
+                    __syncwarp();
                 }
                 if (umma::elect_one()) umma::mma_commit(&tfull[buf]);
                 __syncwarp();
