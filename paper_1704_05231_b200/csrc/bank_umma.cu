@@ -12,23 +12,24 @@
 //
 // Per CTA (persistent, one per SM, 448 threads, 512 TMEM columns):
 //   warp 12  TMA producer: 64-column x 64-row boxes of the x- and y-padded
-//            split-fp16 image planes (2 per J block: K_r = 128 input columns)
+//            split-fp16 image planes (2 per J block: K_r <= 128 input columns)
 //   warp 13  TMEM allocator + MMA issuer, per unit in dependency order:
-//            row block j (8 K steps x 3 MMAs, M 128 x N 64), then column tile
-//            j - 2 (K_c / 16 steps x 3 MMAs, M 128 x N 128) once blocks
-//            j - 2 .. j are in the ring
+//            row block j (K_r / 16 steps x 2 MMAs: Wh [Fh | Fl] as one N = 128
+//            MMA + Wl Fh, N = 64), then column tile j - 3 (K_c / 16 steps x
+//            3 MMAs, M 128 x N 128) once blocks j - 3 .. j - 1 are in the ring
 //   warps 8-11  row epilogue: D_row (TMEM, read as m8n8 fragments) -> J 2^e ->
 //            fp16 hi / lo -> the ring block with stmatrix.trans (the padded
 //            image rows make the column pass's replicate rows for free)
 //   warps 0-7  column epilogue: D_col read as m8n8 fragments (the ka / kb rows
 //            of an output row sit 8 TMEM lanes apart, so one thread holds both),
-//            F_theta / F_pi-theta formed in registers, streaming stores of
-//            whole 32-byte sectors per thread quad (no staging, no shuffles)
+//            F_theta / F_pi-theta formed in registers (no shuffles), staged as
+//            [16 rows][128 B] boxes (128-byte swizzle) and written by TMA stores
 // Image chunks and J blocks are released by tcgen05.commit from the MMA warp
 // (arrive when the MMAs that read them complete), so neither release waits on
 // an epilogue.
-// TMEM: D_col [0, 128), D_row x 2 [128, 256), row taps hi / lo [256, 384),
-// column taps hi / lo [384, 384 + K_c).  Work unit = (direct, image, row
+// TMEM: D_col [0, 128), D_row [128, 256) (Wh Fh + Wl Fh | Wh Fl), row taps hi / lo
+// [256, 256 + K_r), column taps hi / lo [384, 384 + K_c); K_r = K_c = 64 + 2 JPC,
+// JPC = h rounded up to 16 (a template parameter: 16 or 32).  Work unit = (direct, image, row
 // chunk, 64-column strip), strips fastest; taps rebuilt when the direct changes.
 #include <algorithm>
 #include <cstdio>
@@ -46,21 +47,17 @@ constexpr int kT = 64;              // output columns per strip, rows per J bloc
 constexpr int kJBytes = 32768;      // J block: (hi, lo) x 2 column blocks x 64 rows x 128 B
 constexpr int kJSlots = 4;
 constexpr int kIBytes = 16384;      // image chunk: (hi, lo) x 64 rows x 128 B (64 input columns)
-constexpr int kISlots = 6;
+constexpr int kISlots = 4;
 constexpr int kColWarps = 8, kRowWarps = 4;
 constexpr int kRowW0 = kColWarps, kTmaWarp = kColWarps + kRowWarps, kMmaWarp = kTmaWarp + 1;
 constexpr int kThreads = 32 * (kMmaWarp + 1);
 constexpr int kColThreads = 32 * kColWarps, kRowThreads = 32 * kRowWarps;
-constexpr int kKr = 128;            // row K: 64 + 2 x 32
-constexpr int kJr = 32;             // row tap padding (h <= 32)
+constexpr int kJr = 32;             // largest row / column tap padding (h <= 32); K_r = 64 + 2 JPC
 constexpr uint32_t kDcol = 0, kDrow = 128, kRtap = 256, kCtap = 384;
-constexpr int kSmem = kJSlots * kJBytes + kISlots * kIBytes + 1024;
+constexpr int kStgBytes = 4096;      // per column-epilogue warp: 2 buffers x [16 rows][128 B] (128-byte swizzle, TMA stores)
+constexpr int kSmem = kJSlots * kJBytes + kISlots * kIBytes + kColWarps * kStgBytes + 1024;
 
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
-
-__device__ __forceinline__ void st_cs2(float2* p, float a, float b) {
-    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};\n" ::"l"(p), "f"(a), "f"(b) : "memory");
-}
 
 struct UnitIt {
     int u, job, b, chunk, strip;
@@ -76,16 +73,19 @@ struct UnitIt {
 
 template <int JPC>
 __global__ void __launch_bounds__(kThreads, 1)
-    bank_umma_kernel(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ BankUArgs a) {
+    bank_umma_kernel(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ CUtensorMap omap,
+                     const __grid_constant__ BankUArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* jring = base;
     uint8_t* iring = base + kJSlots * kJBytes;
+    uint8_t* ostg_all = iring + kISlots * kIBytes;
     __shared__ uint64_t ifull[kISlots], iempty[kISlots], jfull[kJSlots], jempty[kJSlots];
-    __shared__ uint64_t rfull[2], rempty[2], cfull, cempty, aready;
+    __shared__ uint64_t rfull, rempty, cfull, cempty, aready;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int Kc = kT + 2 * JPC, jpc = JPC;
+    constexpr int Kr = kT + 2 * JPC;  // row K: the second image chunk contributes Kr / 16 - 4 K steps
     if (threadIdx.x == 0) {
         for (int s = 0; s < kISlots; ++s) {
             mbar_init(&ifull[s], 1);
@@ -95,10 +95,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&jfull[s], kRowThreads);
             mbar_init(&jempty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&rfull[s], 1);
-            mbar_init(&rempty[s], kRowThreads);
-        }
+        mbar_init(&rfull, 1);
+        mbar_init(&rempty, kRowThreads);
         mbar_init(&cfull, 1);
         mbar_init(&cempty, kColThreads);
         mbar_init(&aready, kColThreads + kRowThreads);
@@ -120,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
                 it.decode(a);
                 const int y0 = it.chunk * chunk_rows, nb = tiles_of(it.chunk) + 2;
-                const int xs = it.strip * kT - kJr + a.xbuf;
+                const int xs = it.strip * kT - JPC + a.xbuf;
                 for (int j = 0; j < nb; ++j)
                     for (int kc = 0; kc < 2; ++kc, ++g) {
                         const uint32_t slot = g % kISlots;
@@ -147,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (ncu: with ~60 instructions per K step this warp was the kernel's critical path).
         {
             const uint32_t idr = umma::idesc_f16_f32(128, kT, false, false);   // row: B K-major (image rows)
+            const uint32_t idr2 = umma::idesc_f16_f32(128, 2 * kT, false, false);  // row: hi rows then lo rows
             const uint32_t idc = umma::idesc_f16_f32(128, 128, false, true);   // column: B MN-major (J rows)
             const uint64_t jdesc0 = umma::smem_desc(smem_u32(jring), 8192, 1024, umma::kLayoutSw128);
             const uint64_t idesc0 = umma::smem_desc(smem_u32(iring), 16, 1024, umma::kLayoutSw128);
@@ -209,11 +208,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ++gt;
                 };
                 for (int j = 0; j < nb; ++j) {
-                    // row block j -> D_row[gb % 2]
-                    const uint32_t rb = gb & 1u;
-                    mbar_wait(&rempty[rb], ((gb >> 1) & 1u) ^ 1u);
+                    // row block j -> D_row (one 128-column buffer: its drain overlaps the column tile issued
+                    // in between).  Per K step: Wh . [Fh | Fl] as ONE N = 128 MMA (the lo image rows follow the
+                    // hi rows in the chunk, so the B descriptor just runs on: columns 0-63 = Wh Fh, 64-127 =
+                    // Wh Fl, summed by the row epilogue) + Wl . Fh (N = 64) -- an N = 64 MMA costs ~60 cycles,
+                    // an N = 128 one ~78, so this is 138 instead of 180 cycles per K step
+                    mbar_wait(&rempty, (gb & 1u) ^ 1u);
                     umma::fence_after();
-                    const uint32_t d = tb + kDrow + rb * kT;
+                    const uint32_t d = tb + kDrow;
 #pragma unroll
                     for (int kc = 0; kc < 2; ++kc) {
                         mbar_wait(&ifull[islot], iphase);
@@ -224,16 +226,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                                 for (int q = 0; q < 4; ++q) {
                                     const int kk = 4 * kc + q;
+                                    if (kk >= Kr / 16) continue;
                                     // K-major, 128-byte swizzle: K step = 32 bytes inside the swizzle atom
-                                    const uint64_t bh = bh0 + (uint64_t)(2 * q), bl = bh + (uint64_t)(kIBytes >> 5);
-                                    const uint32_t ah = tb + kRtap + 8 * kk, al = ah + kKr / 2;
-                                    umma::mma_f16_ts(d, ah, bh, idr, kk > 0 ? 1u : 0u);
-                                    umma::mma_f16_ts(d, ah, bl, idr, 1u);
+                                    const uint64_t bh = bh0 + (uint64_t)(2 * q);
+                                    const uint32_t ah = tb + kRtap + 8 * kk, al = ah + Kr / 2;
+                                    umma::mma_f16_ts(d, ah, bh, idr2, kk > 0 ? 1u : 0u);
                                     umma::mma_f16_ts(d, al, bh, idr, 1u);
                                 }
                             }
                             umma::mma_commit(&iempty[islot]);  // the image chunk is free once these MMAs complete
-                            if (kc == 1) umma::mma_commit(&rfull[rb]);
+                            if (kc == 1) umma::mma_commit(&rfull);
                         }
                         __syncwarp();
                         if (++islot == kISlots) {
@@ -276,18 +278,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             it.decode(a);
             const BankUJob& jb = a.jobs[it.job];
             if (it.job != cur) {
-                // row taps: M row m, K column k -> t = k - 32 - xl: (kr[|t|], sgn(t) ki[|t|]) 2^rexp
+                // row taps: M row m, K column k -> t = k - JPC - xl: (kr[|t|], sgn(t) ki[|t|]) 2^rexp
                 const float2* w = a.weights + jb.rofs;
                 const float wsc = pow2f(jb.rexp);
                 inv_r = pow2f(-jb.rexp);
-                for (int c = 0; c < kKr / 2; c += 16) {
+                for (int c = 0; c < Kr / 2; c += 16) {
                     uint32_t hi[16], lo[16];
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
                         float v[2];
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
-                            const int tt = 2 * (c + q) + e - kJr - xl;
+                            const int tt = 2 * (c + q) + e - JPC - xl;
                             const int at = tt < 0 ? -tt : tt;
                             float x = 0.f;
                             if (at <= a.h) {
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         umma::split_f16x2(v[0], v[1], hi[q], lo[q]);
                     }
                     umma::tmem_st16(tb + kRtap + lane_addr + c, hi);
-                    umma::tmem_st16(tb + kRtap + kKr / 2 + lane_addr + c, lo);
+                    umma::tmem_st16(tb + kRtap + Kr / 2 + lane_addr + c, lo);
                 }
                 umma::tmem_st_wait();
                 umma::fence_before();
@@ -308,16 +310,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int nb = tiles_of(it.chunk) + 2;
             for (int j = 0; j < nb; ++j, ++gb) {
-                const uint32_t rb = gb & 1u;
-                mbar_wait(&rfull[rb], (gb >> 1) & 1u);
+                mbar_wait(&rfull, gb & 1u);
                 umma::fence_after();
-                uint32_t v[2][32];
+                uint32_t v[2][32];  // J 2^(e + rexp) = Wh Fh + Wl Fh (columns 0-63) + Wh Fl (columns 64-127)
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
-                    umma::tmem_ld16x256b_x8(tb + kDrow + rb * kT + ((uint32_t)(32 * quad + 16 * hh) << 16), v[hh]);
-                umma::tmem_ld_wait();
+                for (int hh = 0; hh < 2; ++hh) {
+                    uint32_t w2[32];
+                    const uint32_t ta = tb + kDrow + ((uint32_t)(32 * quad + 16 * hh) << 16);
+                    umma::tmem_ld16x256b_x8(ta, v[hh]);
+                    umma::tmem_ld16x256b_x8(ta + kT, w2);
+                    umma::tmem_ld_wait();
+#pragma unroll
+                    for (int q = 0; q < 32; ++q)
+                        v[hh][q] = __float_as_uint(__uint_as_float(v[hh][q]) + __uint_as_float(w2[q]));
+                }
                 umma::fence_before();
-                umma::mbar_arrive(&rempty[rb]);
+                umma::mbar_arrive(&rempty);
                 const uint32_t slot = gb % kJSlots;
                 mbar_wait(&jempty[slot], ((gb / kJSlots) & 1u) ^ 1u);
                 if (!(a.dbg & 8)) {
@@ -350,7 +358,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = (uint32_t)(32 * quad) << 16;
         const int r = 8 * (m >> 4) + (m & 7), odd = (m >> 3) & 1;
         const int fr = lane >> 2, fc = lane & 3;
-        uint32_t gt = 0;  // tiles
+        uint8_t* ostg = ostg_all + warp * kStgBytes;
+        uint32_t gt = 0, nst = 0;  // tiles, staged passes
         int cur = -1, cexp = 0;
         for (UnitIt it{(int)blockIdx.x}; it.u < nunits; it.u += gridDim.x) {
             it.decode(a);
@@ -387,11 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const float inv = pow2f(-(jscale_exp(a.maxbits[it.b]) + cexp));
             const int nout = jb.nout;
-            const int xb = it.strip * kT + 32 * half;  // first complex column of this warp's half
-            float2* dst0 = a.dst_base + jb.dst_off[0] + (int64_t)it.b * a.dst_bstride + xb + fc;
-            float2* dst1 = a.dst_base + (nout > 1 ? jb.dst_off[1] : jb.dst_off[0]) + (int64_t)it.b * a.dst_bstride + xb + fc;
+            const int xf = 2 * (it.strip * kT + 32 * half);  // first float column of this warp's half
+            const int plane0 = (int)((jb.dst_off[0] + (int64_t)it.b * a.dst_bstride) / a.hw);
+            const int plane1 = (int)((jb.dst_off[nout > 1 ? 1 : 0] + (int64_t)it.b * a.dst_bstride) / a.hw);
             const int y0 = it.chunk * chunk_rows, nt = tiles_of(it.chunk);
-            const int kmax = a.dbg & 1 ? 0 : min(8, (a.W - xb + 3) >> 2);  // 4-column groups inside the image
             for (int i = 0; i < nt; ++i, ++gt) {
                 mbar_wait(&cfull, gt & 1u);
                 umma::fence_after();
@@ -402,22 +410,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma::tmem_ld_wait();
                 umma::fence_before();
                 umma::mbar_arrive(&cempty);
+                const int ybase = y0 + i * kT + 16 * quad;  // output row of the warp's 16-row box
+                // four passes (16-column half qq x output o), each one [16 rows][128 B] box through one of the
+                // warp's two staging buffers: 8 conflict-free STS.64 per thread, one TMA store (which also
+                // clips the image edges); the LSU sees 2 wavefronts per 256 bytes instead of 8
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const int orow = y0 + i * kT + 16 * quad + 8 * hh + fr;
-                    if (orow >= a.H) continue;
-                    const int64_t o = (int64_t)orow * a.W;
+                for (int ps = 0; ps < 4; ++ps) {
+                    const int qq = ps >> 1, o = ps & 1;
+                    if (o == 1 && nout < 2) continue;
+                    uint8_t* sb = ostg + 2048 * (nst & 1u);  // buffers alternate over the passes actually stored
+                    ++nst;
+                    if (lane == 0) umma::bulk_wait_read<1>();  // the store that last read this buffer is done
+                    __syncwarp();
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        if (k >= kmax) break;
-                        const float ar = __uint_as_float(v[hh][4 * k]), ai = __uint_as_float(v[hh][4 * k + 1]);
-                        const float br = __uint_as_float(v[hh][4 * k + 2]), bi = __uint_as_float(v[hh][4 * k + 3]);
-                        st_cs2(dst0 + o + 4 * k, (ar + bi) * inv, (ai - br) * inv);
-                        if (nout > 1) st_cs2(dst1 + o + 4 * k, (ar - bi) * inv, -(ai + br) * inv);
+                    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                        for (int kq = 0; kq < 4; ++kq) {
+                            const int k = 4 * qq + kq;
+                            const float ar = __uint_as_float(v[hh][4 * k]), ai = __uint_as_float(v[hh][4 * k + 1]);
+                            const float br = __uint_as_float(v[hh][4 * k + 2]), bi = __uint_as_float(v[hh][4 * k + 3]);
+                            const float2 f = o == 0 ? make_float2((ar + bi) * inv, (ai - br) * inv)
+                                                    : make_float2((ar - bi) * inv, -(ai + br) * inv);
+                            const int rb = 8 * hh + fr;
+                            *reinterpret_cast<float2*>(sb + rb * 128 + (((2 * kq + (fc >> 1)) ^ (rb & 7)) << 4) + 8 * (fc & 1)) = f;
+                        }
+                    umma::fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (!(a.dbg & 1)) umma::tma_store_3d(&omap, xf + 32 * qq, ybase, o == 0 ? plane0 : plane1, sb);
+                        umma::bulk_commit();
                     }
                 }
             }
         }
+        if (lane == 0) umma::bulk_wait_read<0>();  // staging reads done before the CTA exits
     }
     umma::fence_before();
     __syncthreads();
@@ -466,6 +492,22 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
         std::fprintf(stderr, "bank_umma: tensor map encode failed (Wp %d Hq %d)\n", Wp, Hq);
         return cudaErrorInvalidValue;
     }
+    // outputs: [plane][H][W] complex64 from dst_base, stored by TMA from the swizzled staging
+    a.hw = (int64_t)a.H * a.W;
+    CUtensorMap omap;
+    {
+        cuuint64_t od[3] = {(cuuint64_t)2 * a.W, (cuuint64_t)a.H, (cuuint64_t)a.dst_planes};
+        cuuint64_t os[2] = {(cuuint64_t)a.W * 8, (cuuint64_t)a.hw * 8};
+        cuuint32_t ob[3] = {32, 16, 1};
+        if (a.dst_planes < 1 || (reinterpret_cast<uintptr_t>(a.dst_base) & 15) ||
+            enc(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.dst_base, od, os, ob, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+                CUDA_SUCCESS) {
+            std::fprintf(stderr, "bank_umma: output tensor map encode failed (W %d H %d planes %lld)\n", a.W, a.H,
+                         (long long)a.dst_planes);
+            return cudaErrorInvalidValue;
+        }
+    }
     a.nstrips = (a.W + kT - 1) / kT;
     const int ntiles = (a.H + kT - 1) / kT;
     const int64_t basen = (int64_t)a.nstrips * a.batch * a.njobs;
@@ -484,9 +526,9 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
         attr = true;
     }
     if (a.jpc == 16)
-        bank_umma_kernel<16><<<grid, kThreads, kSmem, s>>>(map, a);
+        bank_umma_kernel<16><<<grid, kThreads, kSmem, s>>>(map, omap, a);
     else
-        bank_umma_kernel<32><<<grid, kThreads, kSmem, s>>>(map, a);
+        bank_umma_kernel<32><<<grid, kThreads, kSmem, s>>>(map, omap, a);
     return cudaGetLastError();
 }
 

@@ -1756,6 +1756,7 @@ static int32_t execute(Plan<T>& p, Ctx& cx, const fgb_image& im, const void* img
                         a.njobs = st.njobs;
                         a.batch = nb;
                         a.xbuf = p.xbuf;
+                        a.dst_planes = (int64_t)nb * bsC(st.dst) / ((int64_t)st.H * st.W);
                         FGB_CUDA(launch_bank_umma(a, cx.fprep.p, cx.sms, s));
                     }
                     break;

@@ -151,6 +151,8 @@ struct BankUArgs {
     int H, W, h, njobs, batch, xbuf;
     int jpc, Kc, nstrips, nchunks, ch_tiles;  // set by the launcher
     int dbg;                                  // FGB_UMMA_DBG (ablation only)
+    int64_t hw;                               // H * W (set by the launcher): output planes are [plane][H][W] complex
+    int64_t dst_planes;                       // planes reachable from dst_base (the TMA store map spans them)
 };
 bool bank_umma_supported(int h, int W);
 cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream_t s);
