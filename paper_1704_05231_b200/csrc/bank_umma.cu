@@ -1,5 +1,5 @@
 // K5u: one frequency of the fp32 Gabor bank -- row AND column passes -- in one
-// tensor-core kernel, J kept in shared memory (half-widths h <= 32).
+// tensor-core kernel, J kept in shared memory (half-widths h <= 48).
 //
 // Reference semantics: horizontal_stage -> vertical_stage(_conjugate)
 // (gabor.py:107-169, bank.py:68-74) for every direct orientation of one
@@ -29,7 +29,10 @@
 // an epilogue.
 // TMEM: D_col [0, 128), D_row [128, 256) (Wh Fh + Wl Fh | Wh Fl), row taps hi / lo
 // [256, 256 + K_r), column taps hi / lo [384, 384 + K_c); K_r = K_c = 64 + 2 JPC,
-// JPC = h rounded up to 16 (a template parameter: 16 or 32).  Work unit = (direct, image, row
+// JPC = h rounded up to 16 (a template parameter: 16, 32 or 48).  JPC = 48 (sigma
+// = 16 at radius 3: 320 tap columns) keeps a 64-column D_row and 3 MMAs per row
+// K step: D_col [0, 128), D_row [128, 192), row taps [192, 352), column taps
+// [352, 512) -- the 512 TMEM columns exactly.  Work unit = (direct, image, row
 // chunk, 64-column strip), strips fastest; taps rebuilt when the direct changes.
 #include <algorithm>
 #include <cstdio>
@@ -52,8 +55,8 @@ constexpr int kColWarps = 8, kRowWarps = 4;
 constexpr int kRowW0 = kColWarps, kTmaWarp = kColWarps + kRowWarps, kMmaWarp = kTmaWarp + 1;
 constexpr int kThreads = 32 * (kMmaWarp + 1);
 constexpr int kColThreads = 32 * kColWarps, kRowThreads = 32 * kRowWarps;
-constexpr int kJr = 32;             // largest row / column tap padding (h <= 32); K_r = 64 + 2 JPC
-constexpr uint32_t kDcol = 0, kDrow = 128, kRtap = 256, kCtap = 384;
+constexpr int kJr = 48;             // largest row / column tap padding (h <= 48); K_r = K_c = 64 + 2 JPC
+constexpr uint32_t kDcol = 0, kDrow = 128;  // the tap columns follow D_row (see the kernel)
 constexpr int kStgBytes = 4096;      // per column-epilogue warp: 2 buffers x [16 rows][128 B] (128-byte swizzle, TMA stores)
 constexpr int kSmem = kJSlots * kJBytes + kISlots * kIBytes + kColWarps * kStgBytes + 1024;
 
@@ -85,7 +88,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int Kc = kT + 2 * JPC, jpc = JPC;
-    constexpr int Kr = kT + 2 * JPC;  // row K: the second image chunk contributes Kr / 16 - 4 K steps
+    constexpr int Kr = kT + 2 * JPC;     // row K: the last image chunk contributes Kr / 16 - 4 (NCH - 1) K steps
+    constexpr int NCH = (Kr + 63) / 64;  // 64-column image chunks per row block
+    // JPC <= 32: D_row holds [Wh Fh + Wl Fh | Wh Fl] (128 columns, 2 MMAs per K step); JPC = 48: the taps need
+    // 320 columns, so D_row is 64 columns and the row pass issues the 3 N = 64 MMAs per K step
+    constexpr bool kWideRow = JPC <= 32;
+    constexpr uint32_t kRtap = kDrow + (kWideRow ? 128 : 64), kCtap = kRtap + (kWideRow ? 128 : Kr);
+    static_assert(kCtap + Kc <= 512, "TMEM budget");
     if (threadIdx.x == 0) {
         for (int s = 0; s < kISlots; ++s) {
             mbar_init(&ifull[s], 1);
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int y0 = it.chunk * chunk_rows, nb = tiles_of(it.chunk) + 2;
                 const int xs = it.strip * kT - JPC + a.xbuf;
                 for (int j = 0; j < nb; ++j)
-                    for (int kc = 0; kc < 2; ++kc, ++g) {
+                    for (int kc = 0; kc < NCH; ++kc, ++g) {
                         const uint32_t slot = g % kISlots;
                         mbar_wait(&iempty[slot], ((g / kISlots) & 1u) ^ 1u);
                         uint8_t* sp = iring + slot * kIBytes;
@@ -217,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma::fence_after();
                     const uint32_t d = tb + kDrow;
 #pragma unroll
-                    for (int kc = 0; kc < 2; ++kc) {
+                    for (int kc = 0; kc < NCH; ++kc) {
                         mbar_wait(&ifull[islot], iphase);
                         umma::fence_after();
                         const uint64_t bh0 = idesc0 + (uint64_t)(islot * (kIBytes >> 4));
@@ -230,12 +239,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     // K-major, 128-byte swizzle: K step = 32 bytes inside the swizzle atom
                                     const uint64_t bh = bh0 + (uint64_t)(2 * q);
                                     const uint32_t ah = tb + kRtap + 8 * kk, al = ah + Kr / 2;
-                                    umma::mma_f16_ts(d, ah, bh, idr2, kk > 0 ? 1u : 0u);
-                                    umma::mma_f16_ts(d, al, bh, idr, 1u);
+                                    if constexpr (kWideRow) {
+                                        umma::mma_f16_ts(d, ah, bh, idr2, kk > 0 ? 1u : 0u);
+                                        umma::mma_f16_ts(d, al, bh, idr, 1u);
+                                    } else {
+                                        umma::mma_f16_ts(d, ah, bh, idr, kk > 0 ? 1u : 0u);
+                                        umma::mma_f16_ts(d, ah, bh + (uint64_t)(kIBytes >> 5), idr, 1u);
+                                        umma::mma_f16_ts(d, al, bh, idr, 1u);
+                                    }
                                 }
                             }
                             umma::mma_commit(&iempty[islot]);  // the image chunk is free once these MMAs complete
-                            if (kc == 1) umma::mma_commit(&rfull);
+                            if (kc == NCH - 1) umma::mma_commit(&rfull);
                         }
                         __syncwarp();
                         if (++islot == kISlots) {
@@ -315,15 +330,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t v[2][32];  // J 2^(e + rexp) = Wh Fh + Wl Fh (columns 0-63) + Wh Fl (columns 64-127)
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                    uint32_t w2[32];
                     const uint32_t ta = tb + kDrow + ((uint32_t)(32 * quad + 16 * hh) << 16);
                     umma::tmem_ld16x256b_x8(ta, v[hh]);
-                    umma::tmem_ld16x256b_x8(ta + kT, w2);
-                    umma::tmem_ld_wait();
+                    if constexpr (kWideRow) {
+                        uint32_t w2[32];
+                        umma::tmem_ld16x256b_x8(ta + kT, w2);
+                        umma::tmem_ld_wait();
 #pragma unroll
-                    for (int q = 0; q < 32; ++q)
-                        v[hh][q] = __float_as_uint(__uint_as_float(v[hh][q]) + __uint_as_float(w2[q]));
+                        for (int q = 0; q < 32; ++q)
+                            v[hh][q] = __float_as_uint(__uint_as_float(v[hh][q]) + __uint_as_float(w2[q]));
+                    }
                 }
+                if constexpr (!kWideRow) umma::tmem_ld_wait();
                 umma::fence_before();
                 umma::mbar_arrive(&rempty);
                 const uint32_t slot = gb % kJSlots;
@@ -479,7 +497,7 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
     a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no image loads, 8 no J conversion)
     a.jpc = (a.h + 15) / 16 * 16;
     a.Kc = kT + 2 * a.jpc;
-    if (a.h > kJr || a.xbuf < kJr || a.Kc > 128) return cudaErrorInvalidValue;
+    if (a.h > kJr || a.xbuf < a.jpc || a.Kc > kT + 2 * kJr) return cudaErrorInvalidValue;
     const int Wp = a.W + 2 * a.xbuf, Hq = a.H + 2 * kBankUPadRows;
     CUtensorMap map;
     cuuint64_t dims[3] = {(cuuint64_t)Wp, (cuuint64_t)Hq, (cuuint64_t)2 * a.batch};
@@ -522,13 +540,17 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
         cudaError_t e = cudaFuncSetAttribute(bank_umma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(bank_umma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(bank_umma_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     if (a.jpc == 16)
         bank_umma_kernel<16><<<grid, kThreads, kSmem, s>>>(map, omap, a);
-    else
+    else if (a.jpc == 32)
         bank_umma_kernel<32><<<grid, kThreads, kSmem, s>>>(map, omap, a);
+    else
+        bank_umma_kernel<48><<<grid, kThreads, kSmem, s>>>(map, omap, a);
     return cudaGetLastError();
 }
 

@@ -709,11 +709,14 @@ static bool umma_freq_used(int h, int nj, int H, int W) {
 }
 
 // Row + column passes of one frequency in one tensor-core kernel, J in shared memory
-// (bank_umma.cu; h <= 32).  FGB_BANK_UMMA=0 keeps the separate passes.
+// (bank_umma.cu; h <= 48).  Where the plan gives it enough tiles per SM it also takes the small
+// half-widths of the FFMA fused kernel (config 5 sigma = 2: one 2.3 ms launch instead of two 1.5 ms
+// ones, step +2.3 %).  FGB_BANK_UMMA=0 keeps the separate passes.
 static bool banku_used(int h, int nj, int H, int W) {
     static const bool off = std::getenv("FGB_BANK_UMMA") && std::atoi(std::getenv("FGB_BANK_UMMA")) == 0;
     static const bool coloff = std::getenv("FGB_COL_FFMA") != nullptr;
-    return !off && !coloff && H >= 16 && bank_umma_supported(h, W) && !fused_bank_used(h, nj, H, W);
+    (void)nj;
+    return !off && !coloff && H >= 16 && bank_umma_supported(h, W);
 }
 
 // One frequency worth of Gabor work: row stage for `jobs`, column stage with
@@ -745,7 +748,7 @@ static int32_t build_gabor_freq(Builder<T>& b, const fgb_smoother& sm, double si
             // fused launch each: config 5's sigma = 2 frequency 2.5 ms instead of 3.4 ms for the
             // row + column launches (profiles/r02/unit_costs_c5.json).
             const int ng = (nj + 4) / 5;
-            if (!box && !row_only && !col_only && fused_bank_used(h, nj, H, W)) {
+            if (!box && !row_only && !col_only && fused_bank_used(h, nj, H, W) && !b.p.banku_h.count(h)) {
                 for (int gi = 0; gi < ng; ++gi) {
                     const int g0 = gi * nj / ng, g1 = (gi + 1) * nj / ng, gn = g1 - g0;
                     Step<T> st;
@@ -1103,7 +1106,7 @@ static int32_t build_bank(Plan<T>& p, const fgb_bank_desc& d) {
             if (banku_used(h, (int)per_f[i].size(), H, W) && (force || tiles >= 16 * 148)) {
                 p.banku = true;
                 p.banku_h.insert(h);
-                p.xbuf = std::max(p.xbuf, 32);
+                p.xbuf = std::max(p.xbuf, h > 32 ? 64 : 32);
             } else if (umma_freq_used(h, (int)per_f[i].size(), H, W)) {
                 p.jbuf = std::max(p.jbuf, col_umma_jpad(h));
             }

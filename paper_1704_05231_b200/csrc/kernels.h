@@ -134,7 +134,7 @@ cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstrid
 cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t s);
 // ---- K5u: row + column passes of one frequency in one tensor-core kernel (bank_umma.cu) ----
 // J stays in shared memory.  Reads the prep planes of launch_row_umma_prep (x-padded by xbuf
-// >= 32 columns, y-padded by kBankUPadRows replicate rows); h <= 32.
+// >= h rounded up to 16 columns, y-padded by kBankUPadRows replicate rows); h <= 48.
 constexpr int kBankUPadRows = 64;
 struct BankUJob {
     int32_t rofs, cofs;         // row taps (kr, ki) t = 0..h / column taps (ka, kb) t = -h..h in `weights`

@@ -130,7 +130,8 @@ def test_fused_tensor_core_bank_on_small_images():
         "from tests.conftest import random_image;"
         "cases = [(64, 64, 4, [math.pi / 4], [4.0]), (131, 200, 8, [math.pi / 4, math.pi / 8], [4.0, 8.0]),"
         " (333, 320, 8, [math.pi / 8, math.pi / 3], [8.0, 10.0]), (97, 136, 6, [1.3, 0.4], [5.0, 7.0]),"
-        " (260, 264, 16, [math.pi / 16], [3.0])];"
+        " (260, 264, 16, [math.pi / 16], [3.0]), (200, 328, 8, [math.pi / 16, math.pi / 32], [16.0, 32.0]),"
+        " (131, 72, 5, [0.2], [14.5])];"
         "errs = [bank_err(fg, random_image(H * 7 + W, H, 0.0, 1.0, width=W), N, fr, sg) for H, W, N, fr, sg in cases];"
         "print(errs); assert max(errs) <= 1e-5"
     )
