@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (o == 1 && nout < 2) continue;
                     uint8_t* sb = ostg + 2048 * (nst & 1u);  // buffers alternate over the passes actually stored
                     ++nst;
-                    if (lane == 0) umma::bulk_wait_read<1>();  // the store that last read this buffer is done
+                    if (lane == 0 && !(a.dbg & 32)) umma::bulk_wait_read<1>();  // the store that last read this buffer is done (32: A/B knob)
                     __syncwarp();
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh)

@@ -119,10 +119,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- TMA producer ----------------
         if (lane == 0) {
             uint32_t g = 0;
+            bool run = false;
             for (UnitIter it(a, nunits); it.ok(); it.next(a)) {
                 const int b = it.b, yb = it.yb, strip = it.strip;
                 const int xs = strip * kTX - a.jpad + a.xbuf;  // padded-plane column of K column 0
-                for (int q = 0; q < kst; ++q, ++g) {
+                // consecutive strips of a row block share all but one 64-column stage: the window slides,
+                // only the new stage is loaded (K / 64 times less TMA and L2 traffic than a fresh window)
+                const int q0 = (run && strip > 0) ? kst - 1 : 0;
+                run = true;
+                for (int q = q0; q < kst; ++q, ++g) {
                     const uint32_t slot = g % (uint32_t)kStages, round = g / (uint32_t)kStages;
                     mbar_wait(&empty[slot], (round & 1u) ^ 1u);
                     uint8_t* sp = ring + slot * kStageBytes;
@@ -143,10 +148,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t idesc = umma::idesc_f16_f32(128, kTY, false, false);
             const uint64_t rdesc0 = umma::smem_desc(smem_u32(ring), 16, 1024, umma::kLayoutSw128);
             const bool do_mma = !(a.dbg & 2);  // A/B knob: no MMAs
-            uint32_t g = 0, t = 0, nreload = 0;
+            uint32_t gw = 0, gnext = 0, t = 0, nreload = 0;  // first ring stage of the tile's window; stages issued
+            bool run = false;
             int cur = -1;
             for (UnitIter it(a, nunits); it.ok(); it.next(a), ++t) {
                 const int job = it.job;
+                if (run && it.strip > 0) {
+                    ++gw;
+                    ++gnext;
+                } else {
+                    gw = gnext;
+                    gnext += kst;
+                }
+                run = true;
                 if (job != cur) {
                     mbar_wait(&aready, nreload & 1u);
                     ++nreload;
@@ -160,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // one elect region per ring stage (12 MMAs), descriptors advance by constants (K is a
                 // multiple of 64): the issuing warp stays well under the MMAs' execution time
                 for (int st = 0; st < kst; ++st) {
-                    const uint32_t gs = g + st;
+                    const uint32_t gs = gw + st;
                     const uint32_t slot = gs % (uint32_t)kStages;
                     mbar_wait(&full[slot], (gs / (uint32_t)kStages) & 1u);
                     umma::fence_after();
@@ -180,7 +194,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (umma::elect_one()) umma::mma_commit(&tfull[buf]);
                 __syncwarp();
-                g += kst;
             }
         }
         __syncwarp();
@@ -192,7 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int xl = m >> 1, im = m & 1;
         float* stg = reinterpret_cast<float*>(ring + kStages * kStageBytes) + warp * 32 * kStgPitch;
         int cur = -1;
-        uint32_t t = 0;
+        uint32_t t = 0, gw = 0, gnext = 0;
+        bool run = false;
         float inv_w = 1.f;
         const int H = a.H, W = a.W, jbuf = a.jbuf;
         const int64_t hpw = a.hpw;
@@ -241,8 +255,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t buf = t % nacc, ph = (t / nacc) & 1u;
             mbar_wait(&tfull[buf], ph);
             umma::fence_after();
-            if (threadIdx.x == 0)  // the tile's MMAs are done: its ring stages are free (no per-stage commits)
-                for (int q = 0; q < kst; ++q) umma::mbar_arrive(&empty[(t * kst + q) % (uint32_t)kStages]);
+            if (run && strip > 0) {
+                ++gw;
+                ++gnext;
+            } else {
+                gw = gnext;
+                gnext += kst;
+            }
+            run = true;
+            if (threadIdx.x == 0) {
+                // the tile's MMAs are done (no per-stage commits): the window's oldest stage is free; all of
+                // them when the next unit does not continue this run of strips
+                const bool cont = it.u + 1 < it.u1 && strip + 1 < a.nstrips;
+                const int nrel = cont ? 1 : kst;
+                for (int q = 0; q < nrel; ++q) umma::mbar_arrive(&empty[(gw + q) % (uint32_t)kStages]);
+            }
             float v[64];  // both 32-row passes of this warp's 64 image rows, one TMEM wait
 #pragma unroll
             for (int j = 0; j < 4; ++j)
