@@ -479,8 +479,13 @@ def roofline(args, cfg, prof, nprof, fp32, hbm):
                 "algorithmic_bytes_per_launch": top["bytes"] / top["launches"],
                 "ref_flops_tflops": top["flops"] / (top["ms"] * 1e-3) / 1e12,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                "note": "algorithmic bytes = complex64 J planes read once (split-fp16 hi+lo, 8 B per px) + complex64 "
-                        "outputs written once; ref_flops_tflops = the reference OpCounters flops of the stage / time"}
+                "note": {"bank_umma": "algorithmic bytes = the image read once + complex64 outputs written once "
+                                      "(row + column passes of a frequency in one kernel, J in shared memory)",
+                         "row_umma": "algorithmic bytes = the image read once + split-fp16 J planes written once "
+                                     "(8 B per px and direct)"}.get(
+                    top["name"], "algorithmic bytes = J planes read once (split-fp16 hi+lo, 8 B per px) + complex64 "
+                                 "outputs written once")
+                + "; ref_flops_tflops = the reference OpCounters flops of the stage / time"}
     if cfg["kind"] == "sdft":
         ach = top["bytes"] / (top["ms"] * 1e-3) / 1e9
         return {"bound": "hbm", "kernel": top["name"], "ncu_fma_pipe_pct": fma, "achieved": ach, "peak": hbm, "unit": "GB/s",
