@@ -32,8 +32,9 @@
 // JPC = h rounded up to 16 (a template parameter: 16, 32 or 48).  JPC = 48 (sigma
 // = 16 at radius 3: 320 tap columns) keeps a 64-column D_row and 3 MMAs per row
 // K step: D_col [0, 128), D_row [128, 192), row taps [192, 352), column taps
-// [352, 512) -- the 512 TMEM columns exactly.  Work unit = (direct, image, row
-// chunk, 64-column strip), strips fastest; taps rebuilt when the direct changes.
+// [352, 512) -- the 512 TMEM columns exactly.
+// Work unit = (direct, 64-column strip, row chunk, image), directs fastest: the directs of a strip run at
+// the same time on neighbouring CTAs and share their image reads in L2; taps are rebuilt per unit.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -65,8 +66,18 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max
 struct UnitIt {
     int u, job, b, chunk, strip;
     __device__ void decode(const BankUArgs& a) {
-        strip = u % a.nstrips;
-        int r = u / a.nstrips;
+        int r = u;
+        if (a.job_fastest) {  // the directs of one (strip, chunk) run at the same time on neighbouring CTAs:
+            job = r % a.njobs;  // their image reads hit L2; the taps are rebuilt per unit
+            r /= a.njobs;
+            strip = r % a.nstrips;
+            r /= a.nstrips;
+            chunk = r % a.nchunks;
+            b = r / a.nchunks;
+            return;
+        }
+        strip = r % a.nstrips;
+        r /= a.nstrips;
         chunk = r % a.nchunks;
         r /= a.nchunks;
         b = r % a.batch;
@@ -494,6 +505,10 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     static const int dbg = std::getenv("FGB_UMMA_DBG") ? std::atoi(std::getenv("FGB_UMMA_DBG")) : 0;
+    // unit order: directs fastest by default (config 5: DRAM reads per launch 2.5 -> 0.5 GB, launch -4 %);
+    // FGB_BANKU_ORDER=0 restores strips fastest (taps rebuilt only when a CTA's direct changes)
+    static const int order = std::getenv("FGB_BANKU_ORDER") ? std::atoi(std::getenv("FGB_BANKU_ORDER")) : 1;
+    a.job_fastest = order;
     a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no image loads, 8 no J conversion)
     a.jpc = (a.h + 15) / 16 * 16;
     a.Kc = kT + 2 * a.jpc;

@@ -151,6 +151,7 @@ struct BankUArgs {
     int H, W, h, njobs, batch, xbuf;
     int jpc, Kc, nstrips, nchunks, ch_tiles;  // set by the launcher
     int dbg;                                  // FGB_UMMA_DBG (ablation only)
+    int job_fastest;                          // unit order: directs fastest (FGB_BANKU_ORDER)
     int64_t hw;                               // H * W (set by the launcher): output planes are [plane][H][W] complex
     int64_t dst_planes;                       // planes reachable from dst_base (the TMA store map spans them)
 };
