@@ -34,8 +34,8 @@ namespace {
 // ---- device-time model, parallel.py:_FIT / run_cost (profiles/r02/unit_costs_c5.json) ----
 // cost = A(h) + B1(h) single + B2(h) double (ms on an 8192^2 image), linear in h between the anchors
 constexpr double kMpx = 67.108864;
-constexpr double kFit[5][4] = {{6, 0.1395, 0.2506, 0.2729}, {12, 0.0, 0.2774, 0.3352}, {24, 0.0413, 0.2827, 0.3382},
-                               {48, 0.0224, 0.3902, 0.5254}, {96, 0.0448, 0.5814, 0.6067}};
+constexpr double kFit[5][4] = {{6, 0.0512, 0.1869, 0.2564}, {12, 0.0203, 0.2141, 0.2848}, {24, 0.0613, 0.2159, 0.2791},
+                                {48, 0.0744, 0.29, 0.3393}, {96, 0.2301, 0.4381, 0.5623}};
 
 double run_cost(double sigma, const std::vector<int>& ks, int n, double radius) {
     if (ks.empty()) return 0.0;

@@ -38,13 +38,13 @@ def shard_images(n_images: int, world: int) -> list[list[int]]:
 # h = ceil(r sigma), computing g directs of which `single` have one output (theta = 0, pi/2)
 # and `double` two (theta, pi - theta):
 #     cost = A(h) + B1(h) * single + B2(h) * double          (ms on the fit's 8192^2 image)
-# with (A, B1, B2) interpolated linearly in h between the fitted half-widths: h = 6 the fused
-# FFMA kernel (bank_fused.cu), h = 12 / 24 the fused tensor-core kernel (bank_umma.cu), h = 48 /
-# 96 the tensor-core row + column passes (row_umma.cu, col_umma.cu).  Max error of the fit
-# over the 225 measured ranges: 14 %.  mgpu.cu restates it (same anchors, same order).
+# with (A, B1, B2) interpolated linearly in h between the fitted half-widths: h = 6 / 12 / 24 / 48 the
+# fused tensor-core kernel (bank_umma.cu), h = 96 the tensor-core row + column passes (row_umma.cu,
+# col_umma.cu).  Fitted by tools/fit_unit_costs.py; max error over the 225 measured ranges: 21 %.
+# mgpu.cu restates it (same anchors, same order).
 _MPX = 67.108864  # the fit's 8192^2 image
-_FIT = ((6, 0.1395, 0.2506, 0.2729), (12, 0.0, 0.2774, 0.3352), (24, 0.0413, 0.2827, 0.3382),
-        (48, 0.0224, 0.3902, 0.5254), (96, 0.0448, 0.5814, 0.6067))
+_FIT = ((6, 0.0512, 0.1869, 0.2564), (12, 0.0203, 0.2141, 0.2848), (24, 0.0613, 0.2159, 0.2791),
+        (48, 0.0744, 0.29, 0.3393), (96, 0.2301, 0.4381, 0.5623))
 
 
 def _fit_at(h: int) -> tuple[float, float, float]:

@@ -40,7 +40,7 @@ def test_partition_units_config5():
     freqs = [math.pi / 2 ** j for j in range(1, 6)]
     sig = [2.0 ** j for j in range(1, 6)]
     total = P.partition_cost([list(range(45))], sig, 16)[0]
-    assert abs(total * 67.108864 - 18.5) < 1.5  # the measured config-5 step (profiles/r02/bench_c5.json)
+    assert abs(total * 67.108864 - 15.3) < 1.5  # the measured config-5 kernel time (profiles/r02/bench_c5.json)
     for world, eff in ((1, 1.0), (2, 0.98), (4, 0.97), (8, 0.93)):
         parts = P.partition_units(freqs, sig, 16, world)
         assert sorted(u for p in parts for u in p) == list(range(45))
@@ -54,8 +54,8 @@ def test_partition_units_config5():
 def test_run_cost_model_matches_measurements():
     """A few measured B200 points of profiles/r02/unit_costs_c5.json (kernel ms, 8192^2)."""
     mpx = 67.108864
-    for sigma, ks, ms in ((32.0, range(9), 5.603), (16.0, range(9), 4.451), (8.0, [3], 0.413), (4.0, range(5), 1.492),
-                          (8.0, range(9), 3.126), (16.0, [0], 0.427)):
+    for sigma, ks, ms in ((32.0, range(9), 4.908), (16.0, range(9), 2.961), (8.0, [3], 0.322), (4.0, range(5), 1.287),
+                          (8.0, range(9), 2.695), (16.0, [0], 0.372), (2.0, range(9), 2.162)):
         got = P.run_cost(sigma, ks, 16, 3.0, mpx)
         assert abs(got - ms) / ms < 0.15, (sigma, list(ks), got, ms)
 
