@@ -505,10 +505,6 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     static const int dbg = std::getenv("FGB_UMMA_DBG") ? std::atoi(std::getenv("FGB_UMMA_DBG")) : 0;
-    // unit order: directs fastest by default (config 5: DRAM reads per launch 2.5 -> 0.5 GB, launch -4 %);
-    // FGB_BANKU_ORDER=0 restores strips fastest (taps rebuilt only when a CTA's direct changes)
-    static const int order = std::getenv("FGB_BANKU_ORDER") ? std::atoi(std::getenv("FGB_BANKU_ORDER")) : 1;
-    a.job_fastest = order;
     a.dbg = dbg;  // A/B ablation (1 no stores, 2 no MMAs, 4 no image loads, 8 no J conversion)
     a.jpc = (a.h + 15) / 16 * 16;
     a.Kc = kT + 2 * a.jpc;
@@ -549,6 +545,11 @@ cudaError_t launch_bank_umma(BankUArgs a, const void* fprep, int sms, cudaStream
     a.ch_tiles = (ntiles + nch - 1) / nch;
     a.nchunks = (ntiles + a.ch_tiles - 1) / a.ch_tiles;
     const int64_t units = basen * a.nchunks;
+    // unit order: directs fastest when the split-fp16 image planes do not fit L2 and the units are long enough
+    // to amortise a tap rebuild per unit (config 5: DRAM reads per launch 2.5 -> 0.05 GB, launch -4 %; config 3's
+    // 8-tile units on L2-resident planes lose 7 % with it); FGB_BANKU_ORDER=0 / 1 forces strips / directs fastest
+    static const char* order = std::getenv("FGB_BANKU_ORDER");
+    a.job_fastest = order ? std::atoi(order) : (a.ch_tiles >= 32 && (int64_t)a.batch * Hq * Wp * 4 > (96LL << 20));
     const int grid = (int)std::min<int64_t>(units, sms);
     static bool attr = false;
     if (!attr) {

@@ -25,7 +25,7 @@
 // M = 128, N = 128, K-major B with 128-byte swizzle), warps 0-7 epilogue
 // (TMEM lane quadrant w % 4 = 16 output columns, column half w / 4 = 64 image
 // rows): TMEM -> shared transpose -> hi / lo split -> row-contiguous stores,
-// the first / last image row also into the jbuf replicate pad rows.  Work
+// (the jbuf replicate pad rows are filled by jpad_fill_kernel afterwards).  Work
 // unit = one tile (direct, image, 128-row block, 64-column strip), strips
 // fastest; the taps of a direct are (re)built in TMEM when it changes.
 #include <algorithm>
@@ -301,14 +301,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t* p = pq + 8 * it * 64;
                         *reinterpret_cast<uint4*>(p) = hw;
                         *reinterpret_cast<uint4*>(p + hpw) = lw;
-                        if (y == 0 || y == H - 1) {  // replicate rows of the column pass's padding
-                            const int r0 = y == 0 ? 0 : H + jbuf, r1 = y == 0 ? jbuf : H + 2 * jbuf;
-                            for (int r = r0; r < r1; ++r) {
-                                uint32_t* q = js + (int64_t)r * 64;
-                                *reinterpret_cast<uint4*>(q) = hw;
-                                *reinterpret_cast<uint4*>(q + hpw) = lw;
-                            }
-                        }
                     }
                 }
             }
@@ -388,6 +380,24 @@ cudaError_t launch_row_umma_prep(const float* img, int64_t pitch, int64_t bstrid
     return cudaGetLastError();
 }
 
+// Replicate rows of the column pass's padding: J plane rows [0, jbuf) = image row 0, rows [H + jbuf,
+// H + 2 jbuf) = image row H - 1, per (job, image, plane, strip).  A separate launch after the row kernel:
+// written from its epilogue by the four lanes that hold an edge row, the 2 x jbuf x 2 stores per edge
+// tile made the CTAs that own a job's first / last row block stragglers (ncu: one SM 2.9 M cycles
+// against 1.98 M on average).  Block = (strip, plane of job and image); thread = (row group, u32 column).
+__global__ void __launch_bounds__(256) jpad_fill_kernel(const __grid_constant__ RowUArgs a) {
+    const int strip = blockIdx.x, plane = blockIdx.y & 1, job = (blockIdx.y >> 1) % a.njobs, b = (blockIdx.y >> 1) / a.njobs;
+    const int Hp = a.H + 2 * a.jbuf;
+    uint32_t* js = reinterpret_cast<uint32_t*>(a.dst_base + a.jobs[job].dst_off[0] + (int64_t)b * a.dst_bstride) +
+                   (int64_t)plane * a.hpw + (int64_t)strip * Hp * 64;
+    const int x = threadIdx.x & 63, rg = threadIdx.x >> 6;
+    const uint32_t top = js[(int64_t)a.jbuf * 64 + x], bot = js[(int64_t)(a.jbuf + a.H - 1) * 64 + x];
+    for (int r = rg; r < a.jbuf; r += 4) {
+        js[(int64_t)r * 64 + x] = top;
+        js[(int64_t)(a.H + a.jbuf + r) * 64 + x] = bot;
+    }
+}
+
 cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t s) {
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
@@ -421,6 +431,7 @@ cudaError_t launch_row_umma(RowUArgs a, const void* fprep, int sms, cudaStream_t
         attr = true;
     }
     row_umma_kernel<<<grid, kThreads, smem, s>>>(map, a);
+    if (a.jbuf > 0 && !(a.dbg & 1)) jpad_fill_kernel<<<dim3(a.nstrips, 2 * a.njobs * a.batch), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 
