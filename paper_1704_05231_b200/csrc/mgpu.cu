@@ -34,8 +34,8 @@ namespace {
 // ---- device-time model, parallel.py:_FIT / run_cost (profiles/r02/unit_costs_c5.json) ----
 // cost = A(h) + B1(h) single + B2(h) double (ms on an 8192^2 image), linear in h between the anchors
 constexpr double kMpx = 67.108864;
-constexpr double kFit[5][4] = {{6, 0.0512, 0.1869, 0.2564}, {12, 0.0203, 0.2141, 0.2848}, {24, 0.0613, 0.2159, 0.2791},
-                                {48, 0.0744, 0.29, 0.3393}, {96, 0.2301, 0.4381, 0.5623}};
+constexpr double kFit[5][4] = {{6, 0.0553, 0.2141, 0.3204}, {12, 0.0329, 0.2401, 0.3043}, {24, 0.0701, 0.2338, 0.2985},
+                                {48, 0.0638, 0.2936, 0.3483}, {96, 0.1561, 0.4585, 0.5044}};
 
 double run_cost(double sigma, const std::vector<int>& ks, int n, double radius) {
     if (ks.empty()) return 0.0;

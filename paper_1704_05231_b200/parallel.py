@@ -40,11 +40,14 @@ def shard_images(n_images: int, world: int) -> list[list[int]]:
 #     cost = A(h) + B1(h) * single + B2(h) * double          (ms on the fit's 8192^2 image)
 # with (A, B1, B2) interpolated linearly in h between the fitted half-widths: h = 6 / 12 / 24 / 48 the
 # fused tensor-core kernel (bank_umma.cu), h = 96 the tensor-core row + column passes (row_umma.cu,
-# col_umma.cu).  Fitted by tools/fit_unit_costs.py; max error over the 225 measured ranges: 21 %.
+# col_umma.cu).  Fitted by tools/fit_unit_costs.py (median error 3 %, 90th percentile 9 %; the ranges measured first, on a cold
+# GPU, sit up to 45 % below the fit); B1 / B2 then raised by 0.066 / 0.034 / 0.031 / 0.016 / 0.015 ms per unit
+# (h = 6 .. 96): what each rank's share, timed as a whole call with a cold L2 in round robin
+# (tools/partition_balance.py), took beyond the sum of its kernel times.
 # mgpu.cu restates it (same anchors, same order).
 _MPX = 67.108864  # the fit's 8192^2 image
-_FIT = ((6, 0.0512, 0.1869, 0.2564), (12, 0.0203, 0.2141, 0.2848), (24, 0.0613, 0.2159, 0.2791),
-        (48, 0.0744, 0.29, 0.3393), (96, 0.2301, 0.4381, 0.5623))
+_FIT = ((6, 0.0553, 0.2141, 0.3204), (12, 0.0329, 0.2401, 0.3043), (24, 0.0701, 0.2338, 0.2985),
+        (48, 0.0638, 0.2936, 0.3483), (96, 0.1561, 0.4585, 0.5044))
 
 
 def _fit_at(h: int) -> tuple[float, float, float]:
