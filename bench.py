@@ -362,6 +362,10 @@ class Dist:
         self.dist = dist
         if world > 1:
             if self.backend == "nccl":
+                if torch.cuda.device_count() < world:
+                    raise SystemExit(f"bench.py --gpus {world}: NCCL needs one GPU per rank and this box shows "
+                                     f"{torch.cuda.device_count()}; FGB_DIST_BACKEND=gloo lets ranks share a GPU "
+                                     "(plumbing check only, not a scaling measurement)")
                 dist.init_process_group("nccl", device_id=dev)
             else:
                 dist.init_process_group(self.backend)
